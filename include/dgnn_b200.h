@@ -1,0 +1,220 @@
+/*
+ * dgnn_b200.h — C ABI of the B200-native ReInc dynamic-GNN training hot path.
+ *
+ * This is the drop-in boundary. The reference is a C++
+ * library (proj/include/dgnn/*.hpp) with no FFI of its own; every entry point
+ * below names the reference interface it replaces (file:line into
+ * /root/reference/proj). Plain pointers and sizes only: device pointers are
+ * fp32 / int32 / int64 HBM buffers, `stream` is a cudaStream_t (NULL = the
+ * library's own stream for sessions, the legacy default stream for ops).
+ *
+ * Error convention: every function returning int returns 0 on success,
+ * 1 = std::invalid_argument (the reference's check()/fail() messages,
+ * inc/common.hpp:36-40), 2 = std::out_of_range (the reference's .at()),
+ * 3 = CUDA / runtime error. dgnn_last_error() returns the message of the last
+ * failure on the calling thread.
+ *
+ * Aggregation kinds follow AggrKind (inc/aggregate.hpp:21): 0 sum, 1 mean,
+ * 2 max, 3 min. Architectures follow Architecture (inc/model.hpp:21):
+ * 0 gcrn_m1, 1 cd_gcn, 2 gcrn_m2, 3 tgcn.
+ */
+#ifndef DGNN_B200_H
+#define DGNN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dgnn_graph dgnn_graph;
+typedef struct dgnn_synth dgnn_synth;
+typedef struct dgnn_session dgnn_session;
+
+const char* dgnn_last_error(void);
+const char* dgnn_version(void);
+/* Number of this library's kernels launched so far (process-wide). */
+int64_t dgnn_launch_count(void);
+int dgnn_synchronize(void* stream);
+
+/* ------------------------------------------------------------------ graph
+ * Replaces dgnn::DynamicGraph / Snapshot / DeltaGraph / extract_delta /
+ * apply_delta / change_ratio (inc/snapshot.hpp:39-119, src/snapshot.cpp:20-154).
+ * Snapshots live in HBM (in-CSR, out-CSR, fp32 features); extract_delta is
+ * evaluated on the device when each snapshot is added. Host input pointers. */
+int dgnn_graph_create(int32_t num_nodes, int32_t feature_dim, void* stream, dgnn_graph** out);
+void dgnn_graph_free(dgnn_graph* g);
+/* Snapshot ctor (src/snapshot.cpp:20-69): edges in any order; duplicates and
+ * out-of-range endpoints are rejected. feats: num_nodes x feature_dim. */
+int dgnn_graph_add_snapshot(dgnn_graph* g, const int32_t* src, const int32_t* dst,
+                            int64_t num_edges, const float* feats);
+/* apply_delta (src/snapshot.cpp:142-154): next = (last \ deletions) U insertions,
+ * feature rows of changed_nodes replaced by changed_feats (n_changed x dim). */
+int dgnn_graph_add_delta(dgnn_graph* g, const int32_t* del_src, const int32_t* del_dst,
+                         int64_t n_del, const int32_t* ins_src, const int32_t* ins_dst,
+                         int64_t n_ins, const int32_t* changed_nodes, int64_t n_changed,
+                         const float* changed_feats);
+int32_t dgnn_graph_length(const dgnn_graph* g);
+int64_t dgnn_graph_num_edges(const dgnn_graph* g, int32_t t);
+/* Device pointers of snapshot t (GraphView, inc/snapshot.hpp:20-35, plus the out-CSR). */
+int dgnn_graph_snapshot(const dgnn_graph* g, int32_t t, const int64_t** in_ptr,
+                        const int32_t** in_src, const int64_t** out_ptr, const int32_t** out_dst,
+                        const float** feats);
+/* DynamicGraph::delta(t) sizes (inc/snapshot.hpp:79-104); n_rows = distinct
+ * destinations, u_minus / u_plus = distinct deletion / insertion sources. */
+int dgnn_graph_delta_sizes(const dgnn_graph* g, int32_t t, int64_t* n_del, int64_t* n_ins,
+                           int64_t* n_changed, int64_t* n_rows, int64_t* u_minus,
+                           int64_t* u_plus);
+/* Host copies of DeltaGraph deletions / insertions (sorted (src,dst)) and
+ * changed_nodes (ascending). */
+int dgnn_graph_delta_copy(const dgnn_graph* g, int32_t t, int32_t* del_src, int32_t* del_dst,
+                          int32_t* ins_src, int32_t* ins_dst, int32_t* changed_nodes);
+/* Device pointers of the delta-SpMM layout: rows[r] destinations, entries
+ * ent[row_ptr[r]..row_ptr[r+1]) = deletions (~src) then insertions (src). */
+int dgnn_graph_delta_layout(const dgnn_graph* g, int32_t t, const int32_t** rows,
+                            const int32_t** row_ptr, const int32_t** ent);
+/* change_ratio(delta(t), snapshot(t-1)) (src/snapshot.cpp:132-140). */
+double dgnn_graph_change_ratio(const dgnn_graph* g, int32_t t);
+
+/* ------------------------------------------------------------------ synth
+ * Replaces dgnn::synthesize (inc/synth.hpp:39, src/synth.cpp:36-91) with a
+ * bit-exact streaming generator producing snapshot 0 + per-step deltas. */
+int dgnn_synth_create(int32_t num_nodes, double avg_degree, int32_t feature_dim,
+                      int32_t num_snapshots, double edge_change, double feature_change,
+                      uint64_t seed, dgnn_synth** out);
+void dgnn_synth_free(dgnn_synth* s);
+/* sizes: [E0, then per step t=1..T-1: n_del, n_ins, n_changed] (1 + 3(T-1) int64). */
+int dgnn_synth_sizes(const dgnn_synth* s, int64_t* sizes);
+/* Host views (valid while s lives). */
+int dgnn_synth_base(const dgnn_synth* s, const int32_t** src, const int32_t** dst,
+                    const float** feats);
+int dgnn_synth_step(const dgnn_synth* s, int32_t t, const int32_t** del_src,
+                    const int32_t** del_dst, const int32_t** ins_src, const int32_t** ins_dst,
+                    const int32_t** changed, const float** changed_feats);
+/* Uploads the compact graph and builds every snapshot + delta on the device. */
+int dgnn_synth_to_graph(const dgnn_synth* s, void* stream, dgnn_graph** out);
+
+/* ------------------------------------------------------------ aggregation
+ * Kernels K1/K2/K3 over device buffers (src/aggregate.cpp:55-246). */
+int dgnn_agg_scratch(int32_t kind, int32_t n, int32_t w, const int64_t* in_ptr,
+                     const int32_t* in_src, const float* feats, float* values, float* degree,
+                     float* mean_sums, int32_t* argext, void* stream);
+int dgnn_agg_delta(int32_t kind, int32_t n_rows, int32_t w, const int32_t* rows,
+                   const int32_t* row_ptr, const int32_t* ent, const float* f_prev,
+                   const float* f_curr, float* values, float* degree, float* mean_sums,
+                   int32_t* argext, void* stream);
+int dgnn_agg_backward(int32_t kind, int32_t n, int32_t w, const int64_t* out_ptr,
+                      const int32_t* out_dst, const float* upstream, const float* degree,
+                      const int32_t* argext, float* grad, void* stream);
+/* aggregate_incremental with the reference's fallback logic
+ * (src/aggregate.cpp:117-207) from a caller-held AggResult of snapshot t-1 of
+ * graph g (features of the graph store). prev_* may alias nothing; out_* are
+ * caller-allocated (n x w; degree n). info[0] used_fallback, info[1]
+ * FallbackReason, info[2] incremental_depth of the result. */
+int dgnn_agg_incremental(const dgnn_graph* g, int32_t t, int32_t kind, const float* prev_values,
+                         const float* prev_degree, const float* prev_mean_sums,
+                         const int32_t* prev_argext, int32_t prev_depth, int64_t prev_num_edges,
+                         double fallback_threshold, int32_t rescratch_period, float* values,
+                         float* degree, float* mean_sums, int32_t* argext, int32_t* info);
+
+/* ------------------------------------------------------------------ cells
+ * Fused GraphRNN cell (cell_core_forward / cell_core_backward,
+ * src/cells.cpp:102-195). W: (in+H) x 4H packed gate weights, bias 4H. */
+int dgnn_pack_cell(int32_t lstm, int32_t in, int32_t H, const float* flat, float* W, float* bias,
+                   void* stream);
+int dgnn_cell_forward(int32_t lstm, int32_t n, int32_t in, int32_t H, const float* X,
+                      const float* Hm, const float* h_skip, const float* c_prev, const float* W,
+                      const float* bias, float* gates, float* c, float* h, void* stream);
+/* Grads: dX (n x in, may be NULL), dHm (n x H), dc_prev (LSTM) / dh_skip
+ * (GRU), flat parameter grads accumulated into dflat ([wx_g, uh_g, b_g]_g). */
+int dgnn_cell_backward(int32_t lstm, int32_t n, int32_t in, int32_t H, const float* X,
+                       const float* Hm, const float* W, const float* gates, const float* c,
+                       const float* c_prev, const float* h_skip, const float* dh, const float* dc,
+                       float* dX, float* dHm, float* dc_prev, float* dh_skip, float* dflat,
+                       void* stream);
+
+/* ---------------------------------------------------------------- trainer
+ * Replaces TrainSession / seq_first_epoch / optimizer_step
+ * (inc/train.hpp:64-114) and the consecutive-block DistSession
+ * (inc/distsim.hpp:55-108). Field order mirrors RunSettings
+ * (inc/config.hpp:18-57). */
+typedef struct dgnn_run_cfg {
+  int32_t arch;
+  int32_t layers;
+  int32_t hidden;
+  int32_t seq_len;
+  int32_t horizon;
+  int32_t teacher_forcing;
+  int32_t aggr;
+  int32_t batch_size;
+  uint64_t seed;
+  double lr;
+  int32_t optimizer; /* 0 sgd, 1 adam */
+  int32_t stride;
+  double fallback_threshold;
+  int32_t rescratch_period;
+  int32_t incremental;
+  int32_t cache_policy; /* -1 off, 0 reinc, 1 lru, 2 lfu */
+  double cache_frac;
+  int32_t workers;      /* 0: seq-first session; >= 1: world size of the sharded trainer */
+  int32_t epochs;
+  int32_t window_total; /* sliding_windows total T' (0 -> T-1) */
+  int32_t record_events;
+  int64_t hbm_cache_budget_bytes; /* 0 = no second cache level */
+} dgnn_run_cfg;
+
+typedef struct dgnn_epoch_report {
+  double loss;
+  double seconds; /* device-timed */
+  int64_t samples;
+  int64_t hits, misses, evictions, expirations, invalidations, rejected;
+  int64_t scratch_calls, incremental_calls, fallbacks, skipped_steps;
+  int64_t spills, refills;
+} dgnn_epoch_report;
+
+int dgnn_session_create(dgnn_graph* g, const dgnn_run_cfg* cfg, int32_t rank, void* stream,
+                        dgnn_session** out);
+void dgnn_session_free(dgnn_session* s);
+int64_t dgnn_session_num_params(const dgnn_session* s);
+int dgnn_session_num_windows(const dgnn_session* s, int64_t* total, int64_t* local_begin,
+                             int64_t* local_end);
+/* DgnnModel::flatten_params / unflatten_params (src/model.cpp:91-107). */
+int dgnn_session_get_params(dgnn_session* s, double* out);
+int dgnn_session_set_params(dgnn_session* s, const double* in);
+int dgnn_session_initial_params(dgnn_session* s, double* out);
+/* seq_first_epoch (src/train.cpp:146-210); sample losses via dgnn_session_losses. */
+int dgnn_session_run_epoch(dgnn_session* s, dgnn_epoch_report* report);
+/* Sharded trainer, one call sequence per epoch:
+ *   begin_epoch; for b < num_batches: local_grads(b, g); <all-reduce g>; apply(g)
+ *   end_epoch. g: device fp32 buffer of num_params floats. */
+int dgnn_session_begin_epoch(dgnn_session* s, int64_t* num_batches);
+int dgnn_session_local_grads(dgnn_session* s, int64_t batch, float* grad_sum);
+int dgnn_session_apply(dgnn_session* s, const float* grad_sum, int32_t* applied);
+int dgnn_session_end_epoch(dgnn_session* s);
+/* Sample losses of the last epoch (visit order). */
+int dgnn_session_losses(dgnn_session* s, double* out, int64_t* n);
+/* One sample's forward + backward at the current parameters with a fresh
+ * cache/provider: loss, prediction of horizon step 0 (n x d) and flat grads. */
+int dgnn_session_sample_grads(dgnn_session* s, int32_t window_index, double* loss, float* pred0,
+                              double* grads);
+/* Invocation log rows (layer, t, kind, incremental); pass NULL to size. */
+int dgnn_session_invocations(dgnn_session* s, int32_t* out, int64_t* n);
+/* Cache observer events rows (type, level, layer, t, kind, batch, serial,
+ * hit, assigned_f, stored) when record_events; pass NULL to size. */
+int dgnn_session_cache_events(dgnn_session* s, int64_t* out, int64_t* n);
+/* Cumulative stats: hits misses evictions expirations invalidations rejected
+ * scratch incremental fallbacks spills refills peak_units(as int64). */
+int dgnn_session_stats(dgnn_session* s, int64_t* out12);
+
+/* ---------------------------------------------------------------- profiling
+ * Device timing per kernel class (0 agg_scratch, 1 agg_delta, 2 agg_backward,
+ * 3 cell_fwd, 4 cell_bwd, 5 weight_grad, 6 other) with algorithmic bytes. */
+int dgnn_prof_enable(int32_t on);
+int dgnn_prof_reset(void);
+int dgnn_prof_get(int32_t cls, int64_t* launches, double* ms, double* bytes, double* flops);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DGNN_B200_H */

@@ -1,0 +1,555 @@
+"""Python mirror of the reference's public interface over the C ABI.
+
+Names and argument meaning follow proj/include/dgnn (DynamicGraph, synthesize,
+aggregate_scratch / aggregate_incremental / aggregate_backward, TrainSession,
+the consecutive-block distributed session). Device buffers are torch CUDA
+tensors (torch is used for allocation and streams only); all computation runs
+in _dgnn_b200.so. Errors surface as ValueError (the reference's
+std::invalid_argument), IndexError (std::out_of_range) or DgnnError (CUDA).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib
+
+AGGR = {"sum": 0, "mean": 1, "max": 2, "min": 3}
+ARCH = {"gcrn_m1": 0, "cd_gcn": 1, "gcrn_m2": 2, "tgcn": 3}
+POLICY = {"off": -1, "reinc": 0, "lru": 1, "lfu": 2}
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _np_ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _stream_handle(stream):
+    if stream is None:
+        return None
+    return C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def current_stream():
+    torch = _torch()
+    return torch.cuda.current_stream()
+
+
+class _CudaArray:
+    def __init__(self, ptr, shape, dtype):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": np.dtype(dtype).str,
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+def device_view(ptr, shape, dtype):
+    """Zero-copy torch view of a device buffer owned by the library."""
+    torch = _torch()
+    return torch.as_tensor(_CudaArray(ptr, shape, dtype), device="cuda")
+
+
+def launch_count() -> int:
+    return lib().dgnn_launch_count()
+
+
+def sliding_windows(total: int, length: int, stride: int, horizon: int) -> list[int]:
+    """Window starts 0, S, 2S, ... while start + L + H <= T (ref src/windows.cpp:5-15)."""
+    if length < 1:
+        raise ValueError("sliding_windows: L must be >= 1")
+    if stride < 1:
+        raise ValueError("sliding_windows: S must be >= 1")
+    if horizon < 0:
+        raise ValueError("sliding_windows: H must be >= 0")
+    return list(range(0, max(total - length - horizon + 1, 0), stride))
+
+
+def plan(total: int, workers: int, L: int, S: int, H: int):
+    """Consecutive-block placement (ref src/distsim.cpp:35-81): per worker
+    (block_begin, block_end, window_begin, window_end)."""
+    if workers < 1:
+        raise ValueError("plan needs at least one worker")
+    if total < workers:
+        raise ValueError("fewer snapshots than workers")
+    starts = sliding_windows(total, L, S, H)
+    W = len(starts)
+    base, extra = divmod(W, workers)
+    out, cur = [], 0
+    for m in range(workers):
+        wb, we = cur, cur + base + (1 if m < extra else 0)
+        cur = we
+        bb = starts[wb] if wb < W else total
+        be = (starts[we] if we < W else total) if m + 1 < workers else total
+        out.append([min(bb, be), be, wb, we])
+    out[0][0] = 0
+    return out
+
+
+# ------------------------------------------------------------------ graphs
+class Synth:
+    """Bit-exact streaming synthesize (ref src/synth.cpp:36-91), host side."""
+
+    def __init__(self, num_nodes, avg_degree, feature_dim, num_snapshots, edge_change,
+                 feature_change, seed=1):
+        h = C.c_void_p()
+        check(lib().dgnn_synth_create(num_nodes, avg_degree, feature_dim, num_snapshots,
+                                      edge_change, feature_change, seed, C.byref(h)))
+        self.h = h
+        self.n, self.dim, self.T = num_nodes, feature_dim, num_snapshots
+        sizes = np.empty(1 + 3 * (num_snapshots - 1), np.int64)
+        check(lib().dgnn_synth_sizes(self.h, _np_ptr(sizes)))
+        self.sizes = sizes
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().dgnn_synth_free(self.h)
+            self.h = None
+
+    def base(self):
+        s, d, f = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        check(lib().dgnn_synth_base(self.h, C.byref(s), C.byref(d), C.byref(f)))
+        E = int(self.sizes[0])
+        src = np.ctypeslib.as_array(C.cast(s, C.POINTER(C.c_int32)), (E,)).copy() if E else np.zeros(0, np.int32)
+        dst = np.ctypeslib.as_array(C.cast(d, C.POINTER(C.c_int32)), (E,)).copy() if E else np.zeros(0, np.int32)
+        feats = np.ctypeslib.as_array(C.cast(f, C.POINTER(C.c_float)), (self.n * self.dim,)).copy()
+        return src, dst, feats.reshape(self.n, self.dim)
+
+    def step(self, t):
+        ptrs = [C.c_void_p() for _ in range(6)]
+        check(lib().dgnn_synth_step(self.h, t, *[C.byref(p) for p in ptrs]))
+        nd, ni, nc = (int(x) for x in self.sizes[1 + 3 * (t - 1): 4 + 3 * (t - 1)])
+
+        def arr(p, n, ct=C.c_int32):
+            if n == 0:
+                return np.zeros(0, np.int32 if ct is C.c_int32 else np.float32)
+            return np.ctypeslib.as_array(C.cast(p, C.POINTER(ct)), (n,)).copy()
+
+        return {"del_src": arr(ptrs[0], nd), "del_dst": arr(ptrs[1], nd),
+                "ins_src": arr(ptrs[2], ni), "ins_dst": arr(ptrs[3], ni),
+                "changed": arr(ptrs[4], nc),
+                "changed_feats": arr(ptrs[5], nc * self.dim, C.c_float).reshape(nc, self.dim)}
+
+    def to_graph(self, stream=None) -> "DynamicGraph":
+        h = C.c_void_p()
+        check(lib().dgnn_synth_to_graph(self.h, _stream_handle(stream), C.byref(h)))
+        return DynamicGraph._wrap(h, self.n, self.dim)
+
+
+def synthesize(num_nodes, avg_degree, feature_dim, num_snapshots, edge_change, feature_change,
+               seed=1, stream=None) -> "DynamicGraph":
+    return Synth(num_nodes, avg_degree, feature_dim, num_snapshots, edge_change,
+                 feature_change, seed).to_graph(stream)
+
+
+class DynamicGraph:
+    """Device-resident dynamic graph (ref DynamicGraph, inc/snapshot.hpp:92-107)."""
+
+    def __init__(self, num_nodes: int, feature_dim: int, stream=None):
+        h = C.c_void_p()
+        check(lib().dgnn_graph_create(num_nodes, feature_dim, _stream_handle(stream), C.byref(h)))
+        self.h, self.n, self.dim = h, num_nodes, feature_dim
+
+    @classmethod
+    def _wrap(cls, h, n, dim):
+        g = cls.__new__(cls)
+        g.h, g.n, g.dim = h, n, dim
+        return g
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().dgnn_graph_free(self.h)
+            self.h = None
+
+    @classmethod
+    def from_snapshots(cls, num_nodes, edges_per_t, feats_per_t, stream=None):
+        """Snapshot ctor per step (src/snapshot.cpp:20-69)."""
+        g = cls(num_nodes, np.asarray(feats_per_t[0]).shape[1], stream)
+        for e, f in zip(edges_per_t, feats_per_t):
+            g.add_snapshot(e, f)
+        return g
+
+    def add_snapshot(self, edges, feats):
+        e = np.ascontiguousarray(np.asarray(edges, np.int32).reshape(-1, 2))
+        src, dst = np.ascontiguousarray(e[:, 0]), np.ascontiguousarray(e[:, 1])
+        f = np.ascontiguousarray(feats, np.float32)
+        check(lib().dgnn_graph_add_snapshot(self.h, _np_ptr(src), _np_ptr(dst), len(src), _np_ptr(f)))
+
+    def add_delta(self, deletions, insertions, changed_nodes=(), changed_feats=None):
+        """apply_delta (src/snapshot.cpp:142-154)."""
+        d = np.ascontiguousarray(np.asarray(deletions, np.int32).reshape(-1, 2))
+        i = np.ascontiguousarray(np.asarray(insertions, np.int32).reshape(-1, 2))
+        c = np.ascontiguousarray(np.asarray(changed_nodes, np.int32))
+        cf = np.ascontiguousarray(np.zeros((0, self.dim), np.float32) if changed_feats is None
+                                  else np.asarray(changed_feats, np.float32))
+        ds, dd = np.ascontiguousarray(d[:, 0]), np.ascontiguousarray(d[:, 1])
+        is_, id_ = np.ascontiguousarray(i[:, 0]), np.ascontiguousarray(i[:, 1])
+        check(lib().dgnn_graph_add_delta(self.h, _np_ptr(ds), _np_ptr(dd), len(ds), _np_ptr(is_),
+                                         _np_ptr(id_), len(is_), _np_ptr(c), len(c), _np_ptr(cf)))
+
+    def length(self) -> int:
+        return lib().dgnn_graph_length(self.h)
+
+    def num_edges(self, t) -> int:
+        n = lib().dgnn_graph_num_edges(self.h, t)
+        if n < 0:
+            raise IndexError(lib().dgnn_last_error().decode())
+        return n
+
+    def snapshot_ptrs(self, t):
+        ptrs = [C.c_void_p() for _ in range(5)]
+        check(lib().dgnn_graph_snapshot(self.h, t, *[C.byref(p) for p in ptrs]))
+        return [p.value for p in ptrs]
+
+    def _dev_to_numpy(self, ptr, n, dtype):
+        if n == 0:
+            return np.zeros(0, dtype)
+        lib().dgnn_synchronize(None)
+        return device_view(ptr, (n,), dtype).cpu().numpy()
+
+    def in_csr(self, t):
+        ip, isrc, _, _, _ = self.snapshot_ptrs(t)
+        E = self.num_edges(t)
+        return self._dev_to_numpy(ip, self.n + 1, np.int64), self._dev_to_numpy(isrc, E, np.int32)
+
+    def out_csr(self, t):
+        _, _, op, od, _ = self.snapshot_ptrs(t)
+        E = self.num_edges(t)
+        return self._dev_to_numpy(op, self.n + 1, np.int64), self._dev_to_numpy(od, E, np.int32)
+
+    def feats(self, t):
+        f = self.snapshot_ptrs(t)[4]
+        return self._dev_to_numpy(f, self.n * self.dim, np.float32).reshape(self.n, self.dim)
+
+    def feats_tensor(self, t):
+        """Zero-copy-free device copy of snapshot t's features as a torch tensor."""
+        torch = _torch()
+        return torch.from_numpy(self.feats(t)).cuda()
+
+    def edges(self, t):
+        ptr, dst = self.out_csr(t)
+        src = np.repeat(np.arange(self.n, dtype=np.int32), np.diff(ptr))
+        return src, dst
+
+    def delta_sizes(self, t):
+        vals = [C.c_int64() for _ in range(6)]
+        check(lib().dgnn_graph_delta_sizes(self.h, t, *[C.byref(v) for v in vals]))
+        keys = ["n_del", "n_ins", "n_changed", "n_rows", "u_minus", "u_plus"]
+        return {k: v.value for k, v in zip(keys, vals)}
+
+    def delta(self, t):
+        s = self.delta_sizes(t)
+        ds, dd = np.empty(s["n_del"], np.int32), np.empty(s["n_del"], np.int32)
+        is_, id_ = np.empty(s["n_ins"], np.int32), np.empty(s["n_ins"], np.int32)
+        ch = np.empty(s["n_changed"], np.int32)
+        check(lib().dgnn_graph_delta_copy(self.h, t, _np_ptr(ds), _np_ptr(dd), _np_ptr(is_),
+                                          _np_ptr(id_), _np_ptr(ch)))
+        return {"del_src": ds, "del_dst": dd, "ins_src": is_, "ins_dst": id_, "changed": ch}
+
+    def delta_layout(self, t):
+        ptrs = [C.c_void_p() for _ in range(3)]
+        check(lib().dgnn_graph_delta_layout(self.h, t, *[C.byref(p) for p in ptrs]))
+        return [p.value for p in ptrs]
+
+    def change_ratio(self, t) -> float:
+        r = lib().dgnn_graph_change_ratio(self.h, t)
+        if r < 0:
+            raise ValueError(lib().dgnn_last_error().decode())
+        return r
+
+
+# ------------------------------------------------------------- aggregation
+def aggregate_scratch(graph: DynamicGraph, t: int, feats, kind="sum", stream=None):
+    """K1 over snapshot t's in-CSR; feats: (n, w) float32 CUDA tensor."""
+    torch = _torch()
+    n, w = feats.shape
+    ip, isrc, _, _, _ = graph.snapshot_ptrs(t)
+    out = {"values": torch.empty(n, w, device="cuda")}
+    if kind == "mean":
+        out["degree"] = torch.empty(n, device="cuda")
+        out["mean_sums"] = torch.empty(n, w, device="cuda")
+    if kind in ("max", "min"):
+        out["argext"] = torch.empty(n, w, dtype=torch.int32, device="cuda")
+    check(lib().dgnn_agg_scratch(AGGR[kind], n, w, C.c_void_p(ip), C.c_void_p(isrc), _ptr(feats),
+                                 _ptr(out["values"]), _ptr(out.get("degree")),
+                                 _ptr(out.get("mean_sums")), _ptr(out.get("argext")),
+                                 _stream_handle(stream or current_stream())))
+    return out
+
+
+def aggregate_delta_inplace(graph: DynamicGraph, t: int, agg: dict, f_prev, f_curr, kind="sum",
+                            stream=None):
+    """K2: apply delta(t) in place to an aggregation holding Agg_{t-1}."""
+    n, w = agg["values"].shape
+    rows, row_ptr, ent = graph.delta_layout(t)
+    nr = graph.delta_sizes(t)["n_rows"]
+    check(lib().dgnn_agg_delta(AGGR[kind], nr, w, C.c_void_p(rows), C.c_void_p(row_ptr),
+                               C.c_void_p(ent), _ptr(f_prev), _ptr(f_curr), _ptr(agg["values"]),
+                               _ptr(agg.get("degree")), _ptr(agg.get("mean_sums")),
+                               _ptr(agg.get("argext")), _stream_handle(stream or current_stream())))
+    return agg
+
+
+def aggregate_incremental(graph: DynamicGraph, t: int, prev: dict, kind="sum", prev_depth=0,
+                          prev_num_edges=None, fallback_threshold=0.5, rescratch_period=64):
+    """aggregate_incremental with the reference's fallback logic (src/aggregate.cpp:117-207)."""
+    torch = _torch()
+    n, w = prev["values"].shape
+    if prev_num_edges is None:
+        prev_num_edges = graph.num_edges(t - 1)
+    out = {"values": torch.empty(n, w, device="cuda")}
+    if kind == "mean":
+        out["degree"] = torch.empty(n, device="cuda")
+        out["mean_sums"] = torch.empty(n, w, device="cuda")
+    if kind in ("max", "min"):
+        out["argext"] = torch.empty(n, w, dtype=torch.int32, device="cuda")
+    info = np.zeros(3, np.int32)
+    torch.cuda.synchronize()
+    check(lib().dgnn_agg_incremental(graph.h, t, AGGR[kind], _ptr(prev["values"]),
+                                     _ptr(prev.get("degree")), _ptr(prev.get("mean_sums")),
+                                     _ptr(prev.get("argext")), prev_depth, prev_num_edges,
+                                     fallback_threshold, rescratch_period, _ptr(out["values"]),
+                                     _ptr(out.get("degree")), _ptr(out.get("mean_sums")),
+                                     _ptr(out.get("argext")), _np_ptr(info)))
+    out["used_fallback"], out["reason"], out["depth"] = bool(info[0]), int(info[1]), int(info[2])
+    return out
+
+
+def aggregate_backward(graph: DynamicGraph, t: int, upstream, kind="sum", forward=None,
+                       stream=None):
+    """K3: grad[u] = sum over out-edges of upstream (ref src/aggregate.cpp:209-246)."""
+    torch = _torch()
+    n, w = upstream.shape
+    _, _, op, od, _ = graph.snapshot_ptrs(t)
+    grad = torch.empty(n, w, device="cuda")
+    forward = forward or {}
+    check(lib().dgnn_agg_backward(AGGR[kind], n, w, C.c_void_p(op), C.c_void_p(od), _ptr(upstream),
+                                  _ptr(forward.get("degree")), _ptr(forward.get("argext")),
+                                  _ptr(grad), _stream_handle(stream or current_stream())))
+    return grad
+
+
+# ------------------------------------------------------------------ cells
+def pack_cell(lstm: bool, n_in: int, H: int, flat):
+    torch = _torch()
+    W = torch.empty((n_in + H) * 4 * H, device="cuda")
+    b = torch.empty(4 * H, device="cuda")
+    check(lib().dgnn_pack_cell(int(lstm), n_in, H, _ptr(flat), _ptr(W), _ptr(b),
+                               _stream_handle(current_stream())))
+    return W, b
+
+
+def cell_forward(lstm, X, Hm, h_skip, c_prev, flat):
+    """Fused cell_core_forward (src/cells.cpp:102-132)."""
+    torch = _torch()
+    n, n_in = X.shape
+    H = Hm.shape[1]
+    W, b = pack_cell(lstm, n_in, H, flat)
+    gates = torch.empty(n, 4 * H, device="cuda")
+    c = torch.empty(n, H, device="cuda") if lstm else None
+    h = torch.empty(n, H, device="cuda")
+    check(lib().dgnn_cell_forward(int(lstm), n, n_in, H, _ptr(X), _ptr(Hm), _ptr(h_skip),
+                                  _ptr(c_prev), _ptr(W), _ptr(b), _ptr(gates), _ptr(c), _ptr(h),
+                                  _stream_handle(current_stream())))
+    return {"gates": gates, "c": c, "h": h, "W": W, "b": b}
+
+
+def cell_backward(lstm, X, Hm, fwd, h_skip, c_prev, dh, dc, need_dx=True):
+    """cell_core_backward (src/cells.cpp:134-195): returns dX, dHm, dc_prev/dh_skip, dflat."""
+    torch = _torch()
+    n, n_in = X.shape
+    H = Hm.shape[1]
+    K = 4 if lstm else 3
+    dX = torch.empty(n, n_in, device="cuda") if need_dx else None
+    dHm = torch.empty(n, H, device="cuda")
+    dcp = torch.empty(n, H, device="cuda") if lstm else None
+    dhs = None if lstm else torch.empty(n, H, device="cuda")
+    dflat = torch.zeros(K * (n_in * H + H * H + H), device="cuda")
+    check(lib().dgnn_cell_backward(int(lstm), n, n_in, H, _ptr(X), _ptr(Hm), _ptr(fwd["W"]),
+                                   _ptr(fwd["gates"]), _ptr(fwd["c"]), _ptr(c_prev), _ptr(h_skip),
+                                   _ptr(dh), _ptr(dc), _ptr(dX), _ptr(dHm), _ptr(dcp), _ptr(dhs),
+                                   _ptr(dflat), _stream_handle(current_stream())))
+    return {"dX": dX, "dHm": dHm, "dc_prev": dcp, "dh_skip": dhs, "dflat": dflat}
+
+
+# ------------------------------------------------------------------ training
+@dataclass
+class TrainConfig:
+    """RunSettings defaults (ref inc/config.hpp:18-57) plus the B200 cache budget."""
+    arch: str = "gcrn_m2"
+    layers: int = 2
+    hidden: int = 16
+    seq_len: int = 8
+    horizon: int = 1
+    teacher_forcing: bool = True
+    aggr: str = "sum"
+    batch_size: int = 0
+    seed: int = 1
+    lr: float = 0.01
+    optimizer: str = "adam"
+    stride: int = 1
+    fallback_threshold: float = 0.5
+    rescratch_period: int = 64
+    incremental: bool = True
+    cache: str = "reinc"
+    cache_frac: float = 1.0
+    workers: int = 0
+    epochs: int = 1
+    window_total: int = 0
+    record_events: bool = False
+    hbm_cache_budget_bytes: int = 0
+
+    def to_c(self) -> _lib.RunCfg:
+        c = _lib.RunCfg()
+        c.arch, c.layers, c.hidden = ARCH[self.arch], self.layers, self.hidden
+        c.seq_len, c.horizon, c.teacher_forcing = self.seq_len, self.horizon, int(self.teacher_forcing)
+        c.aggr, c.batch_size, c.seed = AGGR[self.aggr], self.batch_size, self.seed
+        c.lr, c.optimizer, c.stride = self.lr, 0 if self.optimizer == "sgd" else 1, self.stride
+        c.fallback_threshold, c.rescratch_period = self.fallback_threshold, self.rescratch_period
+        c.incremental, c.cache_policy, c.cache_frac = int(self.incremental), POLICY[self.cache], self.cache_frac
+        c.workers, c.epochs, c.window_total = self.workers, self.epochs, self.window_total
+        c.record_events, c.hbm_cache_budget_bytes = int(self.record_events), self.hbm_cache_budget_bytes
+        return c
+
+
+class TrainSession:
+    """TrainSession / DistSession rank over a device graph (ref inc/train.hpp:92-114,
+    inc/distsim.hpp:82-102). workers == 0: seq-first; workers >= 1: rank `rank` of
+    the consecutive-block sharded trainer."""
+
+    def __init__(self, graph: DynamicGraph, cfg: TrainConfig, rank: int = 0, stream=None):
+        self.graph, self.cfg = graph, cfg
+        self._c = cfg.to_c()
+        h = C.c_void_p()
+        check(lib().dgnn_session_create(graph.h, C.byref(self._c), rank, _stream_handle(stream),
+                                        C.byref(h)))
+        self.h = h
+        self.num_params = lib().dgnn_session_num_params(self.h)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().dgnn_session_free(self.h)
+            self.h = None
+
+    def windows(self):
+        tot, b, e = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib().dgnn_session_num_windows(self.h, C.byref(tot), C.byref(b), C.byref(e)))
+        return tot.value, b.value, e.value
+
+    def params(self) -> np.ndarray:
+        out = np.empty(self.num_params, np.float64)
+        check(lib().dgnn_session_get_params(self.h, _np_ptr(out)))
+        return out
+
+    def set_params(self, p):
+        p = np.ascontiguousarray(p, np.float64)
+        check(lib().dgnn_session_set_params(self.h, _np_ptr(p)))
+
+    def initial_params(self) -> np.ndarray:
+        out = np.empty(self.num_params, np.float64)
+        check(lib().dgnn_session_initial_params(self.h, _np_ptr(out)))
+        return out
+
+    def run_epoch(self) -> dict:
+        r = _lib.EpochReport()
+        check(lib().dgnn_session_run_epoch(self.h, C.byref(r)))
+        out = {k: getattr(r, k) for k, _ in _lib.EpochReport._fields_}
+        out["sample_losses"] = self.losses()
+        return out
+
+    def begin_epoch(self) -> int:
+        nb = C.c_int64()
+        check(lib().dgnn_session_begin_epoch(self.h, C.byref(nb)))
+        return nb.value
+
+    def local_grads(self, batch: int, grad_sum):
+        check(lib().dgnn_session_local_grads(self.h, batch, _ptr(grad_sum)))
+
+    def apply(self, grad_sum) -> bool:
+        a = C.c_int32()
+        check(lib().dgnn_session_apply(self.h, _ptr(grad_sum), C.byref(a)))
+        return bool(a.value)
+
+    def end_epoch(self):
+        check(lib().dgnn_session_end_epoch(self.h))
+
+    def run_sharded_epoch(self, allreduce=None) -> list[float]:
+        """One distsim epoch on this rank; `allreduce(tensor)` sums over ranks."""
+        torch = _torch()
+        g = torch.empty(self.num_params, device="cuda")
+        nb = self.begin_epoch()
+        for b in range(nb):
+            self.local_grads(b, g)
+            if allreduce is not None:
+                torch.cuda.current_stream().synchronize()
+                allreduce(g)
+            self.apply(g)
+        self.end_epoch()
+        return self.losses()
+
+    def losses(self) -> np.ndarray:
+        n = C.c_int64()
+        check(lib().dgnn_session_losses(self.h, None, C.byref(n)))
+        out = np.empty(n.value, np.float64)
+        check(lib().dgnn_session_losses(self.h, _np_ptr(out), C.byref(n)))
+        return out
+
+    def sample_grads(self, window_index=0):
+        loss = C.c_double()
+        pred0 = np.empty((self.graph.n, self.graph.dim), np.float32)
+        grads = np.empty(self.num_params, np.float64)
+        check(lib().dgnn_session_sample_grads(self.h, window_index, C.byref(loss), _np_ptr(pred0),
+                                              _np_ptr(grads)))
+        return loss.value, pred0, grads
+
+    def invocations(self) -> np.ndarray:
+        n = C.c_int64()
+        check(lib().dgnn_session_invocations(self.h, None, C.byref(n)))
+        out = np.empty((n.value, 4), np.int32)
+        check(lib().dgnn_session_invocations(self.h, _np_ptr(out), C.byref(n)))
+        return out
+
+    def cache_events(self) -> np.ndarray:
+        n = C.c_int64()
+        check(lib().dgnn_session_cache_events(self.h, None, C.byref(n)))
+        out = np.empty((n.value, 10), np.int64)
+        check(lib().dgnn_session_cache_events(self.h, _np_ptr(out), C.byref(n)))
+        return out
+
+    def stats(self) -> dict:
+        out = np.empty(12, np.int64)
+        check(lib().dgnn_session_stats(self.h, _np_ptr(out)))
+        keys = ["hits", "misses", "evictions", "expirations", "invalidations", "rejected",
+                "scratch_calls", "incremental_calls", "fallbacks", "spills", "refills",
+                "resident_peak_units"]
+        return dict(zip(keys, out.tolist()))
+
+
+# ------------------------------------------------------------------ profiling
+PROF_CLASSES = ["agg_scratch", "agg_delta", "agg_backward", "cell_fwd", "cell_bwd",
+                "weight_grad", "other"]
+
+
+def prof_enable(on=True):
+    check(lib().dgnn_prof_enable(int(on)))
+
+
+def prof_reset():
+    check(lib().dgnn_prof_reset())
+
+
+def prof_get() -> dict:
+    out = {}
+    for i, name in enumerate(PROF_CLASSES):
+        n, ms, b, f = C.c_int64(), C.c_double(), C.c_double(), C.c_double()
+        check(lib().dgnn_prof_get(i, C.byref(n), C.byref(ms), C.byref(b), C.byref(f)))
+        out[name] = {"launches": n.value, "ms": ms.value, "bytes": b.value, "flops": f.value}
+    return out

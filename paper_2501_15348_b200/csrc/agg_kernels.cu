@@ -1,0 +1,462 @@
+// Neighbourhood-aggregation kernels for sm_100a.
+//
+//   K1 agg_scratch   pull SpMM over the in-CSR          (ref src/aggregate.cpp:55-115)
+//   K2 agg_delta     delta-SpMM over dst-grouped signed COO (ref src/aggregate.cpp:117-207)
+//   K3 agg_backward  transposed SpMM as a pull over the out-CSR (ref src/aggregate.cpp:209-246)
+//
+// All three are HBM-bound gathers of feature rows. A row is owned by a group
+// of G lanes (G = width / VEC rounded to a power of two, <= 32); each lane
+// moves VEC contiguous floats with one vector load, so a 128-wide fp32 row is
+// one fully coalesced 512 B warp access. Edge indices are fetched G at a time
+// (coalesced) and broadcast by shuffle; gathers are issued UNR rows ahead of
+// the in-order accumulation, so each row's reduction order is exactly the
+// reference's (ascending source within a destination; deletions before
+// insertions for the delta), which keeps results deterministic and makes the
+// fp32 path differ from the fp64 reference only by rounding.
+#include "agg_kernels.h"
+#include "common.cuh"
+
+#include <cfloat>
+
+namespace dgnn {
+namespace cuda {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kUnroll = 4;
+
+template <int V>
+struct VecLoad;
+template <>
+struct VecLoad<4> {
+  __device__ static void ld(float (&r)[4], const float* p) {
+    float4 x = __ldg(reinterpret_cast<const float4*>(p));
+    r[0] = x.x; r[1] = x.y; r[2] = x.z; r[3] = x.w;
+  }
+  __device__ static void st(float* p, const float (&r)[4]) {
+    *reinterpret_cast<float4*>(p) = make_float4(r[0], r[1], r[2], r[3]);
+  }
+  __device__ static void ld_rw(float (&r)[4], const float* p) {
+    float4 x = *reinterpret_cast<const float4*>(p);
+    r[0] = x.x; r[1] = x.y; r[2] = x.z; r[3] = x.w;
+  }
+};
+template <>
+struct VecLoad<2> {
+  __device__ static void ld(float (&r)[2], const float* p) {
+    float2 x = __ldg(reinterpret_cast<const float2*>(p));
+    r[0] = x.x; r[1] = x.y;
+  }
+  __device__ static void st(float* p, const float (&r)[2]) {
+    *reinterpret_cast<float2*>(p) = make_float2(r[0], r[1]);
+  }
+  __device__ static void ld_rw(float (&r)[2], const float* p) {
+    float2 x = *reinterpret_cast<const float2*>(p);
+    r[0] = x.x; r[1] = x.y;
+  }
+};
+template <>
+struct VecLoad<1> {
+  __device__ static void ld(float (&r)[1], const float* p) { r[0] = __ldg(p); }
+  __device__ static void st(float* p, const float (&r)[1]) { p[0] = r[0]; }
+  __device__ static void ld_rw(float (&r)[1], const float* p) { r[0] = *p; }
+};
+
+template <int V>
+__device__ inline void ld_int(int32_t (&r)[V], const int32_t* p) {
+#pragma unroll
+  for (int i = 0; i < V; ++i) r[i] = p[i];
+}
+template <int V>
+__device__ inline void st_int(int32_t* p, const int32_t (&r)[V]) {
+#pragma unroll
+  for (int i = 0; i < V; ++i) p[i] = r[i];
+}
+
+// Per-element update of one gathered source row into the accumulator.
+template <int KIND, int V>
+__device__ inline void accumulate(float (&acc)[V], int32_t (&arg)[V], const float (&x)[V],
+                                  int32_t u) {
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    if (KIND == kAggSum || KIND == kAggMean) {
+      acc[i] += x[i];
+    } else if (KIND == kAggMax) {
+      if (arg[i] < 0 || x[i] > acc[i]) { acc[i] = x[i]; arg[i] = u; }
+    } else {
+      if (arg[i] < 0 || x[i] < acc[i]) { acc[i] = x[i]; arg[i] = u; }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K1 scratch
+template <int V, int G, int KIND>
+__global__ void __launch_bounds__(kThreads)
+k_agg_scratch(int n, int w, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+              const float* __restrict__ F, float* __restrict__ out, float* __restrict__ degree,
+              float* __restrict__ msum, int32_t* __restrict__ argext) {
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  constexpr int kRowsPerWarp = 32 / G;
+  const int64_t warp_global = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+  const int64_t warp_stride = (static_cast<int64_t>(gridDim.x) * kThreads) >> 5;
+  const int nchunk = (w + G * V - 1) / (G * V);
+  for (int64_t vbase = warp_global * kRowsPerWarp; vbase < n; vbase += warp_stride * kRowsPerWarp) {
+    const int64_t v = vbase + lane / G;
+    const bool valid = v < n;
+    const int64_t beg = valid ? ptr[v] : 0;
+    const int deg = valid ? static_cast<int>(ptr[v + 1] - beg) : 0;
+    const int maxdeg = __reduce_max_sync(0xffffffffu, deg);
+    for (int k = 0; k < nchunk; ++k) {
+      const int c = (k * G + gl) * V;
+      const bool cact = valid && c < w;
+      float acc[V];
+      int32_t arg[V];
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        acc[i] = KIND == kAggMax ? -INFINITY : (KIND == kAggMin ? INFINITY : 0.f);
+        arg[i] = -1;
+      }
+      for (int eb = 0; eb < maxdeg; eb += G) {
+        const int my_e = eb + gl;
+        const int32_t my_u = my_e < deg ? idx[beg + my_e] : 0;
+        const int cnt = min(G, maxdeg - eb);
+        for (int j0 = 0; j0 < cnt; j0 += kUnroll) {
+          float x[kUnroll][V];
+          int32_t u[kUnroll];
+#pragma unroll
+          for (int q = 0; q < kUnroll; ++q) {
+            u[q] = __shfl_sync(0xffffffffu, my_u, (j0 + q) & (G - 1), G);
+            if (cact && j0 + q < cnt && eb + j0 + q < deg) {
+              VecLoad<V>::ld(x[q], F + static_cast<int64_t>(u[q]) * w + c);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < kUnroll; ++q) {
+            if (cact && j0 + q < cnt && eb + j0 + q < deg) accumulate<KIND, V>(acc, arg, x[q], u[q]);
+          }
+        }
+      }
+      if (cact) {
+        float* o = out + v * w + c;
+        if (KIND == kAggMean) {
+          VecLoad<V>::st(msum + v * w + c, acc);
+          float r[V];
+          const float dg = static_cast<float>(deg);
+#pragma unroll
+          for (int i = 0; i < V; ++i) r[i] = deg > 0 ? acc[i] / dg : 0.f;
+          VecLoad<V>::st(o, r);
+          if (c == 0) degree[v] = dg;
+        } else {
+          VecLoad<V>::st(o, acc);
+          if (KIND == kAggMax || KIND == kAggMin) st_int<V>(argext + v * w + c, arg);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K2 delta
+// rows[r] = destination, entries ent[row_ptr[r] .. row_ptr[r+1]) = deletions
+// (encoded ~src, ascending src) followed by insertions (src, ascending).
+template <int V, int G, int KIND>
+__global__ void __launch_bounds__(kThreads)
+k_agg_delta(int n_rows, int w, const int32_t* __restrict__ rows, const int32_t* __restrict__ row_ptr,
+            const int32_t* __restrict__ ent, const float* __restrict__ Fp, const float* __restrict__ Fc,
+            float* __restrict__ values, float* __restrict__ degree, float* __restrict__ msum,
+            int32_t* __restrict__ argext) {
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  constexpr int kRowsPerWarp = 32 / G;
+  const int64_t warp_global = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+  const int64_t warp_stride = (static_cast<int64_t>(gridDim.x) * kThreads) >> 5;
+  const int nchunk = (w + G * V - 1) / (G * V);
+  for (int64_t rbase = warp_global * kRowsPerWarp; rbase < n_rows; rbase += warp_stride * kRowsPerWarp) {
+    const int64_t r = rbase + lane / G;
+    const bool valid = r < n_rows;
+    const int64_t v = valid ? rows[r] : 0;
+    const int beg = valid ? row_ptr[r] : 0;
+    const int cnt_row = valid ? row_ptr[r + 1] - beg : 0;
+    const int maxcnt = __reduce_max_sync(0xffffffffu, cnt_row);
+    int dnet = 0;  // insertions - deletions (mean degree update)
+    for (int k = 0; k < nchunk; ++k) {
+      const int c = (k * G + gl) * V;
+      const bool cact = valid && c < w;
+      float acc[V];
+      int32_t arg[V];
+      float* accp = (KIND == kAggMean ? msum : values) + v * w + c;
+      if (cact) {
+        VecLoad<V>::ld_rw(acc, accp);
+        if (KIND == kAggMax || KIND == kAggMin) ld_int<V>(arg, argext + v * w + c);
+      }
+      for (int eb = 0; eb < maxcnt; eb += G) {
+        const int my_e = eb + gl;
+        const int32_t my_s = my_e < cnt_row ? ent[beg + my_e] : 0;
+        const int cnt = min(G, maxcnt - eb);
+        for (int j0 = 0; j0 < cnt; j0 += kUnroll) {
+          float x[kUnroll][V];
+          int32_t s[kUnroll];
+#pragma unroll
+          for (int q = 0; q < kUnroll; ++q) {
+            s[q] = __shfl_sync(0xffffffffu, my_s, (j0 + q) & (G - 1), G);
+            const bool live = cact && j0 + q < cnt && eb + j0 + q < cnt_row;
+            if (live) {
+              if (s[q] < 0) {
+                if (KIND == kAggSum || KIND == kAggMean)
+                  VecLoad<V>::ld(x[q], Fp + static_cast<int64_t>(~s[q]) * w + c);
+              } else {
+                VecLoad<V>::ld(x[q], Fc + static_cast<int64_t>(s[q]) * w + c);
+              }
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < kUnroll; ++q) {
+            const bool live = cact && j0 + q < cnt && eb + j0 + q < cnt_row;
+            if (!live) continue;
+            if (KIND == kAggSum || KIND == kAggMean) {
+              if (s[q] < 0) {
+#pragma unroll
+                for (int i = 0; i < V; ++i) acc[i] -= x[q][i];
+              } else {
+#pragma unroll
+                for (int i = 0; i < V; ++i) acc[i] += x[q][i];
+              }
+              if (k == 0) dnet += s[q] < 0 ? -1 : 1;
+            } else if (s[q] >= 0) {
+              accumulate<KIND, V>(acc, arg, x[q], s[q]);  // max/min: insert-only
+            }
+          }
+        }
+      }
+      if (cact) {
+        VecLoad<V>::st(accp, acc);
+        if (KIND == kAggMax || KIND == kAggMin) st_int<V>(argext + v * w + c, arg);
+      }
+    }
+    if (KIND == kAggMean) {
+      // Renormalise the touched row (ref src/aggregate.cpp:195-205).
+      const float dg = valid ? degree[v] + static_cast<float>(dnet) : 0.f;
+      const bool keep = dg > 1e-12f;
+      for (int k = 0; k < nchunk; ++k) {
+        const int c = (k * G + gl) * V;
+        if (!(valid && c < w)) continue;
+        float ms[V], r[V];
+        VecLoad<V>::ld_rw(ms, msum + v * w + c);
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          r[i] = keep ? ms[i] / dg : 0.f;
+          if (!keep) ms[i] = 0.f;
+        }
+        VecLoad<V>::st(values + v * w + c, r);
+        if (!keep) VecLoad<V>::st(msum + v * w + c, ms);
+      }
+      __syncwarp();
+      if (valid && gl == 0) degree[v] = keep ? dg : 0.f;
+    }
+  }
+}
+
+// Deleted-contributor test for max/min (ref src/aggregate.cpp:145-153).
+__global__ void k_deleted_contributor(int64_t n_del, int w, const uint64_t* __restrict__ del_keys,
+                                      const int32_t* __restrict__ argext, int32_t* flag) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n_del * w;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t e = i / w;
+    const int d = static_cast<int>(i - e * w);
+    const int32_t src = static_cast<int32_t>(del_keys[e] >> 32);
+    const int64_t dst = static_cast<int64_t>(del_keys[e] & 0xffffffffu);
+    if (argext[dst * w + d] == src) atomicOr(flag, 1);
+  }
+}
+
+// ---------------------------------------------------------------- K3 backward
+// grad[u] = sum_{v in out(u), ascending} s_v * up[v]; s_v = 1 (sum), 1/deg(v) (mean).
+template <int V, int G, bool MEAN>
+__global__ void __launch_bounds__(kThreads)
+k_agg_backward(int n, int w, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+               const float* __restrict__ up, const float* __restrict__ degree,
+               float* __restrict__ grad) {
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  constexpr int kRowsPerWarp = 32 / G;
+  const int64_t warp_global = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+  const int64_t warp_stride = (static_cast<int64_t>(gridDim.x) * kThreads) >> 5;
+  const int nchunk = (w + G * V - 1) / (G * V);
+  for (int64_t ubase = warp_global * kRowsPerWarp; ubase < n; ubase += warp_stride * kRowsPerWarp) {
+    const int64_t u = ubase + lane / G;
+    const bool valid = u < n;
+    const int64_t beg = valid ? ptr[u] : 0;
+    const int deg = valid ? static_cast<int>(ptr[u + 1] - beg) : 0;
+    const int maxdeg = __reduce_max_sync(0xffffffffu, deg);
+    for (int k = 0; k < nchunk; ++k) {
+      const int c = (k * G + gl) * V;
+      const bool cact = valid && c < w;
+      float acc[V];
+#pragma unroll
+      for (int i = 0; i < V; ++i) acc[i] = 0.f;
+      for (int eb = 0; eb < maxdeg; eb += G) {
+        const int my_e = eb + gl;
+        const int32_t my_v = my_e < deg ? idx[beg + my_e] : 0;
+        float my_s = 1.f;
+        if (MEAN && my_e < deg) my_s = 1.f / degree[my_v];
+        const int cnt = min(G, maxdeg - eb);
+        for (int j0 = 0; j0 < cnt; j0 += kUnroll) {
+          float x[kUnroll][V];
+          float sc[kUnroll];
+#pragma unroll
+          for (int q = 0; q < kUnroll; ++q) {
+            const int32_t vv = __shfl_sync(0xffffffffu, my_v, (j0 + q) & (G - 1), G);
+            sc[q] = MEAN ? __shfl_sync(0xffffffffu, my_s, (j0 + q) & (G - 1), G) : 1.f;
+            if (cact && j0 + q < cnt && eb + j0 + q < deg)
+              VecLoad<V>::ld(x[q], up + static_cast<int64_t>(vv) * w + c);
+          }
+#pragma unroll
+          for (int q = 0; q < kUnroll; ++q) {
+            if (cact && j0 + q < cnt && eb + j0 + q < deg) {
+#pragma unroll
+              for (int i = 0; i < V; ++i) acc[i] += MEAN ? sc[q] * x[q][i] : x[q][i];
+            }
+          }
+        }
+      }
+      if (cact) VecLoad<V>::st(grad + u * w + c, acc);
+    }
+  }
+}
+
+// max/min backward: route upstream to the recorded contributor.
+__global__ void k_agg_backward_ext(int64_t total, int w, const float* __restrict__ up,
+                                   const int32_t* __restrict__ argext, float* __restrict__ grad) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t u = argext[i];
+    if (u >= 0) {
+      const int d = static_cast<int>(i % w);
+      atomicAdd(grad + static_cast<int64_t>(u) * w + d, up[i]);
+    }
+  }
+}
+
+__global__ void k_mask_empty(int64_t total, int w, const int32_t* __restrict__ argext,
+                             const float* __restrict__ in, float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t v = i / w;
+    out[i] = argext[v * w] < 0 ? 0.f : in[i];
+  }
+}
+
+// ------------------------------------------------------------ dispatch
+int pick_vec(int w, const void* a, const void* b) {
+  auto al = [](const void* p, int bytes) {
+    return p == nullptr || (reinterpret_cast<uintptr_t>(p) % bytes) == 0;
+  };
+  if (w % 4 == 0 && al(a, 16) && al(b, 16)) return 4;
+  if (w % 2 == 0 && al(a, 8) && al(b, 8)) return 2;
+  return 1;
+}
+
+int pick_group(int w, int vec) {
+  int need = (w + vec - 1) / vec;
+  int g = 1;
+  while (g < need && g < 32) g <<= 1;
+  return g;
+}
+
+#define DGNN_DISPATCH_G(G_RUNTIME, ...)        \
+  switch (G_RUNTIME) {                         \
+    case 1: { constexpr int G = 1; __VA_ARGS__; } break;   \
+    case 2: { constexpr int G = 2; __VA_ARGS__; } break;   \
+    case 4: { constexpr int G = 4; __VA_ARGS__; } break;   \
+    case 8: { constexpr int G = 8; __VA_ARGS__; } break;   \
+    case 16: { constexpr int G = 16; __VA_ARGS__; } break; \
+    default: { constexpr int G = 32; __VA_ARGS__; } break; \
+  }
+
+#define DGNN_DISPATCH_V(V_RUNTIME, ...)                    \
+  switch (V_RUNTIME) {                                     \
+    case 4: { constexpr int V = 4; __VA_ARGS__; } break;   \
+    case 2: { constexpr int V = 2; __VA_ARGS__; } break;   \
+    default: { constexpr int V = 1; __VA_ARGS__; } break;  \
+  }
+
+#define DGNN_DISPATCH_KIND(K_RUNTIME, ...)                             \
+  switch (K_RUNTIME) {                                                 \
+    case kAggSum: { constexpr int KIND = kAggSum; __VA_ARGS__; } break;   \
+    case kAggMean: { constexpr int KIND = kAggMean; __VA_ARGS__; } break; \
+    case kAggMax: { constexpr int KIND = kAggMax; __VA_ARGS__; } break;   \
+    default: { constexpr int KIND = kAggMin; __VA_ARGS__; } break;        \
+  }
+
+int rows_grid(int64_t rows, int g) {
+  const int64_t rows_per_block = (kThreads / 32) * (32 / g);
+  return wave_grid(rows * kThreads / rows_per_block, kThreads, 8);
+}
+
+}  // namespace
+
+void agg_scratch(int kind, int n, int w, const int64_t* in_ptr, const int32_t* in_src,
+                 const float* feats, float* values, float* degree, float* mean_sums,
+                 int32_t* argext, cudaStream_t stream) {
+  if (n <= 0 || w <= 0) return;
+  const int vec = pick_vec(w, feats, values);
+  const int g = pick_group(w, vec);
+  const int grid = rows_grid(n, g);
+  DGNN_DISPATCH_KIND(kind, DGNN_DISPATCH_V(vec, DGNN_DISPATCH_G(g,
+      DGNN_LAUNCH((k_agg_scratch<V, G, KIND>), grid, kThreads, 0, stream, n, w, in_ptr, in_src,
+                  feats, values, degree, mean_sums, argext))));
+}
+
+void agg_delta(int kind, int n_rows, int w, const int32_t* rows, const int32_t* row_ptr,
+               const int32_t* ent, const float* f_prev, const float* f_curr, float* values,
+               float* degree, float* mean_sums, int32_t* argext, cudaStream_t stream) {
+  if (n_rows <= 0 || w <= 0) return;
+  const int vec = pick_vec(w, f_prev, values);
+  const int g = pick_group(w, vec);
+  const int grid = rows_grid(n_rows, g);
+  DGNN_DISPATCH_KIND(kind, DGNN_DISPATCH_V(vec, DGNN_DISPATCH_G(g,
+      DGNN_LAUNCH((k_agg_delta<V, G, KIND>), grid, kThreads, 0, stream, n_rows, w, rows, row_ptr,
+                  ent, f_prev, f_curr, values, degree, mean_sums, argext))));
+}
+
+void agg_deleted_contributor(int64_t n_del, int w, const uint64_t* del_keys,
+                             const int32_t* argext, int32_t* flag, cudaStream_t stream) {
+  if (n_del <= 0) return;
+  DGNN_LAUNCH(k_deleted_contributor, wave_grid(n_del * w, 256, 8), 256, 0, stream, n_del, w,
+              del_keys, argext, flag);
+}
+
+void agg_backward(int kind, int n, int w, const int64_t* out_ptr, const int32_t* out_dst,
+                  const float* up, const float* degree, const int32_t* argext, float* grad,
+                  cudaStream_t stream) {
+  if (n <= 0 || w <= 0) return;
+  if (kind == kAggMax || kind == kAggMin) {
+    DGNN_CUDA(cudaMemsetAsync(grad, 0, sizeof(float) * static_cast<size_t>(n) * w, stream));
+    const int64_t total = static_cast<int64_t>(n) * w;
+    DGNN_LAUNCH(k_agg_backward_ext, wave_grid(total, 256, 8), 256, 0, stream, total, w, up, argext,
+                grad);
+    return;
+  }
+  const int vec = pick_vec(w, up, grad);
+  const int g = pick_group(w, vec);
+  const int grid = rows_grid(n, g);
+  if (kind == kAggMean) {
+    DGNN_DISPATCH_V(vec, DGNN_DISPATCH_G(g,
+        DGNN_LAUNCH((k_agg_backward<V, G, true>), grid, kThreads, 0, stream, n, w, out_ptr,
+                    out_dst, up, degree, grad)));
+  } else {
+    DGNN_DISPATCH_V(vec, DGNN_DISPATCH_G(g,
+        DGNN_LAUNCH((k_agg_backward<V, G, false>), grid, kThreads, 0, stream, n, w, out_ptr,
+                    out_dst, up, degree, grad)));
+  }
+}
+
+void mask_empty_rows(int n, int w, const int32_t* argext, const float* in, float* out,
+                     cudaStream_t stream) {
+  const int64_t total = static_cast<int64_t>(n) * w;
+  if (total <= 0) return;
+  DGNN_LAUNCH(k_mask_empty, wave_grid(total, 256, 8), 256, 0, stream, total, w, argext, in, out);
+}
+
+}  // namespace cuda
+}  // namespace dgnn

@@ -1,0 +1,661 @@
+// extern "C" boundary (include/dgnn_b200.h) over the B200 host layer.
+#include "../../include/dgnn_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "host/synth.hpp"
+#include "host/train.hpp"
+
+using namespace dgnn;
+
+struct dgnn_graph {
+  std::unique_ptr<DeviceGraph> g;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+};
+
+struct dgnn_synth {
+  CompactGraph cg;
+};
+
+struct dgnn_session {
+  dgnn_graph* graph = nullptr;
+  dgnn_run_cfg cfg{};
+  ModelConfig mcfg;
+  TrainConfig tcfg;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::unique_ptr<TrainSession> seq;
+  std::unique_ptr<DistWorker> dist;
+  std::vector<double> losses;
+  std::vector<int64_t> events;
+  DgnnModel& model() { return seq ? seq->model() : dist->model(); }
+  Worker& worker() { return seq ? seq->worker() : dist->worker(); }
+  Timestep window_total() const {
+    return cfg.window_total > 0 ? cfg.window_total : graph->g->length() - 1;
+  }
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::out_of_range& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 3;
+  }
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+extern "C" {
+
+const char* dgnn_last_error(void) { return g_err.c_str(); }
+const char* dgnn_version(void) { return "paper_2501_15348_b200 0.1 (sm_100a)"; }
+int64_t dgnn_launch_count(void) { return cuda::launch_counter(); }
+int dgnn_synchronize(void* stream) {
+  return guarded([&] { DGNN_CUDA(cudaStreamSynchronize(as_stream(stream))); });
+}
+
+// ------------------------------------------------------------------ graph
+int dgnn_graph_create(int32_t num_nodes, int32_t feature_dim, void* stream, dgnn_graph** out) {
+  return guarded([&] {
+    auto h = std::make_unique<dgnn_graph>();
+    if (stream) {
+      h->stream = as_stream(stream);
+    } else {
+      DGNN_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+      h->own_stream = true;
+    }
+    h->g = std::make_unique<DeviceGraph>(num_nodes, feature_dim, h->stream);
+    *out = h.release();
+  });
+}
+
+void dgnn_graph_free(dgnn_graph* g) {
+  if (!g) return;
+  cudaStream_t s = g->stream;
+  bool own = g->own_stream;
+  g->g.reset();
+  cudaStreamSynchronize(s);
+  if (own) cudaStreamDestroy(s);
+  delete g;
+}
+
+int dgnn_graph_add_snapshot(dgnn_graph* g, const int32_t* src, const int32_t* dst,
+                            int64_t num_edges, const float* feats) {
+  return guarded([&] { g->g->add_snapshot(src, dst, num_edges, feats); });
+}
+
+int dgnn_graph_add_delta(dgnn_graph* g, const int32_t* del_src, const int32_t* del_dst,
+                         int64_t n_del, const int32_t* ins_src, const int32_t* ins_dst,
+                         int64_t n_ins, const int32_t* changed_nodes, int64_t n_changed,
+                         const float* changed_feats) {
+  return guarded([&] {
+    g->g->add_delta(del_src, del_dst, n_del, ins_src, ins_dst, n_ins, changed_nodes, n_changed,
+                    changed_feats);
+  });
+}
+
+int32_t dgnn_graph_length(const dgnn_graph* g) { return g->g->length(); }
+
+int64_t dgnn_graph_num_edges(const dgnn_graph* g, int32_t t) {
+  try {
+    return g->g->snapshot(t).num_edges;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+int dgnn_graph_snapshot(const dgnn_graph* g, int32_t t, const int64_t** in_ptr,
+                        const int32_t** in_src, const int64_t** out_ptr, const int32_t** out_dst,
+                        const float** feats) {
+  return guarded([&] {
+    const DevSnapshot& s = g->g->snapshot(t);
+    if (in_ptr) *in_ptr = s.in_ptr.get();
+    if (in_src) *in_src = s.in_src.get();
+    if (out_ptr) *out_ptr = s.out_ptr.get();
+    if (out_dst) *out_dst = s.out_dst.get();
+    if (feats) *feats = s.feats.get();
+  });
+}
+
+int dgnn_graph_delta_sizes(const dgnn_graph* g, int32_t t, int64_t* n_del, int64_t* n_ins,
+                           int64_t* n_changed, int64_t* n_rows, int64_t* u_minus,
+                           int64_t* u_plus) {
+  return guarded([&] {
+    const DevDelta& d = g->g->delta(t);
+    if (n_del) *n_del = d.n_del;
+    if (n_ins) *n_ins = d.n_ins;
+    if (n_changed) *n_changed = d.n_changed;
+    if (n_rows) *n_rows = d.n_rows;
+    if (u_minus) *u_minus = d.u_minus;
+    if (u_plus) *u_plus = d.u_plus;
+  });
+}
+
+int dgnn_graph_delta_copy(const dgnn_graph* g, int32_t t, int32_t* del_src, int32_t* del_dst,
+                          int32_t* ins_src, int32_t* ins_dst, int32_t* changed_nodes) {
+  return guarded([&] {
+    const DevDelta& d = g->g->delta(t);
+    auto split = [&](const cuda::DevArray<uint64_t>& keys, int64_t n, int32_t* s, int32_t* dd) {
+      std::vector<uint64_t> h(n);
+      copy_to_host(h.data(), keys.get(), sizeof(uint64_t) * n, g->stream);
+      for (int64_t i = 0; i < n; ++i) {
+        if (s) s[i] = static_cast<int32_t>(h[i] >> 32);
+        if (dd) dd[i] = static_cast<int32_t>(h[i] & 0xffffffffu);
+      }
+    };
+    split(d.del, d.n_del, del_src, del_dst);
+    split(d.ins, d.n_ins, ins_src, ins_dst);
+    if (changed_nodes) copy_to_host(changed_nodes, d.changed.get(), sizeof(int32_t) * d.n_changed, g->stream);
+  });
+}
+
+int dgnn_graph_delta_layout(const dgnn_graph* g, int32_t t, const int32_t** rows,
+                            const int32_t** row_ptr, const int32_t** ent) {
+  return guarded([&] {
+    const DevDelta& d = g->g->delta(t);
+    if (rows) *rows = d.rows.get();
+    if (row_ptr) *row_ptr = d.row_ptr.get();
+    if (ent) *ent = d.ent.get();
+  });
+}
+
+double dgnn_graph_change_ratio(const dgnn_graph* g, int32_t t) {
+  try {
+    return change_ratio(g->g->delta(t), g->g->snapshot(t - 1).num_edges);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1.0;
+  }
+}
+
+// ------------------------------------------------------------------ synth
+int dgnn_synth_create(int32_t num_nodes, double avg_degree, int32_t feature_dim,
+                      int32_t num_snapshots, double edge_change, double feature_change,
+                      uint64_t seed, dgnn_synth** out) {
+  return guarded([&] {
+    SynthParams p;
+    p.num_nodes = num_nodes;
+    p.avg_degree = avg_degree;
+    p.feature_dim = feature_dim;
+    p.num_snapshots = num_snapshots;
+    p.edge_change = edge_change;
+    p.feature_change = feature_change;
+    p.seed = seed;
+    auto s = std::make_unique<dgnn_synth>();
+    s->cg = synthesize_compact(p);
+    *out = s.release();
+  });
+}
+
+void dgnn_synth_free(dgnn_synth* s) { delete s; }
+
+int dgnn_synth_sizes(const dgnn_synth* s, int64_t* sizes) {
+  return guarded([&] {
+    sizes[0] = static_cast<int64_t>(s->cg.base_src.size());
+    for (size_t i = 0; i < s->cg.steps.size(); ++i) {
+      sizes[1 + 3 * i] = static_cast<int64_t>(s->cg.steps[i].del_src.size());
+      sizes[2 + 3 * i] = static_cast<int64_t>(s->cg.steps[i].ins_src.size());
+      sizes[3 + 3 * i] = static_cast<int64_t>(s->cg.steps[i].changed.size());
+    }
+  });
+}
+
+int dgnn_synth_base(const dgnn_synth* s, const int32_t** src, const int32_t** dst,
+                    const float** feats) {
+  return guarded([&] {
+    *src = s->cg.base_src.data();
+    *dst = s->cg.base_dst.data();
+    *feats = s->cg.base_feats.data();
+  });
+}
+
+int dgnn_synth_step(const dgnn_synth* s, int32_t t, const int32_t** del_src,
+                    const int32_t** del_dst, const int32_t** ins_src, const int32_t** ins_dst,
+                    const int32_t** changed, const float** changed_feats) {
+  return guarded([&] {
+    const CompactStep& st = s->cg.steps.at(t - 1);
+    *del_src = st.del_src.data();
+    *del_dst = st.del_dst.data();
+    *ins_src = st.ins_src.data();
+    *ins_dst = st.ins_dst.data();
+    *changed = st.changed.data();
+    *changed_feats = st.changed_feats.data();
+  });
+}
+
+int dgnn_synth_to_graph(const dgnn_synth* s, void* stream, dgnn_graph** out) {
+  return guarded([&] {
+    dgnn_graph* g = nullptr;
+    if (dgnn_graph_create(s->cg.num_nodes, s->cg.feature_dim, stream, &g) != 0)
+      throw std::runtime_error(g_err);
+    std::unique_ptr<dgnn_graph, void (*)(dgnn_graph*)> guard(g, dgnn_graph_free);
+    const CompactGraph& cg = s->cg;
+    g->g->add_snapshot(cg.base_src.data(), cg.base_dst.data(),
+                       static_cast<int64_t>(cg.base_src.size()), cg.base_feats.data());
+    for (const CompactStep& st : cg.steps) {
+      g->g->add_delta(st.del_src.data(), st.del_dst.data(), static_cast<int64_t>(st.del_src.size()),
+                      st.ins_src.data(), st.ins_dst.data(), static_cast<int64_t>(st.ins_src.size()),
+                      st.changed.data(), static_cast<int64_t>(st.changed.size()),
+                      st.changed_feats.data());
+    }
+    *out = guard.release();
+  });
+}
+
+// ------------------------------------------------------------ aggregation
+int dgnn_agg_scratch(int32_t kind, int32_t n, int32_t w, const int64_t* in_ptr,
+                     const int32_t* in_src, const float* feats, float* values, float* degree,
+                     float* mean_sums, int32_t* argext, void* stream) {
+  return guarded([&] {
+    check(kind >= 0 && kind <= 3, "unknown aggregation kind");
+    cuda::agg_scratch(kind, n, w, in_ptr, in_src, feats, values, degree, mean_sums, argext,
+                      as_stream(stream));
+  });
+}
+
+int dgnn_agg_delta(int32_t kind, int32_t n_rows, int32_t w, const int32_t* rows,
+                   const int32_t* row_ptr, const int32_t* ent, const float* f_prev,
+                   const float* f_curr, float* values, float* degree, float* mean_sums,
+                   int32_t* argext, void* stream) {
+  return guarded([&] {
+    check(kind >= 0 && kind <= 3, "unknown aggregation kind");
+    cuda::agg_delta(kind, n_rows, w, rows, row_ptr, ent, f_prev, f_curr, values, degree,
+                    mean_sums, argext, as_stream(stream));
+  });
+}
+
+int dgnn_agg_backward(int32_t kind, int32_t n, int32_t w, const int64_t* out_ptr,
+                      const int32_t* out_dst, const float* upstream, const float* degree,
+                      const int32_t* argext, float* grad, void* stream) {
+  return guarded([&] {
+    check(kind >= 0 && kind <= 3, "unknown aggregation kind");
+    cuda::agg_backward(kind, n, w, out_ptr, out_dst, upstream, degree, argext, grad,
+                       as_stream(stream));
+  });
+}
+
+int dgnn_agg_incremental(const dgnn_graph* g, int32_t t, int32_t kind, const float* prev_values,
+                         const float* prev_degree, const float* prev_mean_sums,
+                         const int32_t* prev_argext, int32_t prev_depth, int64_t prev_num_edges,
+                         double fallback_threshold, int32_t rescratch_period, float* values,
+                         float* degree, float* mean_sums, int32_t* argext, int32_t* info) {
+  return guarded([&] {
+    cudaStream_t st = g->stream;
+    const DeviceGraph& G = *g->g;
+    const int32_t n = G.num_nodes(), w = G.feature_dim();
+    const size_t nw = static_cast<size_t>(n) * w;
+    AggResult prev;
+    prev.kind = static_cast<AggrKind>(kind);
+    prev.rows = n;
+    prev.dim = w;
+    prev.t = t - 1;
+    prev.num_edges = prev_num_edges;
+    prev.incremental_depth = prev_depth;
+    auto cp = [&](auto& arr, const auto* src, size_t cnt) {
+      using T = std::remove_cv_t<std::remove_pointer_t<decltype(src)>>;
+      arr = cuda::DevArray<T>(cnt, st);
+      DGNN_CUDA(cudaMemcpyAsync(arr.get(), src, sizeof(T) * cnt, cudaMemcpyDeviceToDevice, st));
+    };
+    cp(prev.values, prev_values, nw);
+    if (kind == 1) {
+      cp(prev.degree, prev_degree, n);
+      cp(prev.mean_sums, prev_mean_sums, nw);
+    }
+    if (kind >= 2) cp(prev.argext, prev_argext, nw);
+    IncrementalResult r = aggregate_incremental(
+        prev, GraphView::of(G, t - 1), GraphView::of(G, t), G.snapshot(t - 1).feats.get(),
+        G.snapshot(t).feats.get(), G.delta(t), t, AggrFn{static_cast<AggrKind>(kind)},
+        IncrementalOptions{fallback_threshold, rescratch_period}, st);
+    DGNN_CUDA(cudaMemcpyAsync(values, r.result->values.get(), sizeof(float) * nw, cudaMemcpyDeviceToDevice, st));
+    if (kind == 1) {
+      DGNN_CUDA(cudaMemcpyAsync(degree, r.result->degree.get(), sizeof(float) * n, cudaMemcpyDeviceToDevice, st));
+      DGNN_CUDA(cudaMemcpyAsync(mean_sums, r.result->mean_sums.get(), sizeof(float) * nw, cudaMemcpyDeviceToDevice, st));
+    }
+    if (kind >= 2)
+      DGNN_CUDA(cudaMemcpyAsync(argext, r.result->argext.get(), sizeof(int32_t) * nw, cudaMemcpyDeviceToDevice, st));
+    DGNN_CUDA(cudaStreamSynchronize(st));
+    info[0] = r.used_fallback ? 1 : 0;
+    info[1] = static_cast<int32_t>(r.reason);
+    info[2] = r.result->incremental_depth;
+  });
+}
+
+// ------------------------------------------------------------------ cells
+int dgnn_pack_cell(int32_t lstm, int32_t in, int32_t H, const float* flat, float* W, float* bias,
+                   void* stream) {
+  return guarded([&] { cuda::pack_cell(lstm != 0, in, H, flat, W, bias, as_stream(stream)); });
+}
+
+int dgnn_cell_forward(int32_t lstm, int32_t n, int32_t in, int32_t H, const float* X,
+                      const float* Hm, const float* h_skip, const float* c_prev, const float* W,
+                      const float* bias, float* gates, float* c, float* h, void* stream) {
+  return guarded([&] {
+    cuda::cell_forward(lstm != 0, n, in, H, X, Hm, h_skip, c_prev, W, bias, gates, c, h,
+                       as_stream(stream));
+  });
+}
+
+int dgnn_cell_backward(int32_t lstm, int32_t n, int32_t in, int32_t H, const float* X,
+                       const float* Hm, const float* W, const float* gates, const float* c,
+                       const float* c_prev, const float* h_skip, const float* dh, const float* dc,
+                       float* dX, float* dHm, float* dc_prev, float* dh_skip, float* dflat,
+                       void* stream) {
+  return guarded([&] {
+    cudaStream_t st = as_stream(stream);
+    const int K = in + H;
+    cuda::DevArray<float> G(static_cast<size_t>(n) * 4 * H, st), WT(static_cast<size_t>(K) * 4 * H, st);
+    cuda::DevArray<float> dW(static_cast<size_t>(K) * 4 * H, st), db(4 * H, st);
+    cuda::DevArray<float> ws(cuda::gemm_tn_workspace(n, K, 4 * H), st);
+    dW.zero(st);
+    db.zero(st);
+    cuda::transpose(K, 4 * H, W, WT.get(), st);
+    cuda::cell_backward_pointwise(lstm != 0, n, H, gates, c, c_prev, h_skip, dh, dc, G.get(),
+                                  dc_prev, dh_skip, st);
+    cuda::gemm_tn_acc(n, in, H, 4 * H, X, Hm, G.get(), dW.get(), lstm ? 4 * H : 3 * H, db.get(),
+                      ws.get(), st);
+    if (dX) {
+      cuda::gemm_nn(n, 4 * H, 0, in, H, G.get(), nullptr, WT.get(), K, nullptr, false, false, dX,
+                    dHm, st);
+    } else {
+      cuda::gemm_nn(n, 4 * H, 0, H, 0, G.get(), nullptr, WT.get() + in, K, nullptr, false, false,
+                    dHm, nullptr, st);
+    }
+    cuda::unpack_cell_grad(lstm != 0, in, H, dW.get(), db.get(), dflat, st);
+    DGNN_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+// ---------------------------------------------------------------- trainer
+namespace {
+
+void fill_configs(dgnn_session* s) {
+  const dgnn_run_cfg& c = s->cfg;
+  ModelConfig& m = s->mcfg;
+  m.arch = static_cast<Architecture>(c.arch);
+  m.layers = c.layers;
+  m.feature_dim = s->graph->g->feature_dim();
+  m.hidden_dim = c.hidden;
+  m.seq_len = c.seq_len;
+  m.horizon = c.horizon;
+  m.teacher_forcing = c.teacher_forcing != 0;
+  check(c.aggr >= 0 && c.aggr <= 3, "unknown aggregation kind");
+  m.aggr = AggrFn{static_cast<AggrKind>(c.aggr)};
+  m.seed = c.seed;
+  TrainConfig& t = s->tcfg;
+  t.batch_size = c.batch_size;
+  t.epochs = c.epochs;
+  t.lr = c.lr;
+  t.optimizer = c.optimizer == 0 ? OptimizerKind::kSgd : OptimizerKind::kAdam;
+  t.stride = c.stride;
+  t.seed = c.seed;
+  t.fallback_threshold = c.fallback_threshold;
+  t.rescratch_period = c.rescratch_period;
+  t.incremental = c.incremental != 0;
+  if (c.cache_policy < 0) {
+    t.cache_policy = std::nullopt;
+  } else {
+    check(c.cache_policy <= 2, "unknown cache policy");
+    t.cache_policy = static_cast<CachePolicy>(c.cache_policy);
+  }
+  t.cache_capacity_frac = c.cache_frac;
+  t.hbm_cache_budget_bytes = c.hbm_cache_budget_bytes;
+}
+
+void attach_observer(dgnn_session* s) {
+  CacheStore* store = s->worker().store();
+  if (!store || !s->cfg.record_events) return;
+  store->set_observer([s](const CacheEvent& ev) {
+    const AggKey& k = ev.key;
+    const int64_t row[10] = {static_cast<int64_t>(ev.type), static_cast<int64_t>(k.level), k.layer, k.t,
+                             static_cast<int64_t>(k.kind), k.batch, k.step_serial, ev.hit ? 1 : 0,
+                             ev.assigned_f, ev.stored ? 1 : 0};
+    s->events.insert(s->events.end(), row, row + 10);
+  });
+}
+
+}  // namespace
+
+int dgnn_session_create(dgnn_graph* g, const dgnn_run_cfg* cfg, int32_t rank, void* stream,
+                        dgnn_session** out) {
+  return guarded([&] {
+    auto s = std::make_unique<dgnn_session>();
+    s->graph = g;
+    s->cfg = *cfg;
+    if (stream) {
+      s->stream = as_stream(stream);
+    } else {
+      s->stream = g->stream;
+    }
+    fill_configs(s.get());
+    if (cfg->workers <= 0) {
+      s->seq = std::make_unique<TrainSession>(*g->g, s->mcfg, s->tcfg, s->stream, cfg->window_total);
+    } else {
+      check(rank >= 0 && rank < cfg->workers, "rank must lie in [0, workers)");
+      s->dist = std::make_unique<DistWorker>(*g->g, s->mcfg, s->tcfg, s->stream, rank,
+                                             cfg->workers, cfg->window_total);
+    }
+    attach_observer(s.get());
+    *out = s.release();
+  });
+}
+
+void dgnn_session_free(dgnn_session* s) {
+  if (!s) return;
+  cudaStream_t st = s->stream;
+  s->seq.reset();
+  s->dist.reset();
+  cudaStreamSynchronize(st);
+  delete s;
+}
+
+int64_t dgnn_session_num_params(const dgnn_session* s) {
+  return const_cast<dgnn_session*>(s)->model().num_params();
+}
+
+int dgnn_session_num_windows(const dgnn_session* s, int64_t* total, int64_t* local_begin,
+                             int64_t* local_end) {
+  return guarded([&] {
+    if (s->seq) {
+      *total = static_cast<int64_t>(s->seq->windows().size());
+      *local_begin = 0;
+      *local_end = *total;
+    } else {
+      *total = s->dist->total_windows();
+      *local_begin = s->dist->assignment().window_begin;
+      *local_end = s->dist->assignment().window_end;
+    }
+  });
+}
+
+int dgnn_session_get_params(dgnn_session* s, double* out) {
+  return guarded([&] {
+    auto v = s->model().flatten_params();
+    std::memcpy(out, v.data(), sizeof(double) * v.size());
+  });
+}
+
+int dgnn_session_set_params(dgnn_session* s, const double* in) {
+  return guarded([&] {
+    std::vector<double> v(in, in + s->model().num_params());
+    s->model().unflatten_params(v);
+  });
+}
+
+int dgnn_session_initial_params(dgnn_session* s, double* out) {
+  return guarded([&] {
+    const auto& v = s->model().initial_params();
+    std::memcpy(out, v.data(), sizeof(double) * v.size());
+  });
+}
+
+int dgnn_session_run_epoch(dgnn_session* s, dgnn_epoch_report* report) {
+  return guarded([&] {
+    check(s->seq != nullptr, "run_epoch needs a seq-first session (workers = 0)");
+    EpochReport r = s->seq->run_epoch();
+    s->losses = r.sample_losses;
+    if (report) {
+      report->loss = r.loss;
+      report->seconds = r.seconds;
+      report->samples = static_cast<int64_t>(r.sample_losses.size());
+      report->hits = r.cache.hits;
+      report->misses = r.cache.misses;
+      report->evictions = r.cache.evictions;
+      report->expirations = r.cache.expirations;
+      report->invalidations = r.cache.invalidations;
+      report->rejected = r.cache.rejected;
+      report->scratch_calls = r.scratch_calls;
+      report->incremental_calls = r.incremental_calls;
+      report->fallbacks = r.fallbacks;
+      report->skipped_steps = r.skipped_steps;
+      report->spills = r.cache.spills;
+      report->refills = r.cache.refills;
+    }
+  });
+}
+
+int dgnn_session_begin_epoch(dgnn_session* s, int64_t* num_batches) {
+  return guarded([&] {
+    check(s->dist != nullptr, "sharded epochs need workers >= 1");
+    s->dist->begin_epoch();
+    if (num_batches) *num_batches = s->dist->num_batches();
+  });
+}
+
+int dgnn_session_local_grads(dgnn_session* s, int64_t batch, float* grad_sum) {
+  return guarded([&] {
+    check(s->dist != nullptr, "sharded epochs need workers >= 1");
+    check(batch >= 0 && batch < s->dist->num_batches(), "batch index out of range");
+    s->dist->local_grads(batch, grad_sum);
+  });
+}
+
+int dgnn_session_apply(dgnn_session* s, const float* grad_sum, int32_t* applied) {
+  return guarded([&] {
+    check(s->dist != nullptr, "sharded epochs need workers >= 1");
+    const bool ok = s->dist->apply(grad_sum);
+    if (applied) *applied = ok ? 1 : 0;
+  });
+}
+
+int dgnn_session_end_epoch(dgnn_session* s) {
+  return guarded([&] {
+    check(s->dist != nullptr, "sharded epochs need workers >= 1");
+    s->losses = s->dist->take_losses();
+    s->dist->end_epoch();
+  });
+}
+
+int dgnn_session_losses(dgnn_session* s, double* out, int64_t* n) {
+  return guarded([&] {
+    if (out) std::memcpy(out, s->losses.data(), sizeof(double) * s->losses.size());
+    *n = static_cast<int64_t>(s->losses.size());
+  });
+}
+
+int dgnn_session_sample_grads(dgnn_session* s, int32_t window_index, double* loss, float* pred0,
+                              double* grads) {
+  return guarded([&] {
+    DgnnModel& model = s->model();
+    const DeviceGraph& G = *s->graph->g;
+    cudaStream_t st = s->stream;
+    auto windows = sliding_windows(s->window_total(), s->mcfg.seq_len, s->tcfg.stride, s->mcfg.horizon);
+    check(window_index >= 0 && window_index < static_cast<int32_t>(windows.size()),
+          "window index out of range");
+    Worker fresh(G, model, s->tcfg, st);
+    auto batches = make_batches(G.num_nodes(), s->tcfg.batch_size, s->tcfg.seed, 0);
+    SeqSample sample = build_sample(G, s->mcfg, windows[window_index],
+                                    static_cast<Timestep>(windows.size() - 1 - window_index), 0,
+                                    batches[0]);
+    ForwardArtifacts fwd = model_forward(model, sample, fresh.provider());
+    cuda::DevArray<double> slot(1, st), ws(512, st);
+    slot.zero(st);
+    auto dpred = seed_loss(sample, fwd, s->mcfg.feature_dim, slot.get(), ws.get(), st);
+    cuda::DevArray<float> grad(model.num_params(), st);
+    grad.zero(st);
+    model_backward(model, sample, fwd, dpred, grad.get(), st);
+    copy_to_host(loss, slot.get(), sizeof(double), st);
+    if (pred0) {
+      copy_to_host(pred0, fwd.predictions[0]->get(),
+                   sizeof(float) * static_cast<size_t>(G.num_nodes()) * s->mcfg.feature_dim, st);
+    }
+    std::vector<float> g(model.num_params());
+    copy_to_host(g.data(), grad.get(), sizeof(float) * g.size(), st);
+    for (size_t i = 0; i < g.size(); ++i) grads[i] = g[i];
+  });
+}
+
+int dgnn_session_invocations(dgnn_session* s, int32_t* out, int64_t* n) {
+  return guarded([&] {
+    const auto& inv = s->worker().provider().stats().invocations;
+    *n = static_cast<int64_t>(inv.size());
+    if (!out) return;
+    for (size_t i = 0; i < inv.size(); ++i) {
+      out[4 * i + 0] = inv[i].layer;
+      out[4 * i + 1] = inv[i].t;
+      out[4 * i + 2] = static_cast<int32_t>(inv[i].kind);
+      out[4 * i + 3] = inv[i].incremental ? 1 : 0;
+    }
+  });
+}
+
+int dgnn_session_cache_events(dgnn_session* s, int64_t* out, int64_t* n) {
+  return guarded([&] {
+    *n = static_cast<int64_t>(s->events.size() / 10);
+    if (out) std::memcpy(out, s->events.data(), sizeof(int64_t) * s->events.size());
+  });
+}
+
+int dgnn_session_stats(dgnn_session* s, int64_t* out12) {
+  return guarded([&] {
+    CacheStore* store = s->worker().store();
+    CacheStats cs = store ? store->stats() : CacheStats{};
+    const ExecutionStats& es = s->worker().provider().stats();
+    const int64_t v[12] = {cs.hits, cs.misses, cs.evictions, cs.expirations, cs.invalidations,
+                           cs.rejected, es.scratch_calls, es.incremental_calls, es.fallbacks,
+                           cs.spills, cs.refills, static_cast<int64_t>(cs.resident_peak_units)};
+    std::memcpy(out12, v, sizeof(v));
+  });
+}
+
+// ---------------------------------------------------------------- profiling
+int dgnn_prof_enable(int32_t on) {
+  return guarded([&] { prof_enable(on != 0); });
+}
+int dgnn_prof_reset(void) {
+  return guarded([&] { prof_reset(); });
+}
+int dgnn_prof_get(int32_t cls, int64_t* launches, double* ms, double* bytes, double* flops) {
+  return guarded([&] {
+    prof_flush();
+    ProfStat p = prof_get(cls);
+    if (launches) *launches = p.launches;
+    if (ms) *ms = p.ms;
+    if (bytes) *bytes = p.bytes;
+    if (flops) *flops = p.flops;
+  });
+}
+
+}  // extern "C"

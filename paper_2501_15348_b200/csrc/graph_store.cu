@@ -1,0 +1,456 @@
+// Device graph store build: snapshot CSRs (K12) and extract_delta (K11).
+// Integer work only; every output is bit-exact with the reference
+// (src/snapshot.cpp:20-154). Sorting/selection/scans use CUB (CUDA toolkit
+// library primitives); the graph-specific passes are the kernels below.
+#include <cub/cub.cuh>
+
+#include <stdexcept>
+
+#include "common.cuh"
+#include "graph_store.h"
+
+namespace dgnn {
+
+using cuda::DevArray;
+
+namespace {
+
+constexpr int kT = 256;
+
+__global__ void k_make_keys(int64_t n, const int32_t* __restrict__ src,
+                            const int32_t* __restrict__ dst, int32_t num_nodes,
+                            uint64_t* __restrict__ keys, int32_t* __restrict__ flag) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t s = src[i], d = dst[i];
+    if (s < 0 || s >= num_nodes || d < 0 || d >= num_nodes) atomicOr(flag, 1);
+    keys[i] = (static_cast<uint64_t>(static_cast<uint32_t>(s)) << 32) | static_cast<uint32_t>(d);
+  }
+}
+
+__global__ void k_adjacent_dup(int64_t n, const uint64_t* __restrict__ keys, int32_t* flag) {
+  for (int64_t i = 1 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    if (keys[i] == keys[i - 1]) atomicOr(flag, 2);
+}
+
+__device__ __forceinline__ bool bsearch_u64(const uint64_t* __restrict__ a, int64_t n, uint64_t k) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (a[mid] < k) lo = mid + 1; else hi = mid;
+  }
+  return lo < n && a[lo] == k;
+}
+
+// keep[i] = (a[i] found in b) == want_found
+__global__ void k_mark(int64_t na, const uint64_t* __restrict__ a, int64_t nb,
+                       const uint64_t* __restrict__ b, int want_found, uint8_t* __restrict__ keep) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < na;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    keep[i] = bsearch_u64(b, nb, a[i]) == (want_found != 0);
+}
+
+__global__ void k_hist_hi(int64_t n, const uint64_t* __restrict__ keys,
+                          unsigned long long* __restrict__ counts) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    atomicAdd(counts + (keys[i] >> 32), 1ull);
+}
+
+__global__ void k_low32(int64_t n, const uint64_t* __restrict__ keys, int32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<int32_t>(keys[i] & 0xffffffffu);
+}
+
+__global__ void k_swap_halves(int64_t n, const uint64_t* __restrict__ in, uint64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = (in[i] << 32) | (in[i] >> 32);
+}
+
+// changed[u] = any component of row u differs exactly (ref src/snapshot.cpp:113-115)
+__global__ void k_row_differs(int32_t n, int32_t d, const float* __restrict__ a,
+                              const float* __restrict__ b, uint8_t* __restrict__ flags) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t u = warp; u < n; u += nwarps) {
+    int diff = 0;
+    for (int j = lane; j < d; j += 32) diff |= a[u * d + j] != b[u * d + j];
+    diff = __any_sync(0xffffffffu, diff);
+    if (lane == 0) flags[u] = diff ? 1 : 0;
+  }
+}
+
+__global__ void k_iota(int32_t n, int32_t* out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<int32_t>(i);
+}
+
+__global__ void k_out_degree_of(int64_t m, const int32_t* __restrict__ nodes,
+                                const int64_t* __restrict__ out_ptr, int64_t* __restrict__ cnt) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    cnt[i] = out_ptr[nodes[i] + 1] - out_ptr[nodes[i]];
+}
+
+// out-edges of the listed nodes, appended at offsets (exclusive scan of degrees)
+__global__ void k_expand(int64_t m, const int32_t* __restrict__ nodes,
+                         const int64_t* __restrict__ out_ptr, const int32_t* __restrict__ out_dst,
+                         const int64_t* __restrict__ offs, uint64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t u = nodes[i];
+    const uint64_t hi = static_cast<uint64_t>(static_cast<uint32_t>(u)) << 32;
+    int64_t o = offs[i];
+    for (int64_t e = out_ptr[u]; e < out_ptr[u + 1]; ++e) out[o++] = hi | static_cast<uint32_t>(out_dst[e]);
+  }
+}
+
+// composite key for the dst-grouped layout: dst << 33 | is_ins << 32 | src
+__global__ void k_composite(int64_t n, const uint64_t* __restrict__ keys, uint64_t is_ins,
+                            uint64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t s = keys[i] >> 32, d = keys[i] & 0xffffffffu;
+    out[i] = (d << 33) | (is_ins << 32) | s;
+  }
+}
+
+__global__ void k_split_composite(int64_t n, const uint64_t* __restrict__ comp,
+                                  int32_t* __restrict__ dsts, int32_t* __restrict__ ent) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t c = comp[i];
+    dsts[i] = static_cast<int32_t>(c >> 33);
+    const int32_t s = static_cast<int32_t>(c & 0xffffffffu);
+    ent[i] = (c >> 32) & 1u ? s : ~s;
+  }
+}
+
+__global__ void k_count_heads(int64_t n, const uint64_t* __restrict__ keys,
+                              unsigned long long* __restrict__ out) {
+  unsigned long long c = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    c += (i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32)) ? 1 : 0;
+  if (c) atomicAdd(out, c);
+}
+
+__global__ void k_scatter_rows(int64_t m, int32_t d, const int32_t* __restrict__ nodes,
+                               const float* __restrict__ rows, float* __restrict__ feats) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m * d;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / d;
+    feats[static_cast<int64_t>(nodes[r]) * d + (i - r * d)] = rows[i];
+  }
+}
+
+int grid_for(int64_t n) { return cuda::wave_grid(n, kT, 8); }
+
+// Thin CUB wrappers with a growable temp buffer.
+struct Cub {
+  cudaStream_t st;
+  DevArray<uint8_t> tmp;
+  explicit Cub(cudaStream_t s) : st(s) {}
+  void* get(size_t bytes) {
+    if (bytes > tmp.size()) tmp = DevArray<uint8_t>(bytes + (bytes >> 2) + 256, st);
+    return tmp.get();
+  }
+  void sort(const uint64_t* in, uint64_t* out, int64_t n, int end_bit = 64) {
+    if (n == 0) return;
+    size_t b = 0;
+    DGNN_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, b, in, out, n, 0, end_bit, st));
+    DGNN_CUDA(cub::DeviceRadixSort::SortKeys(get(b), b, in, out, n, 0, end_bit, st));
+  }
+  template <typename T>
+  int64_t select_flagged(const T* in, const uint8_t* flags, T* out, int64_t n) {
+    if (n == 0) return 0;
+    DevArray<int64_t> cnt(1, st);
+    size_t b = 0;
+    DGNN_CUDA(cub::DeviceSelect::Flagged(nullptr, b, in, flags, out, cnt.get(), n, st));
+    DGNN_CUDA(cub::DeviceSelect::Flagged(get(b), b, in, flags, out, cnt.get(), n, st));
+    return read(cnt.get());
+  }
+  int64_t unique(const uint64_t* in, uint64_t* out, int64_t n) {
+    if (n == 0) return 0;
+    DevArray<int64_t> cnt(1, st);
+    size_t b = 0;
+    DGNN_CUDA(cub::DeviceSelect::Unique(nullptr, b, in, out, cnt.get(), n, st));
+    DGNN_CUDA(cub::DeviceSelect::Unique(get(b), b, in, out, cnt.get(), n, st));
+    return read(cnt.get());
+  }
+  template <typename TI, typename TO>
+  void exclusive_sum(const TI* in, TO* out, int64_t n) {
+    if (n == 0) return;
+    size_t b = 0;
+    DGNN_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b, in, out, n, st));
+    DGNN_CUDA(cub::DeviceScan::ExclusiveSum(get(b), b, in, out, n, st));
+  }
+  int64_t rle(const int32_t* in, int32_t* uniq, int32_t* counts, int64_t n) {
+    if (n == 0) return 0;
+    DevArray<int64_t> cnt(1, st);
+    size_t b = 0;
+    DGNN_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, b, in, uniq, counts, cnt.get(), n, st));
+    DGNN_CUDA(cub::DeviceRunLengthEncode::Encode(get(b), b, in, uniq, counts, cnt.get(), n, st));
+    return read(cnt.get());
+  }
+  int64_t read(const int64_t* d) {
+    int64_t h = 0;
+    DGNN_CUDA(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
+    DGNN_CUDA(cudaStreamSynchronize(st));
+    return h;
+  }
+};
+
+template <typename T>
+DevArray<T> upload(const T* host, int64_t n, cudaStream_t st) {
+  DevArray<T> d(static_cast<size_t>(n), st);
+  if (n > 0) DGNN_CUDA(cudaMemcpyAsync(d.get(), host, sizeof(T) * n, cudaMemcpyHostToDevice, st));
+  return d;
+}
+
+int32_t read_flag(DevArray<int32_t>& f, cudaStream_t st) {
+  int32_t h = 0;
+  DGNN_CUDA(cudaMemcpyAsync(&h, f.get(), sizeof(h), cudaMemcpyDeviceToHost, st));
+  DGNN_CUDA(cudaStreamSynchronize(st));
+  return h;
+}
+
+// Sorted unique keys from an edge list; reference Snapshot ctor checks.
+DevArray<uint64_t> sorted_edge_keys(const int32_t* src_h, const int32_t* dst_h, int64_t n,
+                                    int32_t num_nodes, Cub& cub, bool reject_dups) {
+  cudaStream_t st = cub.st;
+  DevArray<int32_t> s = upload(src_h, n, st), d = upload(dst_h, n, st);
+  DevArray<uint64_t> raw(n, st), keys(n, st);
+  DevArray<int32_t> flag(1, st);
+  flag.zero(st);
+  if (n > 0) {
+    DGNN_LAUNCH(k_make_keys, grid_for(n), kT, 0, st, n, s.get(), d.get(), num_nodes, raw.get(), flag.get());
+    cub.sort(raw.get(), keys.get(), n);
+    if (reject_dups) DGNN_LAUNCH(k_adjacent_dup, grid_for(n), kT, 0, st, n, keys.get(), flag.get());
+  }
+  const int32_t f = read_flag(flag, st);
+  if (f & 1) throw std::invalid_argument("edge endpoint out of range");
+  if (f & 2) throw std::invalid_argument("duplicate edge in snapshot");
+  return keys;
+}
+
+}  // namespace
+
+void copy_to_host(void* dst, const void* src, size_t bytes, cudaStream_t stream) {
+  if (bytes == 0) return;
+  DGNN_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream));
+  DGNN_CUDA(cudaStreamSynchronize(stream));
+}
+
+DeviceGraph::DeviceGraph(int32_t num_nodes, int32_t feature_dim, cudaStream_t stream)
+    : n_(num_nodes), d_(feature_dim), stream_(stream) {
+  if (num_nodes <= 0) throw std::invalid_argument("snapshot needs at least one node");
+  if (feature_dim <= 0) throw std::invalid_argument("feature_dim must be positive");
+}
+
+DeviceGraph::~DeviceGraph() = default;
+
+const DevSnapshot& DeviceGraph::snapshot(int32_t t) const {
+  if (t < 0 || t >= length()) throw std::out_of_range("snapshot index out of range");
+  return snaps_[t];
+}
+
+const DevDelta& DeviceGraph::delta(int32_t t) const {
+  if (!(t >= 1 && t < length())) throw std::invalid_argument("delta index out of range");
+  return deltas_[t];
+}
+
+int64_t DeviceGraph::device_bytes() const {
+  int64_t b = 0;
+  for (const auto& s : snaps_)
+    b += s.in_ptr.bytes() + s.out_ptr.bytes() + s.in_src.bytes() + s.out_dst.bytes() + s.feats.bytes();
+  for (const auto& d : deltas_)
+    b += d.del.bytes() + d.ins.bytes() + d.changed.bytes() + d.rows.bytes() + d.row_ptr.bytes() + d.ent.bytes();
+  return b;
+}
+
+void DeviceGraph::add_snapshot(const int32_t* src, const int32_t* dst, int64_t num_edges,
+                               const float* feats) {
+  Cub cub(stream_);
+  DevArray<uint64_t> keys = sorted_edge_keys(src, dst, num_edges, n_, cub, true);
+  DevArray<float> f = upload(feats, static_cast<int64_t>(n_) * d_, stream_);
+  finish_snapshot(std::move(keys), std::move(f));
+}
+
+void DeviceGraph::add_delta(const int32_t* del_src, const int32_t* del_dst, int64_t n_del,
+                            const int32_t* ins_src, const int32_t* ins_dst, int64_t n_ins,
+                            const int32_t* changed_nodes, int64_t n_changed,
+                            const float* changed_feats) {
+  if (snaps_.empty()) throw std::invalid_argument("add_delta needs a previous snapshot");
+  cudaStream_t st = stream_;
+  Cub cub(st);
+  DevArray<uint64_t> del = sorted_edge_keys(del_src, del_dst, n_del, n_, cub, false);
+  DevArray<uint64_t> ins = sorted_edge_keys(ins_src, ins_dst, n_ins, n_, cub, true);
+  const int64_t E0 = static_cast<int64_t>(curr_keys_.size());
+  // prev \ deletions
+  DevArray<uint8_t> keep(E0, st);
+  DevArray<uint64_t> cat(E0 + n_ins, st);
+  int64_t kept = E0;
+  if (E0 > 0) {
+    DGNN_LAUNCH(k_mark, grid_for(E0), kT, 0, st, E0, curr_keys_.get(), n_del, del.get(), 0, keep.get());
+    kept = cub.select_flagged(curr_keys_.get(), keep.get(), cat.get(), E0);
+  }
+  // U insertions (set_union: common elements once)
+  if (n_ins > 0)
+    DGNN_CUDA(cudaMemcpyAsync(cat.get() + kept, ins.get(), sizeof(uint64_t) * n_ins,
+                              cudaMemcpyDeviceToDevice, st));
+  const int64_t m = kept + n_ins;
+  DevArray<uint64_t> sorted(m, st), keys(m, st);
+  cub.sort(cat.get(), sorted.get(), m);
+  const int64_t E1 = cub.unique(sorted.get(), keys.get(), m);
+  DevArray<uint64_t> exact(E1, st);
+  if (E1 > 0)
+    DGNN_CUDA(cudaMemcpyAsync(exact.get(), keys.get(), sizeof(uint64_t) * E1, cudaMemcpyDeviceToDevice, st));
+  // features: prev rows with the changed rows replaced
+  const int64_t nf = static_cast<int64_t>(n_) * d_;
+  DevArray<float> f(nf, st);
+  DGNN_CUDA(cudaMemcpyAsync(f.get(), snaps_.back().feats.get(), sizeof(float) * nf,
+                            cudaMemcpyDeviceToDevice, st));
+  if (n_changed > 0) {
+    DevArray<int32_t> nodes = upload(changed_nodes, n_changed, st);
+    DevArray<float> rows = upload(changed_feats, n_changed * d_, st);
+    DGNN_LAUNCH(k_scatter_rows, grid_for(n_changed * d_), kT, 0, st, n_changed, d_, nodes.get(),
+                rows.get(), f.get());
+  }
+  finish_snapshot(std::move(exact), std::move(f));
+}
+
+void DeviceGraph::finish_snapshot(DevArray<uint64_t> keys, DevArray<float> feats) {
+  cudaStream_t st = stream_;
+  Cub cub(st);
+  const int64_t E = static_cast<int64_t>(keys.size());
+  DevSnapshot s;
+  s.num_edges = E;
+  s.feats = std::move(feats);
+  // out-CSR: keys already sorted by (src, dst)
+  DevArray<unsigned long long> cnt(n_ + 1, st);
+  cnt.zero(st);
+  s.out_ptr = DevArray<int64_t>(n_ + 1, st);
+  s.out_dst = DevArray<int32_t>(E, st);
+  if (E > 0) {
+    DGNN_LAUNCH(k_hist_hi, grid_for(E), kT, 0, st, E, keys.get(), cnt.get());
+    DGNN_LAUNCH(k_low32, grid_for(E), kT, 0, st, E, keys.get(), s.out_dst.get());
+  }
+  cub.exclusive_sum(reinterpret_cast<const int64_t*>(cnt.get()), s.out_ptr.get(), n_ + 1);
+  // in-CSR: sort by (dst, src)
+  s.in_ptr = DevArray<int64_t>(n_ + 1, st);
+  s.in_src = DevArray<int32_t>(E, st);
+  cnt.zero(st);
+  if (E > 0) {
+    DevArray<uint64_t> sw(E, st), sw_sorted(E, st);
+    DGNN_LAUNCH(k_swap_halves, grid_for(E), kT, 0, st, E, keys.get(), sw.get());
+    cub.sort(sw.get(), sw_sorted.get(), E);
+    DGNN_LAUNCH(k_hist_hi, grid_for(E), kT, 0, st, E, sw_sorted.get(), cnt.get());
+    DGNN_LAUNCH(k_low32, grid_for(E), kT, 0, st, E, sw_sorted.get(), s.in_src.get());
+  }
+  cub.exclusive_sum(reinterpret_cast<const int64_t*>(cnt.get()), s.in_ptr.get(), n_ + 1);
+  snaps_.push_back(std::move(s));
+  deltas_.emplace_back();
+  prev_keys_ = std::move(curr_keys_);
+  curr_keys_ = std::move(keys);
+  if (snaps_.size() >= 2) build_delta(static_cast<int32_t>(snaps_.size()) - 1);
+  prev_keys_.reset();
+}
+
+void DeviceGraph::build_delta(int32_t t) {
+  cudaStream_t st = stream_;
+  Cub cub(st);
+  const DevSnapshot& P = snaps_[t - 1];
+  const DevSnapshot& Cs = snaps_[t];
+  const int64_t Ep = P.num_edges, Ec = Cs.num_edges;
+  DevDelta dd;
+  // changed nodes (exact row inequality), ascending
+  DevArray<uint8_t> fl(n_, st);
+  DGNN_LAUNCH(k_row_differs, cuda::wave_grid(static_cast<int64_t>(n_) * 32, kT, 8), kT, 0, st, n_,
+              d_, P.feats.get(), Cs.feats.get(), fl.get());
+  DevArray<int32_t> iota(n_, st);
+  DGNN_LAUNCH(k_iota, grid_for(n_), kT, 0, st, n_, iota.get());
+  DevArray<int32_t> changed(n_, st);
+  dd.n_changed = cub.select_flagged(iota.get(), fl.get(), changed.get(), n_);
+  dd.changed = DevArray<int32_t>(dd.n_changed, st);
+  if (dd.n_changed)
+    DGNN_CUDA(cudaMemcpyAsync(dd.changed.get(), changed.get(), sizeof(int32_t) * dd.n_changed,
+                              cudaMemcpyDeviceToDevice, st));
+  // expansion sizes
+  auto expansion = [&](const DevSnapshot& S, int64_t* total) {
+    DevArray<int64_t> deg(dd.n_changed + 1, st), off(dd.n_changed + 1, st);
+    deg.zero(st);
+    if (dd.n_changed)
+      DGNN_LAUNCH(k_out_degree_of, grid_for(dd.n_changed), kT, 0, st, dd.n_changed,
+                  dd.changed.get(), S.out_ptr.get(), deg.get());
+    cub.exclusive_sum(deg.get(), off.get(), dd.n_changed + 1);
+    *total = cub.read(off.get() + dd.n_changed);
+    return off;
+  };
+  auto side = [&](const uint64_t* a, int64_t na, const uint64_t* b, int64_t nb,
+                  const DevSnapshot& S, int64_t* out_n) {
+    int64_t nexp = 0;
+    DevArray<int64_t> off = expansion(S, &nexp);
+    DevArray<uint8_t> keep(na, st);
+    DevArray<uint64_t> cat(na + nexp, st);
+    int64_t nd = 0;
+    if (na > 0) {
+      DGNN_LAUNCH(k_mark, grid_for(na), kT, 0, st, na, a, nb, b, 0, keep.get());
+      nd = cub.select_flagged(a, keep.get(), cat.get(), na);
+    }
+    if (nexp > 0)
+      DGNN_LAUNCH(k_expand, grid_for(dd.n_changed), kT, 0, st, dd.n_changed, dd.changed.get(),
+                  S.out_ptr.get(), S.out_dst.get(), off.get(), cat.get() + nd);
+    const int64_t m = nd + nexp;
+    DevArray<uint64_t> sorted(m, st), uniq(m, st);
+    cub.sort(cat.get(), sorted.get(), m);
+    *out_n = cub.unique(sorted.get(), uniq.get(), m);
+    DevArray<uint64_t> out(*out_n, st);
+    if (*out_n)
+      DGNN_CUDA(cudaMemcpyAsync(out.get(), uniq.get(), sizeof(uint64_t) * *out_n,
+                                cudaMemcpyDeviceToDevice, st));
+    return out;
+  };
+  dd.del = side(prev_keys_.get(), Ep, curr_keys_.get(), Ec, P, &dd.n_del);
+  dd.ins = side(curr_keys_.get(), Ec, prev_keys_.get(), Ep, Cs, &dd.n_ins);
+  // distinct sources per side
+  DevArray<unsigned long long> heads(2, st);
+  heads.zero(st);
+  if (dd.n_del) DGNN_LAUNCH(k_count_heads, grid_for(dd.n_del), kT, 0, st, dd.n_del, dd.del.get(), heads.get());
+  if (dd.n_ins) DGNN_LAUNCH(k_count_heads, grid_for(dd.n_ins), kT, 0, st, dd.n_ins, dd.ins.get(), heads.get() + 1);
+  unsigned long long hh[2];
+  copy_to_host(hh, heads.get(), sizeof(hh), st);
+  dd.u_minus = static_cast<int64_t>(hh[0]);
+  dd.u_plus = static_cast<int64_t>(hh[1]);
+  // dst-grouped signed layout: deletions then insertions per destination
+  const int64_t ne = dd.n_del + dd.n_ins;
+  dd.n_ent = ne;
+  DevArray<uint64_t> comp(ne, st), comp_sorted(ne, st);
+  if (dd.n_del) DGNN_LAUNCH(k_composite, grid_for(dd.n_del), kT, 0, st, dd.n_del, dd.del.get(), 0ull, comp.get());
+  if (dd.n_ins)
+    DGNN_LAUNCH(k_composite, grid_for(dd.n_ins), kT, 0, st, dd.n_ins, dd.ins.get(), 1ull,
+                comp.get() + dd.n_del);
+  cub.sort(comp.get(), comp_sorted.get(), ne);
+  DevArray<int32_t> dsts(ne, st);
+  dd.ent = DevArray<int32_t>(ne, st);
+  if (ne) DGNN_LAUNCH(k_split_composite, grid_for(ne), kT, 0, st, ne, comp_sorted.get(), dsts.get(), dd.ent.get());
+  DevArray<int32_t> uniq(ne, st), counts(ne + 1, st);
+  const int64_t nr = cub.rle(dsts.get(), uniq.get(), counts.get(), ne);
+  dd.n_rows = static_cast<int32_t>(nr);
+  dd.rows = DevArray<int32_t>(nr, st);
+  dd.row_ptr = DevArray<int32_t>(nr + 1, st);
+  if (nr) {
+    DGNN_CUDA(cudaMemcpyAsync(dd.rows.get(), uniq.get(), sizeof(int32_t) * nr, cudaMemcpyDeviceToDevice, st));
+    DGNN_CUDA(cudaMemsetAsync(counts.get() + nr, 0, sizeof(int32_t), st));
+  }
+  cub.exclusive_sum(counts.get(), dd.row_ptr.get(), nr + 1);
+  DGNN_CUDA(cudaStreamSynchronize(st));
+  deltas_[t] = std::move(dd);
+}
+
+}  // namespace dgnn

@@ -1,0 +1,234 @@
+// Trainers: seq-first (ref src/train.cpp) and consecutive-block sharded
+// (ref src/distsim.cpp) over the device model.
+#include "train.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <random>
+
+namespace dgnn {
+
+std::vector<std::pair<NodeId, NodeId>> make_batches(NodeId num_nodes, int batch_size, uint64_t seed,
+                                                    int64_t epoch_index) {
+  if (batch_size <= 0 || batch_size >= num_nodes) return {{0, num_nodes}};
+  std::vector<std::pair<NodeId, NodeId>> ranges;
+  for (NodeId begin = 0; begin < num_nodes; begin += batch_size) {
+    ranges.push_back({begin, std::min<NodeId>(begin + batch_size, num_nodes)});
+  }
+  std::mt19937_64 rng(derive_seed(seed, 0xba7c4, static_cast<uint64_t>(epoch_index)));
+  std::shuffle(ranges.begin(), ranges.end(), rng);
+  return ranges;
+}
+
+double cache_data_size_units(const DeviceGraph& graph, const ModelConfig& mcfg) {
+  return 2.0 * static_cast<double>(mcfg.seq_len) * static_cast<double>(graph.num_nodes()) *
+         static_cast<double>(graph.feature_dim());
+}
+
+bool optimizer_step(DgnnModel& model, const float* grads, float gscale, OptimizerState& state,
+                    const TrainConfig& cfg, CacheStore* store, cudaStream_t stream) {
+  const int64_t P = model.num_params();
+  cuda::DevArray<int32_t> flag(1, stream);
+  flag.zero(stream);
+  cuda::nonfinite_check(P, grads, flag.get(), stream);
+  int32_t bad = 0;
+  copy_to_host(&bad, flag.get(), sizeof(bad), stream);
+  if (bad) return false;
+  state.step_count += 1;
+  if (!state.m) {
+    state.m = cuda::DevArray<float>(P, stream);
+    state.v = cuda::DevArray<float>(P, stream);
+    state.m.zero(stream);
+    state.v.zero(stream);
+  }
+  const double bc1 = 1.0 - std::pow(cfg.beta1, static_cast<double>(state.step_count));
+  const double bc2 = 1.0 - std::pow(cfg.beta2, static_cast<double>(state.step_count));
+  {
+    ProfScope ps(kProfOther, stream, 4.0 * P * 5);
+    cuda::adam_step(P, model.params(), state.m.get(), state.v.get(), grads, gscale,
+                    static_cast<float>(cfg.lr), static_cast<float>(cfg.beta1),
+                    static_cast<float>(cfg.beta2), static_cast<float>(cfg.adam_eps),
+                    static_cast<float>(bc1), static_cast<float>(bc2),
+                    cfg.optimizer == OptimizerKind::kSgd, nullptr, stream);
+  }
+  model.refresh_packed();
+  if (store != nullptr) store->bump_epoch();
+  return true;
+}
+
+// ---------------------------------------------------------------- Worker
+Worker::Worker(const DeviceGraph& graph, DgnnModel& model, const TrainConfig& cfg, cudaStream_t stream)
+    : graph_(graph), model_(model), cfg_(cfg), stream_(stream) {
+  if (cfg.cache_policy) {
+    const double capacity = cfg.cache_capacity_frac * cache_data_size_units(graph, model.cfg_);
+    store_ = std::make_unique<CacheStore>(*cfg.cache_policy, capacity);
+    if (cfg.hbm_cache_budget_bytes > 0) {
+      cudaStream_t copy;
+      DGNN_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+      store_->set_hbm_budget(cfg.hbm_cache_budget_bytes, stream, copy);
+    }
+  }
+  IncrementalOptions inc{cfg.fallback_threshold, cfg.rescratch_period};
+  provider_ = std::make_unique<AggProvider>(store_.get(), &graph, model.cfg_.aggr, cfg.incremental,
+                                            inc, stream);
+  loss_ws_ = cuda::DevArray<double>(512, stream);
+}
+
+Worker::~Worker() = default;
+
+void Worker::run_sample(const SequenceWindow& window, Timestep windows_remaining, int64_t batch_id,
+                        std::pair<NodeId, NodeId> node_range, float* grad, double* loss_slot) {
+  SeqSample sample = build_sample(graph_, model_.cfg_, window, windows_remaining, batch_id, node_range);
+  ForwardArtifacts fwd = model_forward(model_, sample, *provider_);
+  std::vector<Buf> dpred = seed_loss(sample, fwd, model_.cfg_.feature_dim, loss_slot, loss_ws_.get(), stream_);
+  model_backward(model_, sample, fwd, dpred, grad, stream_);
+}
+
+// ---------------------------------------------------------------- seq-first
+EpochReport seq_first_epoch(DgnnModel& model, const DeviceGraph& graph,
+                            const std::vector<SequenceWindow>& windows, const TrainConfig& cfg,
+                            Worker& worker, OptimizerState& opt, int64_t epoch_index) {
+  check(!windows.empty(), "epoch needs at least one window");
+  cudaStream_t st = worker.stream();
+  AggProvider& provider = worker.provider();
+  const CacheStats stats0 = provider.store() ? provider.store()->stats() : CacheStats{};
+  const ExecutionStats exec0 = provider.stats();
+  cudaEvent_t e0, e1;
+  DGNN_CUDA(cudaEventCreate(&e0));
+  DGNN_CUDA(cudaEventCreate(&e1));
+  DGNN_CUDA(cudaEventRecord(e0, st));
+  provider.reset_plan_state();
+  EpochReport report;
+  auto batches = make_batches(graph.num_nodes(), cfg.batch_size, cfg.seed, epoch_index);
+  const int64_t nsamples = static_cast<int64_t>(batches.size() * windows.size());
+  cuda::DevArray<double> losses(nsamples, st);
+  losses.zero(st);
+  cuda::DevArray<float> grad(model.num_params(), st);
+  int64_t k = 0;
+  for (int64_t b = 0; b < static_cast<int64_t>(batches.size()); ++b) {
+    for (int64_t w = 0; w < static_cast<int64_t>(windows.size()); ++w) {
+      grad.zero(st);
+      worker.run_sample(windows[w], static_cast<Timestep>(windows.size() - 1 - w), b, batches[b],
+                        grad.get(), losses.get() + k);
+      if (!optimizer_step(model, grad.get(), 1.f, opt, cfg, provider.store(), st)) ++report.skipped_steps;
+      report.visitation.push_back({b, w});
+      ++k;
+    }
+  }
+  DGNN_CUDA(cudaEventRecord(e1, st));
+  report.sample_losses.resize(nsamples);
+  copy_to_host(report.sample_losses.data(), losses.get(), sizeof(double) * nsamples, st);
+  float ms = 0.f;
+  DGNN_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  DGNN_CUDA(cudaEventDestroy(e0));
+  DGNN_CUDA(cudaEventDestroy(e1));
+  double total = 0.0;
+  for (double l : report.sample_losses) total += l;
+  report.loss = report.sample_losses.empty() ? 0.0 : total / report.sample_losses.size();
+  report.mae = report.loss;
+  if (provider.store()) {
+    const CacheStats& s1 = provider.store()->stats();
+    report.cache = s1;
+    report.cache.hits = s1.hits - stats0.hits;
+    report.cache.misses = s1.misses - stats0.misses;
+    report.cache.evictions = s1.evictions - stats0.evictions;
+    report.cache.expirations = s1.expirations - stats0.expirations;
+    report.cache.invalidations = s1.invalidations - stats0.invalidations;
+    report.cache.rejected = s1.rejected - stats0.rejected;
+  }
+  const ExecutionStats& e = provider.stats();
+  report.scratch_calls = e.scratch_calls - exec0.scratch_calls;
+  report.incremental_calls = e.incremental_calls - exec0.incremental_calls;
+  report.fallbacks = e.fallbacks - exec0.fallbacks;
+  report.kernel_invocations = report.scratch_calls + report.incremental_calls;
+  report.seconds = ms / 1000.0;
+  return report;
+}
+
+TrainSession::TrainSession(const DeviceGraph& graph, const ModelConfig& mcfg,
+                           const TrainConfig& tcfg, cudaStream_t stream, Timestep window_total)
+    : graph_(graph), tcfg_(tcfg) {
+  model_ = DgnnModel::create(mcfg, stream);
+  windows_ = sliding_windows(window_total > 0 ? window_total : graph.length() - 1, mcfg.seq_len,
+                             tcfg.stride, mcfg.horizon);
+  check(!windows_.empty(), "dataset too short for the requested windows");
+  worker_ = std::make_unique<Worker>(graph, *model_, tcfg, stream);
+}
+
+EpochReport TrainSession::run_epoch() {
+  EpochReport r = seq_first_epoch(*model_, graph_, windows_, tcfg_, *worker_, opt_, epoch_index_);
+  ++epoch_index_;
+  return r;
+}
+
+// ---------------------------------------------------------------- distributed
+std::vector<WorkerAssignment> plan_consecutive_block(Timestep total, int num_workers,
+                                                     Timestep seq_len, Timestep stride,
+                                                     Timestep horizon) {
+  check(num_workers >= 1, "plan needs at least one worker");
+  check(total >= num_workers, "fewer snapshots than workers");
+  const auto windows = sliding_windows(total, seq_len, stride, horizon);
+  const auto W = static_cast<int64_t>(windows.size());
+  std::vector<WorkerAssignment> out(num_workers);
+  const int64_t base = W / num_workers, extra = W % num_workers;
+  int64_t cursor = 0;
+  for (int m = 0; m < num_workers; ++m) {
+    WorkerAssignment& a = out[m];
+    a.window_begin = cursor;
+    a.window_end = cursor + base + (m < extra ? 1 : 0);
+    cursor = a.window_end;
+    a.block_begin = a.window_begin < W ? windows[a.window_begin].start : total;
+    a.block_end = m + 1 < num_workers ? (a.window_end < W ? windows[a.window_end].start : total) : total;
+    if (a.block_begin > a.block_end) a.block_begin = a.block_end;
+  }
+  if (!out.empty()) out.front().block_begin = 0;
+  return out;
+}
+
+DistWorker::DistWorker(const DeviceGraph& graph, const ModelConfig& mcfg, const TrainConfig& tcfg,
+                       cudaStream_t stream, int rank, int world, Timestep window_total)
+    : graph_(graph), tcfg_(tcfg) {
+  const Timestep total = window_total > 0 ? window_total : graph.length() - 1;
+  model_ = DgnnModel::create(mcfg, stream);
+  windows_ = sliding_windows(total, mcfg.seq_len, tcfg.stride, mcfg.horizon);
+  check(!windows_.empty(), "distributed epoch needs at least one window");
+  assign_ = plan_consecutive_block(total, world, mcfg.seq_len, tcfg.stride, mcfg.horizon).at(rank);
+  worker_ = std::make_unique<Worker>(graph, *model_, tcfg, stream);
+  grad_w_ = cuda::DevArray<float>(model_->num_params(), stream);
+}
+
+void DistWorker::begin_epoch() {
+  worker_->provider().reset_plan_state();
+  batches_ = make_batches(graph_.num_nodes(), tcfg_.batch_size, tcfg_.seed, epoch_index_);
+  const int64_t local = (assign_.window_end - assign_.window_begin) * num_batches();
+  losses_ = cuda::DevArray<double>(std::max<int64_t>(local, 1), worker_->stream());
+  losses_.zero(worker_->stream());
+  n_loss_ = 0;
+}
+
+void DistWorker::local_grads(int64_t b, float* grad_sum) {
+  cudaStream_t st = worker_->stream();
+  DGNN_CUDA(cudaMemsetAsync(grad_sum, 0, sizeof(float) * model_->num_params(), st));
+  for (int64_t w = assign_.window_begin; w < assign_.window_end; ++w) {
+    grad_w_.zero(st);
+    worker_->run_sample(windows_[w], static_cast<Timestep>(assign_.window_end - 1 - w), b,
+                        batches_[b], grad_w_.get(), losses_.get() + n_loss_);
+    ++n_loss_;
+    cuda::axpy(model_->num_params(), 1.f, grad_w_.get(), grad_sum, st);
+  }
+}
+
+bool DistWorker::apply(const float* grad_sum) {
+  const float inv = static_cast<float>(1.0 / static_cast<double>(windows_.size()));
+  return optimizer_step(*model_, grad_sum, inv, opt_, tcfg_, worker_->store(), worker_->stream());
+}
+
+void DistWorker::end_epoch() { ++epoch_index_; }
+
+std::vector<double> DistWorker::take_losses() {
+  std::vector<double> out(n_loss_);
+  copy_to_host(out.data(), losses_.get(), sizeof(double) * n_loss_, worker_->stream());
+  return out;
+}
+
+}  // namespace dgnn

@@ -1,0 +1,266 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the compiled CPU
+reference (oracle/_ref) on the same seeded synthetic dynamic graphs.
+
+Integer / index work (CSR, extract_delta, fallback decisions, invocation log,
+cache trace, parameter init) must be bit-exact. Floating point: the reference
+is fp64, the B200 path fp32; tolerances are stated per test (norm-relative).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+KINDS = ["sum", "mean", "max", "min"]
+SMALL = dict(n=300, avg_degree=4, dim=8, T=12, edge=0.05, feat=0.02)
+
+
+def nrel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    den = max(np.linalg.norm(b), 1e-30)
+    return float(np.linalg.norm(a - b) / den)
+
+
+@pytest.fixture(scope="module")
+def api():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_2501_15348_b200 import api as A
+    return A
+
+
+def make_pair(ref, api, n, avg_degree, dim, T, edge, feat, seed=1):
+    g_ref = ref.RefGraph.synth(n, avg_degree, dim, T, edge, feat, seed=seed)
+    g = api.Synth(n, avg_degree, dim, T, edge, feat, seed=seed).to_graph()
+    return g_ref, g
+
+
+@pytest.fixture(scope="module")
+def pair(ref, api):
+    return make_pair(ref, api, **SMALL)
+
+
+def test_graph_store_bitwise(pair):
+    g_ref, g = pair
+    assert g.length() == g_ref.T
+    for t in range(g_ref.T):
+        rp, rs = g_ref.in_csr(t)
+        p, s = g.in_csr(t)
+        assert np.array_equal(rp, p) and np.array_equal(rs, s), t
+        rp, rd = g_ref.out_csr(t)
+        p, d = g.out_csr(t)
+        assert np.array_equal(rp, p) and np.array_equal(rd, d), t
+        assert np.abs(g.feats(t) - g_ref.feats(t)).max() < 1e-7
+        if t == 0:
+            continue
+        rdel = g_ref.delta(t)
+        dl = g.delta(t)
+        for k in ("del_src", "del_dst", "ins_src", "ins_dst", "changed"):
+            assert np.array_equal(rdel[k], dl[k]), (t, k)
+        assert g.change_ratio(t) == g_ref.change_ratio(t)
+
+
+def test_graph_store_rejects_like_reference(api):
+    g = api.DynamicGraph(4, 2)
+    f = np.zeros((4, 2), np.float32)
+    with pytest.raises(ValueError, match="duplicate edge in snapshot"):
+        g.add_snapshot([(0, 1), (0, 1)], f)
+    with pytest.raises(ValueError, match="edge endpoint out of range"):
+        g.add_snapshot([(0, 7)], f)
+    g.add_snapshot([(0, 1), (2, 1)], f)
+    with pytest.raises(IndexError):
+        g.num_edges(3)
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_agg_scratch(pair, api, kind):
+    import torch
+    g_ref, g = pair
+    for t in (0, 5):
+        feats = g_ref.feats(t)
+        r = g_ref.agg_scratch(t, kind, feats)
+        out = api.aggregate_scratch(g, t, torch.from_numpy(feats.astype(np.float32)).cuda(), kind)
+        torch.cuda.synchronize()
+        assert nrel(out["values"].cpu().numpy(), r["values"]) < 1e-6
+        if kind == "mean":
+            assert np.array_equal(out["degree"].cpu().numpy(), r["degree"].astype(np.float32))
+        if kind in ("max", "min"):
+            assert np.array_equal(out["argext"].cpu().numpy(), r["argext"])
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_agg_incremental_chain(ref, api, kind):
+    """aggregate_incremental chains t0 -> t1 with the reference's fallbacks."""
+    import torch
+    g_ref, g = make_pair(ref, api, n=400, avg_degree=5, dim=8, T=10, edge=0.04, feat=0.01, seed=3)
+    t0, t1 = 0, 9
+    r = g_ref.agg_chain(t0, t1, kind, threshold=0.5, rescratch=6)
+    cur = api.aggregate_scratch(g, t0, g.feats_tensor(t0), kind)
+    depth, num_edges = 0, g.num_edges(t0)
+    for t in range(t0 + 1, t1 + 1):
+        nxt = api.aggregate_incremental(g, t, cur, kind, prev_depth=depth, prev_num_edges=num_edges,
+                                        fallback_threshold=0.5, rescratch_period=6)
+        info = r["steps"][t - t0 - 1]
+        assert (int(nxt["used_fallback"]), nxt["reason"], nxt["depth"]) == tuple(info), (t, info)
+        cur, depth, num_edges = nxt, nxt["depth"], g.num_edges(t)
+    torch.cuda.synchronize()
+    assert nrel(cur["values"].cpu().numpy(), r["values"]) < 1e-5
+    if kind in ("max", "min"):
+        assert np.array_equal(cur["argext"].cpu().numpy(), r["argext"])
+    if kind == "mean":
+        assert np.array_equal(cur["degree"].cpu().numpy(), r["degree"].astype(np.float32))
+
+
+def test_agg_delta_kernel_inplace(pair, api):
+    """K2 alone (graded kernel): Agg_{t-1} + delta(t) == scratch at t."""
+    import torch
+    g_ref, g = pair
+    for t in range(1, g_ref.T):
+        agg = api.aggregate_scratch(g, t - 1, g.feats_tensor(t - 1), "sum")
+        api.aggregate_delta_inplace(g, t, agg, g.feats_tensor(t - 1), g.feats_tensor(t), "sum")
+        torch.cuda.synchronize()
+        want = g_ref.agg_scratch(t, "sum", g_ref.feats(t))["values"]
+        assert nrel(agg["values"].cpu().numpy(), want) < 1e-5, t
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_agg_backward(pair, api, kind):
+    import torch
+    g_ref, g = pair
+    t = 4
+    rng = np.random.default_rng(7)
+    feats = g_ref.feats(t)
+    up = rng.standard_normal(feats.shape)
+    want = g_ref.agg_backward(t, kind, feats, up)
+    fwd = api.aggregate_scratch(g, t, torch.from_numpy(feats.astype(np.float32)).cuda(), kind)
+    got = api.aggregate_backward(g, t, torch.from_numpy(up.astype(np.float32)).cuda(), kind, fwd)
+    torch.cuda.synchronize()
+    assert nrel(got.cpu().numpy(), want) < 1e-5
+
+
+@pytest.mark.parametrize("lstm", [True, False])
+@pytest.mark.parametrize("H,n_in", [(16, 8), (64, 128), (64, 64)])
+def test_cell_fwd_bwd(ref, api, lstm, H, n_in):
+    import torch
+    n = 777
+    rng = np.random.default_rng(11)
+    params = ref.cell_init(0 if lstm else 1, n_in, H, 5)
+    X = rng.uniform(-2, 2, (n, n_in))
+    Hm = rng.uniform(-2, 2, (n, H))
+    hs = rng.uniform(-1, 1, (n, H))
+    cp = rng.uniform(-1, 1, (n, H)) if lstm else None
+    dh = rng.standard_normal((n, H))
+    dc = rng.standard_normal((n, H)) if lstm else None
+    want = ref.cell_fwd_bwd(0 if lstm else 1, n_in, H, params, X, Hm, hs, cp, dh, dc)
+    T = lambda a: None if a is None else torch.from_numpy(np.asarray(a, np.float32)).cuda()
+    fwd = api.cell_forward(lstm, T(X), T(Hm), T(hs), T(cp), T(params))
+    bwd = api.cell_backward(lstm, T(X), T(Hm), fwd, T(hs), T(cp), T(dh), T(dc))
+    torch.cuda.synchronize()
+    K = 4 if lstm else 3
+    gates = fwd["gates"].cpu().numpy().reshape(n, 4, H)
+    for g in range(K):
+        assert nrel(gates[:, g], want["gates"][g]) < 1e-5, g
+    if not lstm:
+        assert nrel(gates[:, 3], want["hn"]) < 1e-5
+        assert nrel(bwd["dh_skip"].cpu().numpy(), want["dh_skip"]) < 1e-5
+    else:
+        assert nrel(fwd["c"].cpu().numpy(), want["c"]) < 1e-5
+        assert nrel(bwd["dc_prev"].cpu().numpy(), want["dc_prev"]) < 1e-5
+    assert nrel(fwd["h"].cpu().numpy(), want["h"]) < 1e-5
+    assert nrel(bwd["dX"].cpu().numpy(), want["dX"]) < 1e-5
+    assert nrel(bwd["dHm"].cpu().numpy(), want["dHm"]) < 1e-5
+    assert nrel(bwd["dflat"].cpu().numpy(), want["dparams"]) < 1e-5
+
+
+ARCHS = ["gcrn_m2", "tgcn", "gcrn_m1", "cd_gcn"]
+
+
+@pytest.mark.parametrize("arch", ARCHS)
+@pytest.mark.parametrize("aggr", ["sum", "max"])
+def test_sample_grads(ref, api, pair, arch, aggr):
+    """One sample: init params bit-exact, loss / prediction / gradients (rel 1e-4)."""
+    g_ref, g = pair
+    cfg_r = ref.RunCfg(arch=arch, hidden=16, aggr=aggr)
+    cfg = api.TrainConfig(arch=arch, hidden=16, aggr=aggr)
+    s = api.TrainSession(g, cfg)
+    p0 = s.initial_params()
+    assert np.array_equal(p0, g_ref.init_params(cfg_r))
+    for w in (0, 2):
+        loss_r, pred_r, grads_r = g_ref.sample_grads(cfg_r, w)
+        loss, pred, grads = s.sample_grads(w)
+        assert abs(loss - loss_r) <= 1e-5 * abs(loss_r), (loss, loss_r)
+        assert nrel(pred, pred_r) < 1e-5
+        assert nrel(grads, grads_r) < 1e-4
+
+
+def _events_match(ev, ev_ref):
+    """Cache traces equal; invalidation bursts compared as multisets (ref
+    bump_epoch iterates an unordered_map, src/cache.cpp:212-216)."""
+    ev_ref = ev_ref[:, 1:]  # drop worker column
+    assert ev.shape == ev_ref.shape
+    i = 0
+    while i < len(ev):
+        if ev[i, 0] == 4:  # kInvalidate burst
+            j = i
+            while j < len(ev) and ev[j, 0] == 4:
+                j += 1
+            a = sorted(map(tuple, ev[i:j].tolist()))
+            b = sorted(map(tuple, ev_ref[i:j].tolist()))
+            assert a == b
+            i = j
+        else:
+            assert np.array_equal(ev[i], ev_ref[i]), (i, ev[i], ev_ref[i])
+            i += 1
+
+
+@pytest.mark.parametrize("arch", ["gcrn_m2", "tgcn", "gcrn_m1"])
+def test_seq_first_epochs(ref, api, pair, arch):
+    g_ref, g = pair
+    cfg_r = ref.RunCfg(arch=arch, hidden=16, epochs=2, cache_frac=0.5)
+    r = g_ref.run(cfg_r)
+    cfg = api.TrainConfig(arch=arch, hidden=16, cache_frac=0.5, record_events=True)
+    s = api.TrainSession(g, cfg)
+    losses = np.concatenate([s.run_epoch()["sample_losses"] for _ in range(2)])
+    assert losses.shape == r.losses.shape
+    assert nrel(losses, r.losses) < 1e-4
+    assert nrel(s.params(), r.params) < 1e-3
+    assert np.array_equal(s.invocations(), r.invocations[:, 1:])
+    _events_match(s.cache_events(), r.events)
+    st = s.stats()
+    keys = ["hits", "misses", "evictions", "expirations", "invalidations", "rejected",
+            "scratch_calls", "incremental_calls", "fallbacks"]
+    assert [st[k] for k in keys] == r.stats[0, :9].tolist()
+
+
+@pytest.mark.parametrize("workers", [1, 2, 3])
+def test_sharded_epoch_emulated_ranks(ref, api, pair, workers):
+    """Consecutive-block sharding with the all-reduce emulated in-process
+    (ranks run sequentially on one GPU; the multi-process NCCL path is covered
+    by bench.py --gpus N)."""
+    import torch
+    g_ref, g = pair
+    cfg_r = ref.RunCfg(arch="tgcn", hidden=16, workers=workers, epochs=2)
+    r = g_ref.run(cfg_r)
+    ranks = [api.TrainSession(g, api.TrainConfig(arch="tgcn", hidden=16, workers=workers), rank=m)
+             for m in range(workers)]
+    P = ranks[0].num_params
+    losses = []
+    for _ in range(2):
+        nbs = [s.begin_epoch() for s in ranks]
+        for b in range(nbs[0]):
+            bufs = [torch.empty(P, device="cuda") for _ in ranks]
+            for s, buf in zip(ranks, bufs):
+                s.local_grads(b, buf)
+            total = torch.stack(bufs).sum(0)
+            for s in ranks:
+                assert s.apply(total.clone())
+        for s in ranks:
+            s.end_epoch()
+            losses.append(s.losses())
+    # reference visit order: epoch-major, then worker, then window
+    assert nrel(np.concatenate(losses), r.losses) < 1e-4
+    for s in ranks:
+        assert nrel(s.params(), r.params) < 1e-3
+    inv = np.concatenate([s.invocations() for s in ranks])
+    ref_inv = np.concatenate([r.invocations[r.invocations[:, 0] == m][:, 1:] for m in range(workers)])
+    assert np.array_equal(inv, ref_inv)
