@@ -206,6 +206,27 @@ int dgnn_session_cache_events(dgnn_session* s, int64_t* out, int64_t* n);
  * scratch incremental fallbacks spills refills peak_units(as int64). */
 int dgnn_session_stats(dgnn_session* s, int64_t* out12);
 
+/* ------------------------------------------------------- host-side plan logic
+ * Pure host functions (no device needed). */
+/* sliding_windows (src/windows.cpp:5-15): writes up to cap starts, returns count. */
+int64_t dgnn_sliding_windows(int32_t total, int32_t L, int32_t S, int32_t H, int32_t* starts,
+                             int64_t cap);
+/* plan, consecutive_block (src/distsim.cpp:35-81): out[4m..4m+3] =
+ * block_begin, block_end, window_begin, window_end. */
+int dgnn_plan(int32_t total, int32_t workers, int32_t L, int32_t S, int32_t H, int64_t* out);
+/* future_access_count / imminence (src/cache.cpp:27-62); ctx = num_layers,
+ * gates, gate, L, S, idx, part, layer, teacher_forcing, H, windows_remaining, kind. */
+int dgnn_cache_scores(const int32_t* ctx, int32_t* f, int32_t* imm);
+/* AggKeyHash (inc/cache.hpp:54-61). */
+uint64_t dgnn_key_hash(int32_t level, int32_t layer, int32_t t, int32_t kind, int64_t batch,
+                       int64_t serial);
+/* make_batches (src/train.cpp:54-64): out[2i], out[2i+1] = range; returns count. */
+int64_t dgnn_make_batches(int32_t num_nodes, int32_t batch_size, uint64_t seed,
+                          int64_t epoch_index, int32_t* out, int64_t cap);
+/* DgnnModel::create parameter draws (src/model.cpp:41-70) without a device:
+ * writes the fp64 flat init (visit order) when out != NULL; returns count. */
+int64_t dgnn_init_params(const dgnn_run_cfg* cfg, int32_t feature_dim, double* out);
+
 /* ---------------------------------------------------------------- profiling
  * Device timing per kernel class (0 agg_scratch, 1 agg_delta, 2 agg_backward,
  * 3 cell_fwd, 4 cell_bwd, 5 weight_grad, 6 other) with algorithmic bytes. */

@@ -83,6 +83,12 @@ SIGNATURES = {
     "dgnn_session_invocations": (C.c_int, [P, P, C.POINTER(I64)]),
     "dgnn_session_cache_events": (C.c_int, [P, P, C.POINTER(I64)]),
     "dgnn_session_stats": (C.c_int, [P, P]),
+    "dgnn_sliding_windows": (I64, [I32, I32, I32, I32, P, I64]),
+    "dgnn_plan": (C.c_int, [I32, I32, I32, I32, I32, P]),
+    "dgnn_cache_scores": (C.c_int, [P, C.POINTER(I32), C.POINTER(I32)]),
+    "dgnn_key_hash": (U64, [I32, I32, I32, I32, I64, I64]),
+    "dgnn_make_batches": (I64, [I32, I32, U64, I64, P, I64]),
+    "dgnn_init_params": (I64, [C.POINTER(RunCfg), I32, P]),
     "dgnn_prof_enable": (C.c_int, [I32]),
     "dgnn_prof_reset": (C.c_int, []),
     "dgnn_prof_get": (C.c_int, [I32, C.POINTER(I64), C.POINTER(D), C.POINTER(D), C.POINTER(D)]),

@@ -110,7 +110,7 @@ class Synth:
         self.sizes = sizes
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and _lib is not None and _lib._lib is not None:
             lib().dgnn_synth_free(self.h)
             self.h = None
 
@@ -165,7 +165,7 @@ class DynamicGraph:
         return g
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and _lib is not None and _lib._lib is not None:
             lib().dgnn_graph_free(self.h)
             self.h = None
 
@@ -435,7 +435,7 @@ class TrainSession:
         self.num_params = lib().dgnn_session_num_params(self.h)
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and _lib is not None and _lib._lib is not None:
             lib().dgnn_session_free(self.h)
             self.h = None
 

@@ -640,6 +640,84 @@ int dgnn_session_stats(dgnn_session* s, int64_t* out12) {
   });
 }
 
+// ------------------------------------------------------- host-side plan logic
+int64_t dgnn_sliding_windows(int32_t total, int32_t L, int32_t S, int32_t H, int32_t* starts,
+                             int64_t cap) {
+  try {
+    auto w = sliding_windows(total, L, S, H);
+    for (int64_t i = 0; i < static_cast<int64_t>(w.size()) && i < cap; ++i) starts[i] = w[i].start;
+    return static_cast<int64_t>(w.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+int dgnn_plan(int32_t total, int32_t workers, int32_t L, int32_t S, int32_t H, int64_t* out) {
+  return guarded([&] {
+    auto p = plan_consecutive_block(total, workers, L, S, H);
+    for (int m = 0; m < workers; ++m) {
+      out[4 * m + 0] = p[m].block_begin;
+      out[4 * m + 1] = p[m].block_end;
+      out[4 * m + 2] = p[m].window_begin;
+      out[4 * m + 3] = p[m].window_end;
+    }
+  });
+}
+
+int dgnn_cache_scores(const int32_t* ctx, int32_t* f, int32_t* imm) {
+  return guarded([&] {
+    ExecContext c;
+    c.num_layers = ctx[0];
+    c.gates = ctx[1];
+    c.gate = ctx[2];
+    c.seq_len = ctx[3];
+    c.stride = ctx[4];
+    c.idx = ctx[5];
+    c.part = static_cast<ModelPart>(ctx[6]);
+    c.layer = ctx[7];
+    c.teacher_forcing = ctx[8] != 0;
+    c.horizon = ctx[9];
+    c.windows_remaining = ctx[10];
+    c.kind = static_cast<AggKeyKind>(ctx[11]);
+    *f = future_access_count(c);
+    *imm = imminence(c);
+  });
+}
+
+uint64_t dgnn_key_hash(int32_t level, int32_t layer, int32_t t, int32_t kind, int64_t batch,
+                       int64_t serial) {
+  AggKey k{static_cast<CacheLevel>(level), layer, t, static_cast<AggKeyKind>(kind), batch, serial};
+  return static_cast<uint64_t>(AggKeyHash{}(k));
+}
+
+int64_t dgnn_make_batches(int32_t num_nodes, int32_t batch_size, uint64_t seed,
+                          int64_t epoch_index, int32_t* out, int64_t cap) {
+  auto b = make_batches(num_nodes, batch_size, seed, epoch_index);
+  for (int64_t i = 0; i < static_cast<int64_t>(b.size()) && i < cap; ++i) {
+    out[2 * i] = b[i].first;
+    out[2 * i + 1] = b[i].second;
+  }
+  return static_cast<int64_t>(b.size());
+}
+
+int64_t dgnn_init_params(const dgnn_run_cfg* cfg, int32_t feature_dim, double* out) {
+  try {
+    ModelConfig m;
+    m.arch = static_cast<Architecture>(cfg->arch);
+    m.layers = cfg->layers;
+    m.feature_dim = feature_dim;
+    m.hidden_dim = cfg->hidden;
+    m.seed = cfg->seed;
+    auto v = initial_params_host(m);
+    if (out) std::memcpy(out, v.data(), sizeof(double) * v.size());
+    return static_cast<int64_t>(v.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 // ---------------------------------------------------------------- profiling
 int dgnn_prof_enable(int32_t on) {
   return guarded([&] { prof_enable(on != 0); });

@@ -95,14 +95,9 @@ void cell_init(int gates, int64_t in, int64_t H, std::mt19937_64& rng,
   }
 }
 
-}  // namespace
-
-std::unique_ptr<DgnnModel> DgnnModel::create(const ModelConfig& cfg, cudaStream_t stream) {
-  check(cfg.layers >= 1, "model needs at least one layer");
-  check(cfg.feature_dim >= 1 && cfg.hidden_dim >= 1, "model dims must be positive");
-  auto m = std::make_unique<DgnnModel>();
-  m->cfg_ = cfg;
-  m->stream_ = stream;
+// Parameter draws in the reference's init order (src/model.cpp:41-70),
+// keyed by visit_params name.
+std::map<std::string, HostMat> draw_named(const ModelConfig& cfg) {
   std::mt19937_64 rng(derive_seed(cfg.seed, 0x90de1));
   const int K = gate_count(cell_kind_of(cfg.arch));
   const bool lstm = cell_kind_of(cfg.arch) == CellKind::kLstm;
@@ -140,6 +135,59 @@ std::unique_ptr<DgnnModel> DgnnModel::create(const ModelConfig& cfg, cudaStream_
     named["head/w"] = std::move(w);
     named["head/b"] = std::move(b);
   }
+  return named;
+}
+
+}  // namespace
+
+std::vector<double> initial_params_host(const ModelConfig& cfg) {
+  check(cfg.layers >= 1, "model needs at least one layer");
+  check(cfg.feature_dim >= 1 && cfg.hidden_dim >= 1, "model dims must be positive");
+  std::map<std::string, HostMat> named = draw_named(cfg);
+  std::vector<double> flat;
+  for (const std::string& name : visit_order(cfg)) {
+    const HostMat& hm = named.at(name);
+    flat.insert(flat.end(), hm.v.begin(), hm.v.end());
+  }
+  return flat;
+}
+
+std::vector<std::string> visit_order(const ModelConfig& cfg) {
+  std::vector<std::string> out;
+  const int K = gate_count(cell_kind_of(cfg.arch));
+  auto cell = [&](const std::string& prefix) {
+    for (int g = 0; g < K; ++g) {
+      const std::string i = std::to_string(g);
+      out.push_back(prefix + "/wx" + i);
+      out.push_back(prefix + "/uh" + i);
+      out.push_back(prefix + "/b" + i);
+    }
+  };
+  if (!is_stacked(cfg.arch)) {
+    for (int l = 0; l < cfg.layers; ++l) cell("enc" + std::to_string(l + 1));
+    for (int l = 0; l < cfg.layers; ++l) cell("dec" + std::to_string(l + 1));
+  } else {
+    for (int p = 0; p < cfg.layers; ++p) {
+      out.push_back("gcn" + std::to_string(p + 1) + "/w");
+      out.push_back("gcn" + std::to_string(p + 1) + "/b");
+    }
+    for (int p = 0; p < cfg.layers; ++p) cell("rnn" + std::to_string(p + 1));
+  }
+  out.push_back("head/w");
+  out.push_back("head/b");
+  return out;
+}
+
+std::unique_ptr<DgnnModel> DgnnModel::create(const ModelConfig& cfg, cudaStream_t stream) {
+  check(cfg.layers >= 1, "model needs at least one layer");
+  check(cfg.feature_dim >= 1 && cfg.hidden_dim >= 1, "model dims must be positive");
+  auto m = std::make_unique<DgnnModel>();
+  m->cfg_ = cfg;
+  m->stream_ = stream;
+  const int K = gate_count(cell_kind_of(cfg.arch));
+  const bool lstm = cell_kind_of(cfg.arch) == CellKind::kLstm;
+  const int H = cfg.hidden_dim, d = cfg.feature_dim;
+  std::map<std::string, HostMat> named = draw_named(cfg);
   // flat layout in visit order (ref src/model.cpp:72-89)
   int64_t off = 0;
   auto add_slot = [&](const std::string& name) {

@@ -51,6 +51,11 @@ struct ModelConfig {
   uint64_t seed = 1;
 };
 
+// Parameter names in visit_params order (src/model.cpp:72-89) and the fp64
+// initial draws in that order (host only, no device needed).
+std::vector<std::string> visit_order(const ModelConfig& cfg);
+std::vector<double> initial_params_host(const ModelConfig& cfg);
+
 using Buf = std::shared_ptr<cuda::DevArray<float>>;
 Buf new_buf(size_t n, cudaStream_t stream);
 Buf zero_buf(size_t n, cudaStream_t stream);

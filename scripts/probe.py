@@ -32,7 +32,7 @@ for e in range(epochs):
     tb = time.time()
     W = len(losses)
     print(f"epoch {e}: {tb-ta:.2f}s wall, {W} windows, loss {losses.mean():.5f}, "
-          f"snapshots/s {W*9/(tb-ta):.1f}, mem {torch.cuda.max_memory_allocated()/1e9:.1f}GB", flush=True)
+          f"snapshots/s {W*9/(tb-ta):.1f}, free {torch.cuda.mem_get_info()[0]/1e9:.1f}GB", flush=True)
 prof = api.prof_get()
 tot = sum(v["ms"] for v in prof.values())
 for k, v in prof.items():

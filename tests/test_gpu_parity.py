@@ -15,8 +15,14 @@ SMALL = dict(n=300, avg_degree=4, dim=8, T=12, edge=0.05, feat=0.02)
 
 
 def nrel(a, b):
+    """Norm-relative error; +/-inf sentinels (empty max/min rows) must sit at
+    the same positions with the same sign and are excluded from the norm."""
     a = np.asarray(a, np.float64)
     b = np.asarray(b, np.float64)
+    fa, fb = np.isfinite(a), np.isfinite(b)
+    if not np.array_equal(fa, fb) or not np.array_equal(a[~fa], b[~fb]):
+        return float("inf")
+    a, b = a[fa], b[fb]
     den = max(np.linalg.norm(b), 1e-30)
     return float(np.linalg.norm(a - b) / den)
 
