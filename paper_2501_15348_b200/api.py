@@ -428,6 +428,8 @@ class TrainSession:
     def __init__(self, graph: DynamicGraph, cfg: TrainConfig, rank: int = 0, stream=None):
         self.graph, self.cfg = graph, cfg
         self._c = cfg.to_c()
+        if stream is None:  # run on the caller's torch stream: ordering with torch ops is implicit
+            stream = current_stream()
         h = C.c_void_p()
         check(lib().dgnn_session_create(graph.h, C.byref(self._c), rank, _stream_handle(stream),
                                         C.byref(h)))

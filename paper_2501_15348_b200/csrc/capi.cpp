@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "host/synth.hpp"
+#include "umma_kernels.h"
 #include "host/train.hpp"
 
 using namespace dgnn;
@@ -261,6 +262,7 @@ int dgnn_synth_to_graph(const dgnn_synth* s, void* stream, dgnn_graph** out) {
                       st.changed.data(), static_cast<int64_t>(st.changed.size()),
                       st.changed_feats.data());
     }
+    DGNN_CUDA(cudaStreamSynchronize(g->stream));
     *out = guard.release();
   });
 }
@@ -353,8 +355,16 @@ int dgnn_cell_forward(int32_t lstm, int32_t n, int32_t in, int32_t H, const floa
                       const float* Hm, const float* h_skip, const float* c_prev, const float* W,
                       const float* bias, float* gates, float* c, float* h, void* stream) {
   return guarded([&] {
-    cuda::cell_forward(lstm != 0, n, in, H, X, Hm, h_skip, c_prev, W, bias, gates, c, h,
-                       as_stream(stream));
+    cudaStream_t st = as_stream(stream);
+    if (cuda::umma_cell_supported(in, H)) {
+      cuda::DevArray<float> img(cuda::umma_bimage_floats(4 * H, in + H), st);
+      cuda::umma_pack_b(W, 4 * H, true, 0, 4 * H, in + H, img.get(), st);
+      cuda::umma_cell_forward(lstm != 0, n, in, H, X, Hm, h_skip, c_prev, img.get(), bias, gates,
+                              c, h, st);
+      DGNN_CUDA(cudaStreamSynchronize(st));
+      return;
+    }
+    cuda::cell_forward(lstm != 0, n, in, H, X, Hm, h_skip, c_prev, W, bias, gates, c, h, st);
   });
 }
 
@@ -368,12 +378,27 @@ int dgnn_cell_backward(int32_t lstm, int32_t n, int32_t in, int32_t H, const flo
     const int K = in + H;
     cuda::DevArray<float> G(static_cast<size_t>(n) * 4 * H, st), WT(static_cast<size_t>(K) * 4 * H, st);
     cuda::DevArray<float> dW(static_cast<size_t>(K) * 4 * H, st), db(4 * H, st);
-    cuda::DevArray<float> ws(cuda::gemm_tn_workspace(n, K, 4 * H), st);
+    const bool tc = cuda::umma_cell_supported(in, H);
+    cuda::DevArray<float> ws(tc ? cuda::umma_wgrad_workspace(in, H) : cuda::gemm_tn_workspace(n, K, 4 * H), st);
     dW.zero(st);
     db.zero(st);
     cuda::transpose(K, 4 * H, W, WT.get(), st);
     cuda::cell_backward_pointwise(lstm != 0, n, H, gates, c, c_prev, h_skip, dh, dc, G.get(),
                                   dc_prev, dh_skip, st);
+    if (tc) {
+      cuda::umma_wgrad(n, in, H, G.get(), X, Hm, dW.get(), lstm ? 4 * H : 3 * H, db.get(), ws.get(), st);
+      cuda::DevArray<float> img(cuda::umma_bimage_floats(K, 4 * H), st);
+      if (dX) {
+        cuda::umma_pack_b(W, 4 * H, false, 0, K, 4 * H, img.get(), st);
+        cuda::umma_gemm_store2(n, 4 * H, G.get(), img.get(), in, H, dX, dHm, st);
+      } else {
+        cuda::umma_pack_b(W, 4 * H, false, in, H, 4 * H, img.get(), st);
+        cuda::umma_gemm_store2(n, 4 * H, G.get(), img.get(), H, 0, dHm, nullptr, st);
+      }
+      cuda::unpack_cell_grad(lstm != 0, in, H, dW.get(), db.get(), dflat, st);
+      DGNN_CUDA(cudaStreamSynchronize(st));
+      return;
+    }
     cuda::gemm_tn_acc(n, in, H, 4 * H, X, Hm, G.get(), dW.get(), lstm ? 4 * H : 3 * H, db.get(),
                       ws.get(), st);
     if (dX) {
@@ -449,6 +474,8 @@ int dgnn_session_create(dgnn_graph* g, const dgnn_run_cfg* cfg, int32_t rank, vo
     } else {
       s->stream = g->stream;
     }
+    // the graph store may have been built on another stream
+    DGNN_CUDA(cudaStreamSynchronize(g->stream));
     fill_configs(s.get());
     if (cfg->workers <= 0) {
       s->seq = std::make_unique<TrainSession>(*g->g, s->mcfg, s->tcfg, s->stream, cfg->window_total);

@@ -215,6 +215,12 @@ std::unique_ptr<DgnnModel> DgnnModel::create(const ModelConfig& cfg, cudaStream_
     c.bias = cuda::DevArray<float>(4 * H, stream);
     c.dW = cuda::DevArray<float>(KW, stream);
     c.db = cuda::DevArray<float>(4 * H, stream);
+    c.umma = cuda::umma_cell_supported(in, H);
+    if (c.umma) {
+      c.Bf = cuda::DevArray<float>(cuda::umma_bimage_floats(4 * H, in + H), stream);
+      c.Bb = cuda::DevArray<float>(cuda::umma_bimage_floats(in + H, 4 * H), stream);
+      c.Bbh = cuda::DevArray<float>(cuda::umma_bimage_floats(H, 4 * H), stream);
+    }
     dst->push_back(std::move(c));
   };
   if (!is_stacked(cfg.arch)) {
@@ -268,6 +274,12 @@ void DgnnModel::refresh_packed() {
   auto pack = [&](CellSlot& c) {
     cuda::pack_cell(c.lstm, c.in, c.H, params_.get() + c.offset, c.W.get(), c.bias.get(), stream_);
     cuda::transpose(c.in + c.H, 4 * c.H, c.W.get(), c.WT.get(), stream_);
+    if (c.umma) {
+      const int K = c.in + c.H, NC = 4 * c.H;
+      cuda::umma_pack_b(c.W.get(), NC, true, 0, NC, K, c.Bf.get(), stream_);       // W^T
+      cuda::umma_pack_b(c.W.get(), NC, false, 0, K, NC, c.Bb.get(), stream_);      // W
+      cuda::umma_pack_b(c.W.get(), NC, false, c.in, c.H, NC, c.Bbh.get(), stream_);  // W[in:]
+    }
   };
   for (auto& c : enc_) pack(c);
   for (auto& c : dec_) pack(c);
@@ -330,9 +342,15 @@ CellTape cell_forward(const CellSlot& c, NodeId n, const float* X, const float* 
   // X, Hm, W + gates, h (c, c_prev) traffic
   const double bytes = 4.0 * n * (c.in + c.H + 4 * c.H + c.H + (c.lstm ? 2 * c.H : c.H));
   ProfScope ps(kProfCellFwd, st, bytes, cell_flops(n, c.in, c.H));
-  cuda::cell_forward(c.lstm, n, c.in, c.H, X, Hm, h_skip->get(), c.lstm ? c_prev->get() : nullptr,
-                     c.W.get(), c.bias.get(), t.gates->get(), c.lstm ? t.c->get() : nullptr,
-                     t.h->get(), st);
+  if (c.umma) {
+    cuda::umma_cell_forward(c.lstm, n, c.in, c.H, X, Hm, h_skip->get(),
+                            c.lstm ? c_prev->get() : nullptr, c.Bf.get(), c.bias.get(),
+                            t.gates->get(), c.lstm ? t.c->get() : nullptr, t.h->get(), st);
+  } else {
+    cuda::cell_forward(c.lstm, n, c.in, c.H, X, Hm, h_skip->get(), c.lstm ? c_prev->get() : nullptr,
+                       c.W.get(), c.bias.get(), t.gates->get(), c.lstm ? t.c->get() : nullptr,
+                       t.h->get(), st);
+  }
   return t;
 }
 
@@ -523,15 +541,26 @@ StepGrads cell_step_backward(CellSlot& c, const CellTape& tape, const float* X, 
   }
   {
     ProfScope ps(kProfWeightGrad, st, 4.0 * n * (in + H + 4 * H), cell_flops(n, in, H));
-    cuda::gemm_tn_acc(n, in, H, 4 * H, X, Hm, G->get(), c.dW.get(), c.lstm ? 4 * H : 3 * H,
-                      c.db.get(), g.ws, st);
+    if (c.umma) {
+      cuda::umma_wgrad(n, in, H, G->get(), X, Hm, c.dW.get(), c.lstm ? 4 * H : 3 * H, c.db.get(),
+                       g.ws, st);
+    } else {
+      cuda::gemm_tn_acc(n, in, H, 4 * H, X, Hm, G->get(), c.dW.get(), c.lstm ? 4 * H : 3 * H,
+                        c.db.get(), g.ws, st);
+    }
   }
   Buf dX = need_dx ? new_buf(static_cast<size_t>(n) * in, st) : nullptr;
   Buf dHm = new_buf(static_cast<size_t>(n) * H, st);
   {
     ProfScope ps(kProfCellBwd, st, 4.0 * n * (4 * H + (need_dx ? in : 0) + H),
                  2.0 * n * 4 * H * ((need_dx ? in : 0) + H));
-    if (need_dx) {
+    if (c.umma) {
+      if (need_dx) {
+        cuda::umma_gemm_store2(n, 4 * H, G->get(), c.Bb.get(), in, H, dX->get(), dHm->get(), st);
+      } else {
+        cuda::umma_gemm_store2(n, 4 * H, G->get(), c.Bbh.get(), H, 0, dHm->get(), nullptr, st);
+      }
+    } else if (need_dx) {
       cuda::gemm_nn(n, 4 * H, 0, in, H, G->get(), nullptr, c.WT.get(), in + H, nullptr, false,
                     false, dX->get(), dHm->get(), st);
     } else {
@@ -680,6 +709,8 @@ void model_backward(DgnnModel& model, const SeqSample& sample, const ForwardArti
     ws_n = std::max(ws_n, cuda::gemm_tn_workspace(n, in, H));          // gcn
   }
   ws_n = std::max(ws_n, cuda::gemm_tn_workspace(n, H, d));             // head
+  for (int in : {d, H})
+    if (cuda::umma_cell_supported(in, H)) ws_n = std::max(ws_n, cuda::umma_wgrad_workspace(in, H));
   cuda::DevArray<float> ws(ws_n, stream);
   Grads g{grad, ws.get()};
   zero_cell_accumulators(model.enc_, stream);

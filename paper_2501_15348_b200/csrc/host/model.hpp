@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "../dense_kernels.h"
+#include "../umma_kernels.h"
 #include "engine.hpp"
 
 namespace dgnn {
@@ -75,6 +76,10 @@ struct CellSlot {
   bool lstm = true;
   cuda::DevArray<float> W, bias, WT;  // packed (in+H) x 4H, 4H, 4H x (in+H)
   cuda::DevArray<float> dW, db;       // per-sample gradient accumulators
+  // tcgen05 B images (3xTF32 hi/lo, canonical UMMA layout): forward W^T,
+  // backward W (dX | dHm) and its dHm-only rows.
+  bool umma = false;
+  cuda::DevArray<float> Bf, Bb, Bbh;
   int64_t flat_size() const {
     return static_cast<int64_t>(lstm ? 4 : 3) * (int64_t(in) * H + int64_t(H) * H + H);
   }

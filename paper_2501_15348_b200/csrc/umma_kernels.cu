@@ -1,0 +1,563 @@
+// tcgen05 (5th-gen tensor core) kernels for the dense part of the GraphRNN
+// cell, fp32-accurate through a 3xTF32 split:
+//   a*b ~= a_hi*b_hi + a_hi*b_lo + a_lo*b_hi  (kind::tf32, fp32 accumulate in TMEM)
+//
+//   k_row_gemm  D[128-row tile x N] = [A1|A2](rows x K) * B^T, B = packed
+//               weight image (N x K, K-major), with a fused epilogue:
+//               LSTM / GRU gates + state update + tape write (cell forward),
+//               or a column-split store (cell backward dX | dHm).
+//   k_wgrad     per-CTA partial of G^T * [X | Hm | 1] over a contiguous row
+//               range (weight + bias gradients), reduced in fixed CTA order.
+//
+// One CTA per SM (persistent over row tiles). Operands are staged global ->
+// registers (3xTF32 split, transposition for the weight-gradient operands) ->
+// shared memory in the canonical K-major UMMA layout, double/triple buffered
+// against the asynchronous MMAs through mbarriers signalled by tcgen05.commit.
+// A single elected thread issues every tcgen05.mma; accumulators live in TMEM
+// and the epilogue reads them with tcgen05.ld.
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <string>
+#include <type_traits>
+
+#include "common.cuh"
+#include "umma.cuh"
+#include "umma_kernels.h"
+
+namespace dgnn {
+namespace cuda {
+namespace {
+
+using namespace umma;
+
+constexpr int kThreads = 256;
+constexpr int kTileM = 128;  // rows per MMA tile (cta_group::1, M = 128)
+constexpr int kKC = 32;      // K elements staged per chunk (4 MMA K-steps of 8)
+
+__device__ __forceinline__ float sigm(float x) { return 1.f / (1.f + expf(-x)); }
+
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, float a, float b, float c, float d) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
+// ------------------------------------------------------------- B images
+// out: per K chunk c: [hi tile (Npad x KC)][lo tile], canonical layout.
+// B(n, k) = trans ? M[k * ld + (n0 + n)] : M[(n0 + n) * ld + k]; zero padded.
+__global__ void k_pack_b(const float* __restrict__ M, int ld, int trans, int n0, int N, int K,
+                         int Npad, int nchunks, float* __restrict__ out) {
+  const int64_t per_tile = tile_bytes(Npad, kKC) / 4;
+  const int64_t total = static_cast<int64_t>(nchunks) * Npad * kKC;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i / (static_cast<int64_t>(Npad) * kKC));
+    const int rem = static_cast<int>(i - static_cast<int64_t>(c) * Npad * kKC);
+    const int n = rem / kKC, kk = rem % kKC;
+    const int k = c * kKC + kk;
+    float v = 0.f;
+    if (n < N && k < K) v = trans ? M[static_cast<int64_t>(k) * ld + n0 + n] : M[static_cast<int64_t>(n0 + n) * ld + k];
+    float hi, lo;
+    split_tf32(v, hi, lo);
+    float* base = out + static_cast<int64_t>(c) * 2 * per_tile;
+    const uint32_t off = tile_offset(Npad, n, kk) / 4;
+    base[off] = hi;
+    base[per_tile + off] = lo;
+  }
+}
+
+// ------------------------------------------------------------- row GEMM
+enum { kEpiLstm = 0, kEpiGru = 1, kEpiStore2 = 2 };
+
+struct RowGemmArgs {
+  int M, k1, k2, K, nchunks;
+  const float* A1;
+  const float* A2;
+  const float* Bimg;
+  // cell epilogue
+  int H;
+  const float* bias;
+  const float* c_prev;
+  const float* h_skip;
+  float* gates;
+  float* c_out;
+  float* h_out;
+  // store2 epilogue
+  int n1, n2;
+  float* C1;
+  float* C2;
+};
+
+template <int NPAD>
+struct RowGemmSmem {
+  static constexpr uint32_t kA = tile_bytes(kTileM, kKC);  // one A tile (hi or lo)
+  static constexpr uint32_t kB = tile_bytes(NPAD, kKC);
+  static constexpr uint32_t kStage = 2 * kA + 2 * kB;
+  static constexpr uint32_t kBytes = 2 * kStage + 64;
+};
+
+template <int EPI, int NPAD>
+__global__ void __launch_bounds__(kThreads, 1) k_row_gemm(RowGemmArgs p) {
+  using S = RowGemmSmem<NPAD>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * S::kStage);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 2 * S::kStage + 32);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr uint32_t kCols = NPAD <= 64 ? 64 : (NPAD <= 128 ? 128 : 256);
+  if (warp == 0) tmem_alloc(tmem_slot, kCols);
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_barrier_init();
+  }
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sbase = smem_u32(smem);
+  constexpr uint32_t idesc = idesc_tf32(kTileM, NPAD);
+  constexpr uint32_t lboA = tile_lbo(kTileM), lboB = tile_lbo(NPAD);
+  const int ntiles = (p.M + kTileM - 1) / kTileM;
+  uint32_t g = 0;  // global chunk counter (stage = g & 1)
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = static_cast<int64_t>(tile) * kTileM;
+    for (int c = 0; c < p.nchunks; ++c, ++g) {
+      const uint32_t s = g & 1u;
+      if (g >= 2) mbar_wait(&bars[s], ((g - 2) >> 1) & 1u);
+      const uint32_t st = sbase + s * S::kStage;
+      // A chunk: 128 rows x 32 k, one float4 (4 k of one row) per item
+      const int kc0 = c * kKC;
+#pragma unroll
+      for (int it = 0; it < (kTileM * kKC / 4) / kThreads; ++it) {
+        const int f = tid + it * kThreads;
+        const int row = f / (kKC / 4), kq = f % (kKC / 4);
+        const int64_t grow = r0 + row;
+        const int k = kc0 + kq * 4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (grow < p.M && k < p.K) {
+          v = k < p.k1 ? __ldg(reinterpret_cast<const float4*>(p.A1 + grow * p.k1 + k))
+                       : __ldg(reinterpret_cast<const float4*>(p.A2 + grow * p.k2 + (k - p.k1)));
+        }
+        float h0, l0, h1, l1, h2, l2, h3, l3;
+        split_tf32(v.x, h0, l0);
+        split_tf32(v.y, h1, l1);
+        split_tf32(v.z, h2, l2);
+        split_tf32(v.w, h3, l3);
+        const uint32_t off = tile_offset(kTileM, row, kq * 4);
+        st_shared_v4(st + off, h0, h1, h2, h3);
+        st_shared_v4(st + S::kA + off, l0, l1, l2, l3);
+      }
+      // B chunk: contiguous [hi | lo] image
+      {
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(p.Bimg) + static_cast<int64_t>(c) * 2 * S::kB;
+        for (uint32_t o = tid * 16u; o < 2 * S::kB; o += kThreads * 16u) cp_async16(st + 2 * S::kA + o, src + o);
+        cp_async_wait_all();
+      }
+      fence_async_smem();
+      __syncthreads();
+      if (tid == 0) {
+        fence_after_sync();
+#pragma unroll
+        for (int ks = 0; ks < kKC / 8; ++ks) {
+          const uint64_t ahi = make_desc(st + 2 * ks * lboA, lboA, 128);
+          const uint64_t alo = make_desc(st + S::kA + 2 * ks * lboA, lboA, 128);
+          const uint64_t bhi = make_desc(st + 2 * S::kA + 2 * ks * lboB, lboB, 128);
+          const uint64_t blo = make_desc(st + 2 * S::kA + S::kB + 2 * ks * lboB, lboB, 128);
+          mma_tf32(tmem, ahi, bhi, idesc, (c > 0 || ks > 0) ? 1u : 0u);
+          mma_tf32(tmem, ahi, blo, idesc, 1u);
+          mma_tf32(tmem, alo, bhi, idesc, 1u);
+        }
+        commit(&bars[s]);
+      }
+    }
+    // accumulator of this tile complete once the last chunk's commit lands
+    mbar_wait(&bars[(g - 1) & 1u], ((g - 1) >> 1) & 1u);
+    fence_after_sync();
+    const int q = warp & 3, half = warp >> 2;
+    const int64_t row = r0 + q * 32 + lane;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    if (EPI == kEpiLstm || EPI == kEpiGru) {
+      const int H = p.H;
+      const int U = H / 2;
+      for (int j0 = half * U; j0 < (half + 1) * U; j0 += 16) {
+        float a0[16], a1[16], a2[16], a3[16];
+        tmem_ld16(trow + 0 * H + j0, a0);
+        tmem_ld16(trow + 1 * H + j0, a1);
+        tmem_ld16(trow + 2 * H + j0, a2);
+        tmem_ld16(trow + 3 * H + j0, a3);
+        tmem_wait_ld();
+        if (row < p.M) {
+          float* gr = p.gates + row * 4 * H;
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const int j = j0 + u;
+            const float p0 = a0[u] + p.bias[j];
+            const float p1 = a1[u] + p.bias[H + j];
+            if (EPI == kEpiLstm) {
+              const float ig = sigm(p0), fg = sigm(p1);
+              const float gg = tanhf(a2[u] + p.bias[2 * H + j]);
+              const float og = sigm(a3[u] + p.bias[3 * H + j]);
+              const float cc = fg * p.c_prev[row * H + j] + ig * gg;
+              a0[u] = ig;
+              a1[u] = fg;
+              a2[u] = gg;
+              a3[u] = og;
+              p.c_out[row * H + j] = cc;
+              p.h_out[row * H + j] = og * tanhf(cc);
+            } else {
+              const float rr = sigm(p0), zz = sigm(p1);
+              const float hn = a3[u];
+              const float nn = tanhf(a2[u] + rr * hn + p.bias[2 * H + j]);
+              a0[u] = rr;
+              a1[u] = zz;
+              a2[u] = nn;
+              p.h_out[row * H + j] = (1.f - zz) * nn + zz * p.h_skip[row * H + j];
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 16; u += 4) {
+            *reinterpret_cast<float4*>(gr + 0 * H + j0 + u) = make_float4(a0[u], a0[u + 1], a0[u + 2], a0[u + 3]);
+            *reinterpret_cast<float4*>(gr + 1 * H + j0 + u) = make_float4(a1[u], a1[u + 1], a1[u + 2], a1[u + 3]);
+            *reinterpret_cast<float4*>(gr + 2 * H + j0 + u) = make_float4(a2[u], a2[u + 1], a2[u + 2], a2[u + 3]);
+            *reinterpret_cast<float4*>(gr + 3 * H + j0 + u) = make_float4(a3[u], a3[u + 1], a3[u + 2], a3[u + 3]);
+          }
+        }
+      }
+    } else {
+      const int ncol = p.n1 + p.n2;
+      for (int cb = half * 16; cb < ncol; cb += 32) {
+        float a[16];
+        tmem_ld16(trow + cb, a);
+        tmem_wait_ld();
+        if (row < p.M) {
+#pragma unroll
+          for (int u = 0; u < 16; u += 4) {
+            const int col = cb + u;
+            if (col >= ncol) break;
+            float* dst = col < p.n1 ? p.C1 + row * p.n1 + col : p.C2 + row * p.n2 + (col - p.n1);
+            *reinterpret_cast<float4*>(dst) = make_float4(a[u], a[u + 1], a[u + 2], a[u + 3]);
+          }
+        }
+      }
+    }
+    tmem_wait_ld();
+    fence_before_sync();
+    __syncthreads();
+  }
+  __syncthreads();
+  fence_after_sync();
+  if (warp == 0) tmem_free(tmem, kCols);
+}
+
+// ------------------------------------------------------------- weight gradient
+// Partial D'_cta (Mg x Npad) = sum over this CTA's rows of G^T(:, rows) *
+// [X | Hm | 1](rows, :), with Mg = 4H in {128, 256} and Npad >= in + H + 1.
+constexpr int kKW = 16;  // rows (the MMA K) per staged chunk
+
+template <int MG, int NPAD>
+struct WgradSmem {
+  static constexpr uint32_t kA = tile_bytes(MG, kKW);
+  static constexpr uint32_t kB = tile_bytes(NPAD, kKW);
+  static constexpr uint32_t kStage = 2 * kA + 2 * kB;
+  static constexpr int kStages = 3;
+  static constexpr uint32_t kBytes = kStages * kStage + 64;
+};
+
+template <int MG, int NPAD>
+__global__ void __launch_bounds__(kThreads, 1)
+k_wgrad(int M, int in, int H, const float* __restrict__ G, const float* __restrict__ X,
+        const float* __restrict__ Hm, float* __restrict__ ws) {
+  using S = WgradSmem<MG, NPAD>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kStages * S::kStage);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + S::kStages * S::kStage + 32);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int kHalves = MG / 128;
+  constexpr uint32_t kCols = kHalves == 2 ? 512 : 256;
+  if (warp == 0) tmem_alloc(tmem_slot, kCols);
+  if (tid == 0) {
+    for (int s = 0; s < S::kStages; ++s) mbar_init(&bars[s], 1);
+    fence_barrier_init();
+  }
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sbase = smem_u32(smem);
+  constexpr uint32_t idesc = idesc_tf32(128, NPAD);
+  constexpr uint32_t lboA = tile_lbo(MG), lboB = tile_lbo(NPAD);
+  const int KXH = in + H;
+  const int64_t per = (static_cast<int64_t>(M) + gridDim.x - 1) / gridDim.x;
+  const int64_t rb = blockIdx.x * per;
+  const int64_t re = rb + per < M ? rb + per : M;
+  const int nchunks = re > rb ? static_cast<int>((re - rb + kKW - 1) / kKW) : 0;
+  for (int c = 0; c < nchunks; ++c) {
+    const uint32_t s = c % S::kStages;
+    if (c >= S::kStages) mbar_wait(&bars[s], ((c - S::kStages) / S::kStages) & 1u);
+    const uint32_t st = sbase + s * S::kStage;
+    const int64_t q0 = rb + static_cast<int64_t>(c) * kKW;
+    // A' = G^T: 4x4 blocks (4 gate columns x 4 rows), transposed in registers
+    for (int blk = tid; blk < (MG / 4) * (kKW / 4); blk += kThreads) {
+      const int m4 = blk % (MG / 4), k4 = blk / (MG / 4);
+      float v[4][4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int64_t row = q0 + k4 * 4 + r;
+        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (row < re) x = __ldg(reinterpret_cast<const float4*>(G + row * MG + m4 * 4));
+        v[r][0] = x.x; v[r][1] = x.y; v[r][2] = x.z; v[r][3] = x.w;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float h[4], l[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) split_tf32(v[r][i], h[r], l[r]);
+        const uint32_t off = tile_offset(MG, m4 * 4 + i, k4 * 4);
+        st_shared_v4(st + off, h[0], h[1], h[2], h[3]);
+        st_shared_v4(st + S::kA + off, l[0], l[1], l[2], l[3]);
+      }
+    }
+    // B' = [X | Hm | 1]^T
+    for (int blk = tid; blk < (NPAD / 4) * (kKW / 4); blk += kThreads) {
+      const int n4 = blk % (NPAD / 4), k4 = blk / (NPAD / 4);
+      float v[4][4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int64_t row = q0 + k4 * 4 + r;
+        const bool live = row < re;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int n = n4 * 4 + i;
+          float x = 0.f;
+          if (live) {
+            if (n < in) x = X[row * in + n];
+            else if (n < KXH) x = Hm[row * H + (n - in)];
+            else if (n == KXH) x = 1.f;
+          }
+          v[r][i] = x;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float h[4], l[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) split_tf32(v[r][i], h[r], l[r]);
+        const uint32_t off = tile_offset(NPAD, n4 * 4 + i, k4 * 4);
+        st_shared_v4(st + 2 * S::kA + off, h[0], h[1], h[2], h[3]);
+        st_shared_v4(st + 2 * S::kA + S::kB + off, l[0], l[1], l[2], l[3]);
+      }
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      fence_after_sync();
+#pragma unroll
+      for (int ks = 0; ks < kKW / 8; ++ks) {
+        const uint64_t bhi = make_desc(st + 2 * S::kA + 2 * ks * lboB, lboB, 128);
+        const uint64_t blo = make_desc(st + 2 * S::kA + S::kB + 2 * ks * lboB, lboB, 128);
+#pragma unroll
+        for (int hf = 0; hf < kHalves; ++hf) {
+          // rows [hf*128, hf*128+128) of A' start 16 core-matrix groups further
+          const uint32_t aoff = hf * 16 * 128;
+          const uint64_t ahi = make_desc(st + aoff + 2 * ks * lboA, lboA, 128);
+          const uint64_t alo = make_desc(st + S::kA + aoff + 2 * ks * lboA, lboA, 128);
+          const uint32_t d = tmem + hf * 256;
+          mma_tf32(d, ahi, bhi, idesc, (c > 0 || ks > 0) ? 1u : 0u);
+          mma_tf32(d, ahi, blo, idesc, 1u);
+          mma_tf32(d, alo, bhi, idesc, 1u);
+        }
+      }
+      commit(&bars[s]);
+    }
+  }
+  float* out = ws + static_cast<int64_t>(blockIdx.x) * MG * NPAD;
+  if (nchunks > 0) {
+    mbar_wait(&bars[(nchunks - 1) % S::kStages], ((nchunks - 1) / S::kStages) & 1u);
+    fence_after_sync();
+  }
+  const int q = warp & 3, half = warp >> 2;
+  for (int hf = 0; hf < kHalves; ++hf) {
+    const int m = hf * 128 + q * 32 + lane;
+    const uint32_t trow = tmem + hf * 256 + (static_cast<uint32_t>(q * 32) << 16);
+    for (int cb = half * 16; cb < NPAD; cb += 32) {
+      float a[16];
+      if (nchunks > 0) {
+        tmem_ld16(trow + cb, a);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) a[u] = 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; u += 4)
+        *reinterpret_cast<float4*>(out + static_cast<int64_t>(m) * NPAD + cb + u) =
+            make_float4(a[u], a[u + 1], a[u + 2], a[u + 3]);
+    }
+  }
+  tmem_wait_ld();
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  if (warp == 0) tmem_free(tmem, kCols);
+}
+
+// dW[k][m] += sum_cta D'[cta][m][k] (k < in+H); db[m] += sum_cta D'[cta][m][in+H] (m < nb)
+__global__ void k_wgrad_reduce(int nctas, int MG, int NPAD, int KXH, int nb, const float* __restrict__ ws,
+                               float* __restrict__ dW, float* __restrict__ db) {
+  const int64_t total = static_cast<int64_t>(MG) * (KXH + 1);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int m = static_cast<int>(i / (KXH + 1));
+    const int k = static_cast<int>(i % (KXH + 1));
+    float acc = 0.f;
+    for (int c = 0; c < nctas; ++c) acc += ws[(static_cast<int64_t>(c) * MG + m) * NPAD + k];
+    if (k < KXH) {
+      dW[static_cast<int64_t>(k) * MG + m] += acc;
+    } else if (m < nb) {
+      db[m] += acc;
+    }
+  }
+}
+
+int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+template <int EPI, int NPAD>
+void launch_row_gemm(const RowGemmArgs& a, cudaStream_t st) {
+  const uint32_t smem = RowGemmSmem<NPAD>::kBytes;
+  static bool configured = false;
+  if (!configured) {
+    DGNN_CUDA(cudaFuncSetAttribute(k_row_gemm<EPI, NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
+  const int ntiles = (a.M + kTileM - 1) / kTileM;
+  const int grid = ntiles < kNumSMs ? ntiles : kNumSMs;
+  DGNN_LAUNCH((k_row_gemm<EPI, NPAD>), grid, kThreads, smem, st, a);
+}
+
+template <int EPI>
+void dispatch_row_gemm(int npad, const RowGemmArgs& a, cudaStream_t st) {
+  switch (npad) {
+    case 64: launch_row_gemm<EPI, 64>(a, st); break;
+    case 128: launch_row_gemm<EPI, 128>(a, st); break;
+    case 192: launch_row_gemm<EPI, 192>(a, st); break;
+    case 256: launch_row_gemm<EPI, 256>(a, st); break;
+    default: throw std::invalid_argument("umma row gemm: unsupported N " + std::to_string(npad));
+  }
+}
+
+}  // namespace
+
+bool umma_cell_supported(int in, int H) {
+  return umma_enabled() && (H == 32 || H == 64) && in % 4 == 0 && in >= 4 && in + H + 1 <= 256;
+}
+
+bool umma_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DGNN_DISABLE_UMMA");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
+int64_t umma_bimage_floats(int N, int K) {
+  const int npad = N <= 64 ? 64 : (N <= 128 ? 128 : (N <= 192 ? 192 : 256));
+  const int nchunks = (K + kKC - 1) / kKC;
+  return static_cast<int64_t>(nchunks) * 2 * (tile_bytes(npad, kKC) / 4);
+}
+
+int umma_npad(int N) { return N <= 64 ? 64 : (N <= 128 ? 128 : (N <= 192 ? 192 : 256)); }
+
+void umma_pack_b(const float* M, int ld, bool trans, int n0, int N, int K, float* out,
+                 cudaStream_t stream) {
+  const int npad = umma_npad(N);
+  const int nchunks = (K + kKC - 1) / kKC;
+  const int64_t total = static_cast<int64_t>(nchunks) * npad * kKC;
+  DGNN_LAUNCH(k_pack_b, wave_grid(total, 256, 4), 256, 0, stream, M, ld, trans ? 1 : 0, n0, N, K,
+              npad, nchunks, out);
+}
+
+void umma_cell_forward(bool lstm, int n, int in, int H, const float* X, const float* Hm,
+                       const float* h_skip, const float* c_prev, const float* Bimg,
+                       const float* bias, float* gates, float* c, float* h, cudaStream_t stream) {
+  RowGemmArgs a{};
+  a.M = n;
+  a.k1 = in;
+  a.k2 = H;
+  a.K = in + H;
+  a.nchunks = (a.K + kKC - 1) / kKC;
+  a.A1 = X;
+  a.A2 = Hm;
+  a.Bimg = Bimg;
+  a.H = H;
+  a.bias = bias;
+  a.c_prev = c_prev;
+  a.h_skip = h_skip;
+  a.gates = gates;
+  a.c_out = c;
+  a.h_out = h;
+  const int npad = umma_npad(4 * H);
+  if (lstm) dispatch_row_gemm<kEpiLstm>(npad, a, stream);
+  else dispatch_row_gemm<kEpiGru>(npad, a, stream);
+}
+
+void umma_gemm_store2(int n, int K, const float* A, const float* Bimg, int n1, int n2, float* C1,
+                      float* C2, cudaStream_t stream) {
+  RowGemmArgs a{};
+  a.M = n;
+  a.k1 = K;
+  a.k2 = 0;
+  a.K = K;
+  a.nchunks = (K + kKC - 1) / kKC;
+  a.A1 = A;
+  a.A2 = A;
+  a.Bimg = Bimg;
+  a.n1 = n1;
+  a.n2 = n2;
+  a.C1 = C1;
+  a.C2 = C2;
+  dispatch_row_gemm<kEpiStore2>(umma_npad(n1 + n2), a, stream);
+}
+
+int64_t umma_wgrad_workspace(int in, int H) {
+  const int npad = round_up(in + H + 1, 16) <= 144 ? 144 : (round_up(in + H + 1, 16) <= 208 ? 208 : 256);
+  return static_cast<int64_t>(kNumSMs) * 4 * H * npad;
+}
+
+void umma_wgrad(int n, int in, int H, const float* G, const float* X, const float* Hm, float* dW,
+                int nb, float* db, float* ws, cudaStream_t stream) {
+  const int need = round_up(in + H + 1, 16);
+  const int npad = need <= 144 ? 144 : (need <= 208 ? 208 : 256);
+  const int grid = kNumSMs;
+  auto go = [&](auto mg_tag, auto np_tag) {
+    constexpr int MG = decltype(mg_tag)::value, NP = decltype(np_tag)::value;
+    const uint32_t smem = WgradSmem<MG, NP>::kBytes;
+    static bool configured = false;
+    if (!configured) {
+      DGNN_CUDA(cudaFuncSetAttribute(k_wgrad<MG, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      configured = true;
+    }
+    DGNN_LAUNCH((k_wgrad<MG, NP>), grid, kThreads, smem, stream, n, in, H, G, X, Hm, ws);
+  };
+  if (H == 64) {
+    if (npad == 144) go(std::integral_constant<int, 256>{}, std::integral_constant<int, 144>{});
+    else if (npad == 208) go(std::integral_constant<int, 256>{}, std::integral_constant<int, 208>{});
+    else go(std::integral_constant<int, 256>{}, std::integral_constant<int, 256>{});
+  } else {
+    if (npad == 144) go(std::integral_constant<int, 128>{}, std::integral_constant<int, 144>{});
+    else if (npad == 208) go(std::integral_constant<int, 128>{}, std::integral_constant<int, 208>{});
+    else go(std::integral_constant<int, 128>{}, std::integral_constant<int, 256>{});
+  }
+  const int64_t total = static_cast<int64_t>(4 * H) * (in + H + 1);
+  DGNN_LAUNCH(k_wgrad_reduce, wave_grid(total, 256, 4), 256, 0, stream, grid, 4 * H, npad, in + H, nb,
+              ws, dW, db);
+}
+
+}  // namespace cuda
+}  // namespace dgnn

@@ -1,0 +1,39 @@
+// tcgen05 3xTF32 kernels for the GraphRNN cell (umma_kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace dgnn {
+namespace cuda {
+
+// Shapes the tensor-core path covers (others use the FFMA kernels).
+bool umma_cell_supported(int in, int H);
+// Process-wide switch (env DGNN_DISABLE_UMMA=1 forces the FFMA path).
+bool umma_enabled();
+
+int umma_npad(int N);
+// floats of a packed B image for an N x K operand
+int64_t umma_bimage_floats(int N, int K);
+// Packed B image: B(n, k) = trans ? M[k*ld + n0+n] : M[(n0+n)*ld + k], split
+// into TF32 hi/lo tiles in the canonical UMMA layout, K chunked by 32.
+void umma_pack_b(const float* M, int ld, bool trans, int n0, int N, int K, float* out,
+                 cudaStream_t stream);
+
+// Fused cell forward: [X | Hm] * W (+ bias) -> gates / c / h (as cell_forward).
+void umma_cell_forward(bool lstm, int n, int in, int H, const float* X, const float* Hm,
+                       const float* h_skip, const float* c_prev, const float* Bimg,
+                       const float* bias, float* gates, float* c, float* h, cudaStream_t stream);
+
+// [C1 | C2] = A (n x K) * B^T with B the packed (n1+n2) x K image.
+void umma_gemm_store2(int n, int K, const float* A, const float* Bimg, int n1, int n2, float* C1,
+                      float* C2, cudaStream_t stream);
+
+// dW ((in+H) x 4H) += [X|Hm]^T G, db (nb) += colsum(G[:, :nb]); deterministic.
+int64_t umma_wgrad_workspace(int in, int H);
+void umma_wgrad(int n, int in, int H, const float* G, const float* X, const float* Hm, float* dW,
+                int nb, float* db, float* ws, cudaStream_t stream);
+
+}  // namespace cuda
+}  // namespace dgnn

@@ -270,3 +270,17 @@ def test_sharded_epoch_emulated_ranks(ref, api, pair, workers):
     inv = np.concatenate([s.invocations() for s in ranks])
     ref_inv = np.concatenate([r.invocations[r.invocations[:, 0] == m][:, 1:] for m in range(workers)])
     assert np.array_equal(inv, ref_inv)
+
+
+@pytest.mark.parametrize("arch", ARCHS)
+def test_sample_grads_tensor_core_cells(ref, api, pair, arch):
+    """hidden 64: the cell GEMMs run on the tcgen05 3xTF32 kernels."""
+    g_ref, g = pair
+    cfg_r = ref.RunCfg(arch=arch, hidden=64)
+    s = api.TrainSession(g, api.TrainConfig(arch=arch, hidden=64))
+    for w in (0, 1):
+        loss_r, pred_r, grads_r = g_ref.sample_grads(cfg_r, w)
+        loss, pred, grads = s.sample_grads(w)
+        assert abs(loss - loss_r) <= 1e-5 * abs(loss_r), (loss, loss_r)
+        assert nrel(pred, pred_r) < 1e-5
+        assert nrel(grads, grads_r) < 1e-4
