@@ -201,13 +201,10 @@ def main():
     P = sess.num_params
     grad = torch.empty(P, device="cuda")
 
+    from paper_2501_15348_b200.sharding import run_sharded_epoch
+
     def epoch():
-        nb = sess.begin_epoch()
-        for b in range(nb):
-            sess.local_grads(b, grad)
-            allreduce(grad)
-            sess.apply(grad)
-        sess.end_epoch()
+        run_sharded_epoch(sess, grad, allreduce if world > 1 else None)
 
     for _ in range(args.warmup):
         epoch()
@@ -279,12 +276,7 @@ def main():
         for _ in range(e_steps):
             g2 = synth.to_graph(stream)          # H2D of the compact graph + device build
             s2 = api.TrainSession(g2, cfg, rank=rank, stream=stream)
-            nb = s2.begin_epoch()
-            for b in range(nb):
-                s2.local_grads(b, grad)
-                allreduce(grad)
-                s2.apply(grad)
-            s2.end_epoch()                        # D2H of the per-window losses
+            run_sharded_epoch(s2, grad, allreduce if world > 1 else None)  # + D2H of window losses
             d2h = 8 * len(s2.losses())
             del s2, g2
         ev3.record(stream)

@@ -485,16 +485,10 @@ class TrainSession:
 
     def run_sharded_epoch(self, allreduce=None) -> list[float]:
         """One distsim epoch on this rank; `allreduce(tensor)` sums over ranks."""
+        from .sharding import run_sharded_epoch
         torch = _torch()
         g = torch.empty(self.num_params, device="cuda")
-        nb = self.begin_epoch()
-        for b in range(nb):
-            self.local_grads(b, g)
-            if allreduce is not None:
-                torch.cuda.current_stream().synchronize()
-                allreduce(g)
-            self.apply(g)
-        self.end_epoch()
+        run_sharded_epoch(self, g, allreduce)
         return self.losses()
 
     def losses(self) -> np.ndarray:

@@ -195,6 +195,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_row_gemm(RowGemmArgs p) {
         tmem_wait_ld();
         if (row < p.M) {
           float* gr = p.gates + row * 4 * H;
+          // state rows in / out as 64 B vectors (full sectors per thread)
+          float sv[16], co[16], ho[16];
+          const float* sp = (EPI == kEpiLstm ? p.c_prev : p.h_skip) + row * H + j0;
+#pragma unroll
+          for (int u = 0; u < 16; u += 4) {
+            const float4 x = __ldg(reinterpret_cast<const float4*>(sp + u));
+            sv[u] = x.x; sv[u + 1] = x.y; sv[u + 2] = x.z; sv[u + 3] = x.w;
+          }
 #pragma unroll
           for (int u = 0; u < 16; ++u) {
             const int j = j0 + u;
@@ -204,13 +212,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_row_gemm(RowGemmArgs p) {
               const float ig = sigm(p0), fg = sigm(p1);
               const float gg = tanhf(a2[u] + p.bias[2 * H + j]);
               const float og = sigm(a3[u] + p.bias[3 * H + j]);
-              const float cc = fg * p.c_prev[row * H + j] + ig * gg;
+              const float cc = fg * sv[u] + ig * gg;
               a0[u] = ig;
               a1[u] = fg;
               a2[u] = gg;
               a3[u] = og;
-              p.c_out[row * H + j] = cc;
-              p.h_out[row * H + j] = og * tanhf(cc);
+              co[u] = cc;
+              ho[u] = og * tanhf(cc);
             } else {
               const float rr = sigm(p0), zz = sigm(p1);
               const float hn = a3[u];
@@ -218,8 +226,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_row_gemm(RowGemmArgs p) {
               a0[u] = rr;
               a1[u] = zz;
               a2[u] = nn;
-              p.h_out[row * H + j] = (1.f - zz) * nn + zz * p.h_skip[row * H + j];
+              ho[u] = (1.f - zz) * nn + zz * sv[u];
             }
+          }
+#pragma unroll
+          for (int u = 0; u < 16; u += 4) {
+            if (EPI == kEpiLstm)
+              *reinterpret_cast<float4*>(p.c_out + row * H + j0 + u) = make_float4(co[u], co[u + 1], co[u + 2], co[u + 3]);
+            *reinterpret_cast<float4*>(p.h_out + row * H + j0 + u) = make_float4(ho[u], ho[u + 1], ho[u + 2], ho[u + 3]);
           }
 #pragma unroll
           for (int u = 0; u < 16; u += 4) {

@@ -245,12 +245,17 @@ def test_sharded_epoch_emulated_ranks(ref, api, pair, workers):
     by bench.py --gpus N)."""
     import torch
     g_ref, g = pair
-    cfg_r = ref.RunCfg(arch="tgcn", hidden=16, workers=workers, epochs=2)
+    # SGD keeps the parameter comparison linear in the gradient error (Adam's
+    # first steps amplify fp32-vs-fp64 noise on near-zero gradient entries to
+    # +-lr); the Adam step itself is covered by the seq-first test.
+    cfg_r = ref.RunCfg(arch="tgcn", hidden=16, workers=workers, epochs=2, optimizer="sgd", lr=0.1)
     r = g_ref.run(cfg_r)
-    ranks = [api.TrainSession(g, api.TrainConfig(arch="tgcn", hidden=16, workers=workers), rank=m)
+    ranks = [api.TrainSession(g, api.TrainConfig(arch="tgcn", hidden=16, workers=workers,
+                                                 optimizer="sgd", lr=0.1), rank=m)
              for m in range(workers)]
     P = ranks[0].num_params
-    losses = []
+    W = ranks[0].windows()[0]
+    losses, first = [], None
     for _ in range(2):
         nbs = [s.begin_epoch() for s in ranks]
         for b in range(nbs[0]):
@@ -258,15 +263,18 @@ def test_sharded_epoch_emulated_ranks(ref, api, pair, workers):
             for s, buf in zip(ranks, bufs):
                 s.local_grads(b, buf)
             total = torch.stack(bufs).sum(0)
+            if first is None:
+                first = (total / W).cpu().numpy()
             for s in ranks:
                 assert s.apply(total.clone())
         for s in ranks:
             s.end_epoch()
             losses.append(s.losses())
+    assert nrel(first, r.grads0) < 1e-4  # ordered window-gradient sum / W
     # reference visit order: epoch-major, then worker, then window
     assert nrel(np.concatenate(losses), r.losses) < 1e-4
     for s in ranks:
-        assert nrel(s.params(), r.params) < 1e-3
+        assert nrel(s.params(), r.params) < 1e-5
     inv = np.concatenate([s.invocations() for s in ranks])
     ref_inv = np.concatenate([r.invocations[r.invocations[:, 0] == m][:, 1:] for m in range(workers)])
     assert np.array_equal(inv, ref_inv)
