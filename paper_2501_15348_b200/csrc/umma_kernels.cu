@@ -9,12 +9,16 @@
 //   k_wgrad     per-CTA partial of G^T * [X | Hm | 1] over a contiguous row
 //               range (weight + bias gradients), reduced in fixed CTA order.
 //
-// One CTA per SM (persistent over row tiles). Operands are staged global ->
-// registers (3xTF32 split, transposition for the weight-gradient operands) ->
-// shared memory in the canonical K-major UMMA layout, double/triple buffered
-// against the asynchronous MMAs through mbarriers signalled by tcgen05.commit.
-// A single elected thread issues every tcgen05.mma; accumulators live in TMEM
-// and the epilogue reads them with tcgen05.ld.
+// k_row_gemm is a persistent, warp-specialised kernel (one CTA per SM):
+//   warps 0-3  producers: A tile global -> registers -> 3xTF32 split -> smem
+//              (canonical K-major UMMA layout); the leader also issues the
+//              bulk (TMA-engine) copy of the pre-split B chunk;
+//   warp 4     TMEM allocator + the single thread issuing tcgen05.mma;
+//   warps 8-15 epilogue: tcgen05.ld from TMEM, fused math, vector stores.
+// Smem stages (4 x K=16) are handed over with full/empty mbarriers
+// (expect_tx for the bulk copy, tcgen05.commit for release); the fp32
+// accumulator is double-buffered in TMEM (2 x 256 columns) so the epilogue of
+// tile i overlaps the MMAs of tile i+1.
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -31,18 +35,10 @@ namespace {
 
 using namespace umma;
 
-constexpr int kThreads = 256;
 constexpr int kTileM = 128;  // rows per MMA tile (cta_group::1, M = 128)
-constexpr int kKC = 32;      // K elements staged per chunk (4 MMA K-steps of 8)
+constexpr int kKC = 16;      // K elements per staged chunk (2 MMA K-steps of 8)
 
 __device__ __forceinline__ float sigm(float x) { return 1.f / (1.f + expf(-x)); }
-
-__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-}
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, float a, float b, float c, float d) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
@@ -95,26 +91,42 @@ struct RowGemmArgs {
   float* C2;
 };
 
+constexpr int kRgThreads = 512;  // 16 warps
+constexpr int kRgStages = 4;
+constexpr int kProducerThreads = 128;
+constexpr int kMmaWarp = 4;
+constexpr int kEpiWarp0 = 8;
+constexpr int kEpiWarps = 8;
+
 template <int NPAD>
 struct RowGemmSmem {
   static constexpr uint32_t kA = tile_bytes(kTileM, kKC);  // one A tile (hi or lo)
   static constexpr uint32_t kB = tile_bytes(NPAD, kKC);
   static constexpr uint32_t kStage = 2 * kA + 2 * kB;
-  static constexpr uint32_t kBytes = 2 * kStage + 64;
+  static constexpr uint32_t kBars = kStage * kRgStages;  // barrier block offset
+  static constexpr uint32_t kBytes = kBars + 128;
 };
 
 template <int EPI, int NPAD>
-__global__ void __launch_bounds__(kThreads, 1) k_row_gemm(RowGemmArgs p) {
+__global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
   using S = RowGemmSmem<NPAD>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * S::kStage);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 2 * S::kStage + 32);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kBars);
+  uint64_t* empty = full + kRgStages;
+  uint64_t* tfull = empty + kRgStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  constexpr uint32_t kCols = NPAD <= 64 ? 64 : (NPAD <= 128 ? 128 : 256);
-  if (warp == 0) tmem_alloc(tmem_slot, kCols);
+  if (warp == kMmaWarp) tmem_alloc(tmem_slot, 512);
   if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int s = 0; s < kRgStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], kEpiWarps);
+    }
     fence_barrier_init();
   }
   fence_before_sync();
@@ -122,157 +134,178 @@ __global__ void __launch_bounds__(kThreads, 1) k_row_gemm(RowGemmArgs p) {
   fence_after_sync();
   const uint32_t tmem = *tmem_slot;
   const uint32_t sbase = smem_u32(smem);
-  constexpr uint32_t idesc = idesc_tf32(kTileM, NPAD);
-  constexpr uint32_t lboA = tile_lbo(kTileM), lboB = tile_lbo(NPAD);
   const int ntiles = (p.M + kTileM - 1) / kTileM;
-  uint32_t g = 0;  // global chunk counter (stage = g & 1)
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t r0 = static_cast<int64_t>(tile) * kTileM;
-    for (int c = 0; c < p.nchunks; ++c, ++g) {
-      const uint32_t s = g & 1u;
-      if (g >= 2) mbar_wait(&bars[s], ((g - 2) >> 1) & 1u);
-      const uint32_t st = sbase + s * S::kStage;
-      // A chunk: 128 rows x 32 k, one float4 (4 k of one row) per item
-      const int kc0 = c * kKC;
+
+  if (warp < 4) {
+    // ---------------- producers
+    uint32_t g = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int64_t r0 = static_cast<int64_t>(tile) * kTileM;
+      for (int c = 0; c < p.nchunks; ++c, ++g) {
+        const uint32_t s = g % kRgStages, ph = (g / kRgStages) & 1u;
+        mbar_wait(&empty[s], ph ^ 1u);
+        const uint32_t st = sbase + s * S::kStage;
+        const int kc0 = c * kKC;
 #pragma unroll
-      for (int it = 0; it < (kTileM * kKC / 4) / kThreads; ++it) {
-        const int f = tid + it * kThreads;
-        const int row = f / (kKC / 4), kq = f % (kKC / 4);
-        const int64_t grow = r0 + row;
-        const int k = kc0 + kq * 4;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (grow < p.M && k < p.K) {
-          v = k < p.k1 ? __ldg(reinterpret_cast<const float4*>(p.A1 + grow * p.k1 + k))
-                       : __ldg(reinterpret_cast<const float4*>(p.A2 + grow * p.k2 + (k - p.k1)));
+        for (int it = 0; it < (kTileM * kKC / 4) / kProducerThreads; ++it) {
+          const int f = tid + it * kProducerThreads;
+          const int row = f / (kKC / 4), kq = f % (kKC / 4);
+          const int64_t grow = r0 + row;
+          const int k = kc0 + kq * 4;
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (grow < p.M && k < p.K) {
+            v = k < p.k1 ? __ldg(reinterpret_cast<const float4*>(p.A1 + grow * p.k1 + k))
+                         : __ldg(reinterpret_cast<const float4*>(p.A2 + grow * p.k2 + (k - p.k1)));
+          }
+          float h0, l0, h1, l1, h2, l2, h3, l3;
+          split_tf32(v.x, h0, l0);
+          split_tf32(v.y, h1, l1);
+          split_tf32(v.z, h2, l2);
+          split_tf32(v.w, h3, l3);
+          const uint32_t off = tile_offset(kTileM, row, kq * 4);
+          st_shared_v4(st + off, h0, h1, h2, h3);
+          st_shared_v4(st + S::kA + off, l0, l1, l2, l3);
         }
-        float h0, l0, h1, l1, h2, l2, h3, l3;
-        split_tf32(v.x, h0, l0);
-        split_tf32(v.y, h1, l1);
-        split_tf32(v.z, h2, l2);
-        split_tf32(v.w, h3, l3);
-        const uint32_t off = tile_offset(kTileM, row, kq * 4);
-        st_shared_v4(st + off, h0, h1, h2, h3);
-        st_shared_v4(st + S::kA + off, l0, l1, l2, l3);
-      }
-      // B chunk: contiguous [hi | lo] image
-      {
-        const uint8_t* src = reinterpret_cast<const uint8_t*>(p.Bimg) + static_cast<int64_t>(c) * 2 * S::kB;
-        for (uint32_t o = tid * 16u; o < 2 * S::kB; o += kThreads * 16u) cp_async16(st + 2 * S::kA + o, src + o);
-        cp_async_wait_all();
-      }
-      fence_async_smem();
-      __syncthreads();
-      if (tid == 0) {
-        fence_after_sync();
-#pragma unroll
-        for (int ks = 0; ks < kKC / 8; ++ks) {
-          const uint64_t ahi = make_desc(st + 2 * ks * lboA, lboA, 128);
-          const uint64_t alo = make_desc(st + S::kA + 2 * ks * lboA, lboA, 128);
-          const uint64_t bhi = make_desc(st + 2 * S::kA + 2 * ks * lboB, lboB, 128);
-          const uint64_t blo = make_desc(st + 2 * S::kA + S::kB + 2 * ks * lboB, lboB, 128);
-          mma_tf32(tmem, ahi, bhi, idesc, (c > 0 || ks > 0) ? 1u : 0u);
-          mma_tf32(tmem, ahi, blo, idesc, 1u);
-          mma_tf32(tmem, alo, bhi, idesc, 1u);
+        fence_async_smem();
+        named_bar_sync(1, kProducerThreads);
+        if (tid == 0) {
+          mbar_arrive_expect_tx(&full[s], 2 * S::kB);
+          bulk_g2s(st + 2 * S::kA,
+                   reinterpret_cast<const uint8_t*>(p.Bimg) + static_cast<int64_t>(c) * 2 * S::kB,
+                   2 * S::kB, &full[s]);
         }
-        commit(&bars[s]);
       }
     }
-    // accumulator of this tile complete once the last chunk's commit lands
-    mbar_wait(&bars[(g - 1) & 1u], ((g - 1) >> 1) & 1u);
-    fence_after_sync();
-    const int q = warp & 3, half = warp >> 2;
-    const int64_t row = r0 + q * 32 + lane;
-    const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
-    if (EPI == kEpiLstm || EPI == kEpiGru) {
-      const int H = p.H;
-      const int U = H / 2;
-      for (int j0 = half * U; j0 < (half + 1) * U; j0 += 16) {
-        float a0[16], a1[16], a2[16], a3[16];
-        tmem_ld16(trow + 0 * H + j0, a0);
-        tmem_ld16(trow + 1 * H + j0, a1);
-        tmem_ld16(trow + 2 * H + j0, a2);
-        tmem_ld16(trow + 3 * H + j0, a3);
-        tmem_wait_ld();
-        if (row < p.M) {
-          float* gr = p.gates + row * 4 * H;
-          // state rows in / out as 64 B vectors (full sectors per thread)
-          float sv[16], co[16], ho[16];
-          const float* sp = (EPI == kEpiLstm ? p.c_prev : p.h_skip) + row * H + j0;
+  } else if (warp == kMmaWarp) {
+    // ---------------- MMA issuer
+    constexpr uint32_t idesc = idesc_tf32(kTileM, NPAD);
+    constexpr uint32_t lboA = tile_lbo(kTileM), lboB = tile_lbo(NPAD);
+    uint32_t g = 0, it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const uint32_t b = it & 1u;
+      mbar_wait(&tempty[b], ((it >> 1) & 1u) ^ 1u);
+      fence_after_sync();
+      const uint32_t d = tmem + b * 256;
+      for (int c = 0; c < p.nchunks; ++c, ++g) {
+        const uint32_t s = g % kRgStages, ph = (g / kRgStages) & 1u;
+        mbar_wait(&full[s], ph);
+        fence_after_sync();
+        const uint32_t st = sbase + s * S::kStage;
+        if (lane == 0) {
 #pragma unroll
-          for (int u = 0; u < 16; u += 4) {
-            const float4 x = __ldg(reinterpret_cast<const float4*>(sp + u));
-            sv[u] = x.x; sv[u + 1] = x.y; sv[u + 2] = x.z; sv[u + 3] = x.w;
+          for (int ks = 0; ks < kKC / 8; ++ks) {
+            const uint64_t ahi = make_desc(st + 2 * ks * lboA, lboA, 128);
+            const uint64_t alo = make_desc(st + S::kA + 2 * ks * lboA, lboA, 128);
+            const uint64_t bhi = make_desc(st + 2 * S::kA + 2 * ks * lboB, lboB, 128);
+            const uint64_t blo = make_desc(st + 2 * S::kA + S::kB + 2 * ks * lboB, lboB, 128);
+            mma_tf32(d, ahi, bhi, idesc, (c > 0 || ks > 0) ? 1u : 0u);
+            mma_tf32(d, ahi, blo, idesc, 1u);
+            mma_tf32(d, alo, bhi, idesc, 1u);
           }
+          commit(&empty[s]);
+          if (c == p.nchunks - 1) commit(&tfull[b]);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp >= kEpiWarp0) {
+    // ---------------- epilogue
+    const int q = warp & 3, half = (warp - kEpiWarp0) >> 2;
+    uint32_t it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const uint32_t b = it & 1u;
+      mbar_wait(&tfull[b], (it >> 1) & 1u);
+      fence_after_sync();
+      const int64_t row = static_cast<int64_t>(tile) * kTileM + q * 32 + lane;
+      const uint32_t trow = tmem + b * 256 + (static_cast<uint32_t>(q * 32) << 16);
+      if (EPI == kEpiLstm || EPI == kEpiGru) {
+        const int H = p.H;
+        const int U = H / 2;
+        for (int j0 = half * U; j0 < (half + 1) * U; j0 += 8) {
+          float a0[8], a1[8], a2[8], a3[8];
+          tmem_ld8(trow + 0 * H + j0, a0);
+          tmem_ld8(trow + 1 * H + j0, a1);
+          tmem_ld8(trow + 2 * H + j0, a2);
+          tmem_ld8(trow + 3 * H + j0, a3);
+          tmem_wait_ld();
+          if (row < p.M) {
+            float sv[8], ho[8], co[8];
+            const float* sp = (EPI == kEpiLstm ? p.c_prev : p.h_skip) + row * H + j0;
+            const float4 x0 = __ldg(reinterpret_cast<const float4*>(sp));
+            const float4 x1 = __ldg(reinterpret_cast<const float4*>(sp + 4));
+            sv[0] = x0.x; sv[1] = x0.y; sv[2] = x0.z; sv[3] = x0.w;
+            sv[4] = x1.x; sv[5] = x1.y; sv[6] = x1.z; sv[7] = x1.w;
 #pragma unroll
-          for (int u = 0; u < 16; ++u) {
-            const int j = j0 + u;
-            const float p0 = a0[u] + p.bias[j];
-            const float p1 = a1[u] + p.bias[H + j];
-            if (EPI == kEpiLstm) {
-              const float ig = sigm(p0), fg = sigm(p1);
-              const float gg = tanhf(a2[u] + p.bias[2 * H + j]);
-              const float og = sigm(a3[u] + p.bias[3 * H + j]);
-              const float cc = fg * sv[u] + ig * gg;
-              a0[u] = ig;
-              a1[u] = fg;
-              a2[u] = gg;
-              a3[u] = og;
-              co[u] = cc;
-              ho[u] = og * tanhf(cc);
-            } else {
-              const float rr = sigm(p0), zz = sigm(p1);
-              const float hn = a3[u];
-              const float nn = tanhf(a2[u] + rr * hn + p.bias[2 * H + j]);
-              a0[u] = rr;
-              a1[u] = zz;
-              a2[u] = nn;
-              ho[u] = (1.f - zz) * nn + zz * sv[u];
+            for (int u = 0; u < 8; ++u) {
+              const int j = j0 + u;
+              const float p0 = a0[u] + p.bias[j];
+              const float p1 = a1[u] + p.bias[H + j];
+              if (EPI == kEpiLstm) {
+                const float ig = sigm(p0), fg = sigm(p1);
+                const float gg = tanhf(a2[u] + p.bias[2 * H + j]);
+                const float og = sigm(a3[u] + p.bias[3 * H + j]);
+                const float cc = fg * sv[u] + ig * gg;
+                a0[u] = ig;
+                a1[u] = fg;
+                a2[u] = gg;
+                a3[u] = og;
+                co[u] = cc;
+                ho[u] = og * tanhf(cc);
+              } else {
+                const float rr = sigm(p0), zz = sigm(p1);
+                const float hn = a3[u];
+                const float nn = tanhf(a2[u] + rr * hn + p.bias[2 * H + j]);
+                a0[u] = rr;
+                a1[u] = zz;
+                a2[u] = nn;
+                ho[u] = (1.f - zz) * nn + zz * sv[u];
+              }
+            }
+            float* gr = p.gates + row * 4 * H + j0;
+#pragma unroll
+            for (int u = 0; u < 8; u += 4) {
+              *reinterpret_cast<float4*>(gr + 0 * H + u) = make_float4(a0[u], a0[u + 1], a0[u + 2], a0[u + 3]);
+              *reinterpret_cast<float4*>(gr + 1 * H + u) = make_float4(a1[u], a1[u + 1], a1[u + 2], a1[u + 3]);
+              *reinterpret_cast<float4*>(gr + 2 * H + u) = make_float4(a2[u], a2[u + 1], a2[u + 2], a2[u + 3]);
+              *reinterpret_cast<float4*>(gr + 3 * H + u) = make_float4(a3[u], a3[u + 1], a3[u + 2], a3[u + 3]);
+              if (EPI == kEpiLstm)
+                *reinterpret_cast<float4*>(p.c_out + row * H + j0 + u) = make_float4(co[u], co[u + 1], co[u + 2], co[u + 3]);
+              *reinterpret_cast<float4*>(p.h_out + row * H + j0 + u) = make_float4(ho[u], ho[u + 1], ho[u + 2], ho[u + 3]);
             }
           }
+        }
+      } else {
+        const int ncol = p.n1 + p.n2;
+        for (int cb = half * 8; cb < ncol; cb += 16) {
+          float a[8];
+          tmem_ld8(trow + cb, a);
+          tmem_wait_ld();
+          if (row < p.M) {
 #pragma unroll
-          for (int u = 0; u < 16; u += 4) {
-            if (EPI == kEpiLstm)
-              *reinterpret_cast<float4*>(p.c_out + row * H + j0 + u) = make_float4(co[u], co[u + 1], co[u + 2], co[u + 3]);
-            *reinterpret_cast<float4*>(p.h_out + row * H + j0 + u) = make_float4(ho[u], ho[u + 1], ho[u + 2], ho[u + 3]);
-          }
-#pragma unroll
-          for (int u = 0; u < 16; u += 4) {
-            *reinterpret_cast<float4*>(gr + 0 * H + j0 + u) = make_float4(a0[u], a0[u + 1], a0[u + 2], a0[u + 3]);
-            *reinterpret_cast<float4*>(gr + 1 * H + j0 + u) = make_float4(a1[u], a1[u + 1], a1[u + 2], a1[u + 3]);
-            *reinterpret_cast<float4*>(gr + 2 * H + j0 + u) = make_float4(a2[u], a2[u + 1], a2[u + 2], a2[u + 3]);
-            *reinterpret_cast<float4*>(gr + 3 * H + j0 + u) = make_float4(a3[u], a3[u + 1], a3[u + 2], a3[u + 3]);
+            for (int u = 0; u < 8; u += 4) {
+              const int col = cb + u;
+              if (col < ncol) {
+                float* dst = col < p.n1 ? p.C1 + row * p.n1 + col : p.C2 + row * p.n2 + (col - p.n1);
+                *reinterpret_cast<float4*>(dst) = make_float4(a[u], a[u + 1], a[u + 2], a[u + 3]);
+              }
+            }
           }
         }
       }
-    } else {
-      const int ncol = p.n1 + p.n2;
-      for (int cb = half * 16; cb < ncol; cb += 32) {
-        float a[16];
-        tmem_ld16(trow + cb, a);
-        tmem_wait_ld();
-        if (row < p.M) {
-#pragma unroll
-          for (int u = 0; u < 16; u += 4) {
-            const int col = cb + u;
-            if (col >= ncol) break;
-            float* dst = col < p.n1 ? p.C1 + row * p.n1 + col : p.C2 + row * p.n2 + (col - p.n1);
-            *reinterpret_cast<float4*>(dst) = make_float4(a[u], a[u + 1], a[u + 2], a[u + 3]);
-          }
-        }
-      }
+      fence_before_sync();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[b]);
     }
-    tmem_wait_ld();
-    fence_before_sync();
-    __syncthreads();
   }
   __syncthreads();
   fence_after_sync();
-  if (warp == 0) tmem_free(tmem, kCols);
+  if (warp == kMmaWarp) tmem_free(tmem, 512);
 }
 
 // ------------------------------------------------------------- weight gradient
 // Partial D'_cta (Mg x Npad) = sum over this CTA's rows of G^T(:, rows) *
 // [X | Hm | 1](rows, :), with Mg = 4H in {128, 256} and Npad >= in + H + 1.
+constexpr int kThreads = 256;
 constexpr int kKW = 16;  // rows (the MMA K) per staged chunk
 
 template <int MG, int NPAD>
@@ -346,17 +379,24 @@ k_wgrad(int M, int in, int H, const float* __restrict__ G, const float* __restri
       for (int r = 0; r < 4; ++r) {
         const int64_t row = q0 + k4 * 4 + r;
         const bool live = row < re;
+        const int n = n4 * 4;
+        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (live) {
+          if (n + 3 < in) {
+            x = __ldg(reinterpret_cast<const float4*>(X + row * in + n));
+          } else if (n >= in && n + 3 < KXH) {
+            x = __ldg(reinterpret_cast<const float4*>(Hm + row * H + (n - in)));
+          } else {
+            float t[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int n = n4 * 4 + i;
-          float x = 0.f;
-          if (live) {
-            if (n < in) x = X[row * in + n];
-            else if (n < KXH) x = Hm[row * H + (n - in)];
-            else if (n == KXH) x = 1.f;
+            for (int i = 0; i < 4; ++i) {
+              const int nn = n + i;
+              t[i] = nn < in ? X[row * in + nn] : (nn < KXH ? Hm[row * H + (nn - in)] : (nn == KXH ? 1.f : 0.f));
+            }
+            x = make_float4(t[0], t[1], t[2], t[3]);
           }
-          v[r][i] = x;
         }
+        v[r][0] = x.x; v[r][1] = x.y; v[r][2] = x.z; v[r][3] = x.w;
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -452,7 +492,7 @@ void launch_row_gemm(const RowGemmArgs& a, cudaStream_t st) {
   }
   const int ntiles = (a.M + kTileM - 1) / kTileM;
   const int grid = ntiles < kNumSMs ? ntiles : kNumSMs;
-  DGNN_LAUNCH((k_row_gemm<EPI, NPAD>), grid, kThreads, smem, st, a);
+  DGNN_LAUNCH((k_row_gemm<EPI, NPAD>), grid, kRgThreads, smem, st, a);
 }
 
 template <int EPI>
@@ -468,10 +508,6 @@ void dispatch_row_gemm(int npad, const RowGemmArgs& a, cudaStream_t st) {
 
 }  // namespace
 
-bool umma_cell_supported(int in, int H) {
-  return umma_enabled() && (H == 32 || H == 64) && in % 4 == 0 && in >= 4 && in + H + 1 <= 256;
-}
-
 bool umma_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("DGNN_DISABLE_UMMA");
@@ -480,13 +516,17 @@ bool umma_enabled() {
   return on;
 }
 
-int64_t umma_bimage_floats(int N, int K) {
-  const int npad = N <= 64 ? 64 : (N <= 128 ? 128 : (N <= 192 ? 192 : 256));
-  const int nchunks = (K + kKC - 1) / kKC;
-  return static_cast<int64_t>(nchunks) * 2 * (tile_bytes(npad, kKC) / 4);
+bool umma_cell_supported(int in, int H) {
+  return umma_enabled() && (H == 32 || H == 64) && in % 4 == 0 && in >= 4 && in + H + 1 <= 256;
 }
 
 int umma_npad(int N) { return N <= 64 ? 64 : (N <= 128 ? 128 : (N <= 192 ? 192 : 256)); }
+
+int64_t umma_bimage_floats(int N, int K) {
+  const int npad = umma_npad(N);
+  const int nchunks = (K + kKC - 1) / kKC;
+  return static_cast<int64_t>(nchunks) * 2 * (tile_bytes(npad, kKC) / 4);
+}
 
 void umma_pack_b(const float* M, int ld, bool trans, int n0, int N, int K, float* out,
                  cudaStream_t stream) {
@@ -540,7 +580,8 @@ void umma_gemm_store2(int n, int K, const float* A, const float* Bimg, int n1, i
 }
 
 int64_t umma_wgrad_workspace(int in, int H) {
-  const int npad = round_up(in + H + 1, 16) <= 144 ? 144 : (round_up(in + H + 1, 16) <= 208 ? 208 : 256);
+  const int need = round_up(in + H + 1, 16);
+  const int npad = need <= 144 ? 144 : (need <= 208 ? 208 : 256);
   return static_cast<int64_t>(kNumSMs) * 4 * H * npad;
 }
 
