@@ -35,10 +35,17 @@ def _np_ptr(a):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
 
 
+CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy
+
+
 def _stream_handle(stream):
+    """cudaStream_t for the C ABI. torch's default stream has handle 0, which
+    the C ABI would read as "library-owned stream"; pass cudaStreamLegacy so
+    the library and torch share the same (synchronising) default stream."""
     if stream is None:
         return None
-    return C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+    h = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    return C.c_void_p(h if h else CUDA_STREAM_LEGACY)
 
 
 def current_stream():

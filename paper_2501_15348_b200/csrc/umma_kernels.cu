@@ -92,20 +92,34 @@ struct RowGemmArgs {
 };
 
 constexpr int kRgThreads = 512;  // 16 warps
-constexpr int kRgStages = 4;
+constexpr int kRgStages = 3;     // MMA operand stages (A hi/lo + B hi/lo)
+constexpr int kRawSlots = 6;     // cp.async prefetch depth of raw fp32 A chunks
 constexpr int kProducerThreads = 128;
 constexpr int kMmaWarp = 4;
 constexpr int kEpiWarp0 = 8;
 constexpr int kEpiWarps = 8;
+constexpr int kRawPerThread = (kTileM * kKC / 4) / kProducerThreads;  // float4 per thread per chunk
 
 template <int NPAD>
 struct RowGemmSmem {
   static constexpr uint32_t kA = tile_bytes(kTileM, kKC);  // one A tile (hi or lo)
   static constexpr uint32_t kB = tile_bytes(NPAD, kKC);
   static constexpr uint32_t kStage = 2 * kA + 2 * kB;
-  static constexpr uint32_t kBars = kStage * kRgStages;  // barrier block offset
+  static constexpr uint32_t kRaw = kTileM * kKC * 4;      // one raw fp32 A chunk
+  static constexpr uint32_t kRawOff = kStage * kRgStages;
+  static constexpr uint32_t kBars = kRawOff + kRaw * kRawSlots;  // barrier block offset
   static constexpr uint32_t kBytes = kBars + 128;
 };
+
+__device__ __forceinline__ void cp_async16_zfill(uint32_t saddr, const void* g, bool valid) {
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 template <int EPI, int NPAD>
 __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
@@ -138,25 +152,51 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
 
   if (warp < 4) {
     // ---------------- producers
-    uint32_t g = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const int64_t r0 = static_cast<int64_t>(tile) * kTileM;
-      for (int c = 0; c < p.nchunks; ++c, ++g) {
-        const uint32_t s = g % kRgStages, ph = (g / kRgStages) & 1u;
-        mbar_wait(&empty[s], ph ^ 1u);
-        const uint32_t st = sbase + s * S::kStage;
-        const int kc0 = c * kKC;
+    // Flat sequence of (tile, chunk) items; raw fp32 A chunks are prefetched
+    // kRawSlots - 1 items ahead with cp.async (each thread later re-reads only
+    // what it copied, so no cross-thread sync is needed before the split).
+    const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int total = my_tiles * p.nchunks;
+    const uint32_t raw0 = sbase + S::kRawOff;
+    auto issue = [&](int item) {
+      if (item < total) {
+        const int tile = blockIdx.x + (item / p.nchunks) * gridDim.x;
+        const int kc0 = (item % p.nchunks) * kKC;
+        const int64_t r0 = static_cast<int64_t>(tile) * kTileM;
+        const uint32_t slot = raw0 + (item % kRawSlots) * S::kRaw;
 #pragma unroll
-        for (int it = 0; it < (kTileM * kKC / 4) / kProducerThreads; ++it) {
+        for (int it = 0; it < kRawPerThread; ++it) {
           const int f = tid + it * kProducerThreads;
           const int row = f / (kKC / 4), kq = f % (kKC / 4);
           const int64_t grow = r0 + row;
           const int k = kc0 + kq * 4;
-          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (grow < p.M && k < p.K) {
-            v = k < p.k1 ? __ldg(reinterpret_cast<const float4*>(p.A1 + grow * p.k1 + k))
-                         : __ldg(reinterpret_cast<const float4*>(p.A2 + grow * p.k2 + (k - p.k1)));
-          }
+          const bool valid = grow < p.M && k < p.K;
+          const float* src = !valid ? p.A1
+                                    : (k < p.k1 ? p.A1 + grow * p.k1 + k : p.A2 + grow * p.k2 + (k - p.k1));
+          cp_async16_zfill(slot + f * 16, src, valid);
+        }
+      }
+      cp_async_commit();  // one group per item (possibly empty) keeps the accounting uniform
+    };
+    for (int i = 0; i < kRawSlots - 1; ++i) issue(i);
+    for (int item = 0; item < total; ++item) {
+      issue(item + kRawSlots - 1);
+      cp_async_wait<kRawSlots - 1>();
+      const uint32_t g = static_cast<uint32_t>(item);
+      const int c = item % p.nchunks;
+      const uint32_t s = g % kRgStages, ph = (g / kRgStages) & 1u;
+      mbar_wait(&empty[s], ph ^ 1u);
+      const uint32_t st = sbase + s * S::kStage;
+      const uint32_t slot = raw0 + (item % kRawSlots) * S::kRaw;
+      {
+#pragma unroll
+        for (int it = 0; it < kRawPerThread; ++it) {
+          const int f = tid + it * kProducerThreads;
+          const int row = f / (kKC / 4), kq = f % (kKC / 4);
+          float4 v;
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                       : "r"(slot + f * 16));
           float h0, l0, h1, l1, h2, l2, h3, l3;
           split_tf32(v.x, h0, l0);
           split_tf32(v.y, h1, l1);
@@ -176,6 +216,7 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
         }
       }
     }
+    cp_async_wait<0>();
   } else if (warp == kMmaWarp) {
     // ---------------- MMA issuer
     constexpr uint32_t idesc = idesc_tf32(kTileM, NPAD);
