@@ -92,15 +92,17 @@ __device__ inline void accumulate(float (&acc)[V], int32_t (&arg)[V], const floa
 // ---------------------------------------------------------------- K1 scratch
 template <int V, int G, int KIND>
 __global__ void __launch_bounds__(kThreads)
-k_agg_scratch(int n, int w, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
-              const float* __restrict__ F, float* __restrict__ out, float* __restrict__ degree,
-              float* __restrict__ msum, int32_t* __restrict__ argext) {
+k_agg_scratch(int n, int w, int c0, int wc, const int64_t* __restrict__ ptr,
+              const int32_t* __restrict__ idx, const float* __restrict__ F, float* __restrict__ out,
+              float* __restrict__ degree, float* __restrict__ msum, int32_t* __restrict__ argext) {
+  // columns [c0, c0 + wc) of a row-major n x w operand (L2-sized column slice)
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
   constexpr int kRowsPerWarp = 32 / G;
   const int64_t warp_global = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
   const int64_t warp_stride = (static_cast<int64_t>(gridDim.x) * kThreads) >> 5;
-  const int nchunk = (w + G * V - 1) / (G * V);
+  const int nchunk = (wc + G * V - 1) / (G * V);
+  const int cend = c0 + wc;
   for (int64_t vbase = warp_global * kRowsPerWarp; vbase < n; vbase += warp_stride * kRowsPerWarp) {
     const int64_t v = vbase + lane / G;
     const bool valid = v < n;
@@ -108,8 +110,8 @@ k_agg_scratch(int n, int w, const int64_t* __restrict__ ptr, const int32_t* __re
     const int deg = valid ? static_cast<int>(ptr[v + 1] - beg) : 0;
     const int maxdeg = __reduce_max_sync(0xffffffffu, deg);
     for (int k = 0; k < nchunk; ++k) {
-      const int c = (k * G + gl) * V;
-      const bool cact = valid && c < w;
+      const int c = c0 + (k * G + gl) * V;
+      const bool cact = valid && c < cend;
       float acc[V];
       int32_t arg[V];
 #pragma unroll
@@ -273,15 +275,16 @@ __global__ void k_deleted_contributor(int64_t n_del, int w, const uint64_t* __re
 // grad[u] = sum_{v in out(u), ascending} s_v * up[v]; s_v = 1 (sum), 1/deg(v) (mean).
 template <int V, int G, bool MEAN>
 __global__ void __launch_bounds__(kThreads)
-k_agg_backward(int n, int w, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
-               const float* __restrict__ up, const float* __restrict__ degree,
-               float* __restrict__ grad) {
+k_agg_backward(int n, int w, int c0, int wc, const int64_t* __restrict__ ptr,
+               const int32_t* __restrict__ idx, const float* __restrict__ up,
+               const float* __restrict__ degree, float* __restrict__ grad) {
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
   constexpr int kRowsPerWarp = 32 / G;
   const int64_t warp_global = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
   const int64_t warp_stride = (static_cast<int64_t>(gridDim.x) * kThreads) >> 5;
-  const int nchunk = (w + G * V - 1) / (G * V);
+  const int nchunk = (wc + G * V - 1) / (G * V);
+  const int cend = c0 + wc;
   for (int64_t ubase = warp_global * kRowsPerWarp; ubase < n; ubase += warp_stride * kRowsPerWarp) {
     const int64_t u = ubase + lane / G;
     const bool valid = u < n;
@@ -289,8 +292,8 @@ k_agg_backward(int n, int w, const int64_t* __restrict__ ptr, const int32_t* __r
     const int deg = valid ? static_cast<int>(ptr[u + 1] - beg) : 0;
     const int maxdeg = __reduce_max_sync(0xffffffffu, deg);
     for (int k = 0; k < nchunk; ++k) {
-      const int c = (k * G + gl) * V;
-      const bool cact = valid && c < w;
+      const int c = c0 + (k * G + gl) * V;
+      const bool cact = valid && c < cend;
       float acc[V];
 #pragma unroll
       for (int i = 0; i < V; ++i) acc[i] = 0.f;
@@ -388,6 +391,25 @@ int pick_group(int w, int vec) {
     default: { constexpr int KIND = kAggMin; __VA_ARGS__; } break;        \
   }
 
+// Column-slice width for the pull SpMMs: the gathered operand's slice
+// (n x wc fp32) is kept at or below an L2-resident budget so the ~E/N
+// re-gathers of every source row hit L2 instead of HBM; each slice re-reads
+// the index stream once. DGNN_SPMM_SLICES forces the slice count.
+int spmm_slice_width(int n, int w, int vec) {
+  static const int forced = [] {
+    const char* e = std::getenv("DGNN_SPMM_SLICES");
+    return e ? std::atoi(e) : 0;
+  }();
+  static const double budget = [] {
+    const char* e = std::getenv("DGNN_SPMM_L2_MB");
+    return (e ? std::atof(e) : 48.0) * 1048576.0;
+  }();
+  if (forced > 0 && w % forced == 0 && (w / forced) % vec == 0) return w / forced;
+  int wc = w;
+  while (static_cast<double>(n) * wc * 4.0 > budget && wc % (2 * vec) == 0 && wc / 2 >= 8) wc /= 2;
+  return wc;
+}
+
 int rows_grid(int64_t rows, int g) {
   const int64_t rows_per_block = (kThreads / 32) * (32 / g);
   return wave_grid(rows * kThreads / rows_per_block, kThreads, 8);
@@ -400,11 +422,14 @@ void agg_scratch(int kind, int n, int w, const int64_t* in_ptr, const int32_t* i
                  int32_t* argext, cudaStream_t stream) {
   if (n <= 0 || w <= 0) return;
   const int vec = pick_vec(w, feats, values);
-  const int g = pick_group(w, vec);
+  const int wc = spmm_slice_width(n, w, vec);
+  const int g = pick_group(wc, vec);
   const int grid = rows_grid(n, g);
-  DGNN_DISPATCH_KIND(kind, DGNN_DISPATCH_V(vec, DGNN_DISPATCH_G(g,
-      DGNN_LAUNCH((k_agg_scratch<V, G, KIND>), grid, kThreads, 0, stream, n, w, in_ptr, in_src,
-                  feats, values, degree, mean_sums, argext))));
+  for (int c0 = 0; c0 < w; c0 += wc) {
+    DGNN_DISPATCH_KIND(kind, DGNN_DISPATCH_V(vec, DGNN_DISPATCH_G(g,
+        DGNN_LAUNCH((k_agg_scratch<V, G, KIND>), grid, kThreads, 0, stream, n, w, c0, wc, in_ptr,
+                    in_src, feats, values, degree, mean_sums, argext))));
+  }
 }
 
 void agg_delta(int kind, int n_rows, int w, const int32_t* rows, const int32_t* row_ptr,
@@ -438,16 +463,19 @@ void agg_backward(int kind, int n, int w, const int64_t* out_ptr, const int32_t*
     return;
   }
   const int vec = pick_vec(w, up, grad);
-  const int g = pick_group(w, vec);
+  const int wc = spmm_slice_width(n, w, vec);
+  const int g = pick_group(wc, vec);
   const int grid = rows_grid(n, g);
-  if (kind == kAggMean) {
-    DGNN_DISPATCH_V(vec, DGNN_DISPATCH_G(g,
-        DGNN_LAUNCH((k_agg_backward<V, G, true>), grid, kThreads, 0, stream, n, w, out_ptr,
-                    out_dst, up, degree, grad)));
-  } else {
-    DGNN_DISPATCH_V(vec, DGNN_DISPATCH_G(g,
-        DGNN_LAUNCH((k_agg_backward<V, G, false>), grid, kThreads, 0, stream, n, w, out_ptr,
-                    out_dst, up, degree, grad)));
+  for (int c0 = 0; c0 < w; c0 += wc) {
+    if (kind == kAggMean) {
+      DGNN_DISPATCH_V(vec, DGNN_DISPATCH_G(g,
+          DGNN_LAUNCH((k_agg_backward<V, G, true>), grid, kThreads, 0, stream, n, w, c0, wc,
+                      out_ptr, out_dst, up, degree, grad)));
+    } else {
+      DGNN_DISPATCH_V(vec, DGNN_DISPATCH_G(g,
+          DGNN_LAUNCH((k_agg_backward<V, G, false>), grid, kThreads, 0, stream, n, w, c0, wc,
+                      out_ptr, out_dst, up, degree, grad)));
+    }
   }
 }
 
