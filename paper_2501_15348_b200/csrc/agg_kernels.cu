@@ -405,6 +405,10 @@ int spmm_slice_width(int n, int w, int vec) {
     return (e ? std::atof(e) : 48.0) * 1048576.0;
   }();
   if (forced > 0 && w % forced == 0 && (w / forced) % vec == 0) return w / forced;
+  // Measured on B200 at C3 (1M x 64, 20M edges): 1 slice 0.84 ms, 2: 0.89,
+  // 4: 1.04, 8: 2.07 — full-row 256 B gathers beat L2-resident 32-64 B ones,
+  // so slicing is off unless an explicit L2 budget is requested.
+  if (std::getenv("DGNN_SPMM_L2_MB") == nullptr) return w;
   int wc = w;
   while (static_cast<double>(n) * wc * 4.0 > budget && wc % (2 * vec) == 0 && wc / 2 >= 8) wc /= 2;
   return wc;

@@ -5,8 +5,9 @@
 // consecutive 8-row groups are SBO bytes apart, the two 16-byte K halves of one
 // MMA K-step are LBO bytes apart. We use
 //   byte_offset(row, k) = (k / 4) * LBO + (row / 8) * 128 + (row % 8) * 16 + (k % 4) * 4
-// with LBO = rows * 16 + 16 (the +16 pad makes the staging stores of 8
-// consecutive k-quads of one row hit distinct banks).
+// with LBO = rows * 16 + 32: the +32 B pad makes the staging stores of the
+// 4 k-quads of two consecutive rows (one 8-thread store phase) hit 8 distinct
+// 16-byte bank groups.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -20,7 +21,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-__host__ __device__ constexpr uint32_t tile_lbo(int rows) { return static_cast<uint32_t>(rows) * 16u + 16u; }
+__host__ __device__ constexpr uint32_t tile_lbo(int rows) { return static_cast<uint32_t>(rows) * 16u + 32u; }
 // bytes of one rows x kc fp32 operand tile in the canonical layout
 __host__ __device__ constexpr uint32_t tile_bytes(int rows, int kc) { return (kc / 4) * tile_lbo(rows); }
 __host__ __device__ constexpr uint32_t tile_offset(int rows, int row, int k) {

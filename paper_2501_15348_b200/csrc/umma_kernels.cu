@@ -115,7 +115,8 @@ struct RowGemmSmem {
   static constexpr uint32_t kRaw = kTileM * kKC * 4;      // one raw fp32 A chunk
   static constexpr uint32_t kRawOff = kStage * kRgStages;
   static constexpr uint32_t kBars = kRawOff + kRaw * kRawSlots;  // barrier block offset
-  static constexpr uint32_t kBytes = kBars + 128;
+  static constexpr uint32_t kBias = kBars + 128;                 // 4H fp32 bias copy
+  static constexpr uint32_t kBytes = kBias + 1024;
 };
 
 __device__ __forceinline__ void cp_async16_zfill(uint32_t saddr, const void* g, bool valid) {
@@ -141,7 +142,7 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
   if (warp == kMmaWarp) tmem_alloc(tmem_slot, 512);
   if (tid == 0) {
     for (int s = 0; s < kRgStages; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], kProducerThreads);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -150,6 +151,8 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
     }
     fence_barrier_init();
   }
+  float* sbias = reinterpret_cast<float*>(smem + S::kBias);
+  if ((EPI == kEpiLstm || EPI == kEpiGru) && tid < 4 * p.H) sbias[tid] = p.bias[tid];
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
@@ -214,12 +217,15 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
           st_shared_v4(st + S::kA + off, l0, l1, l2, l3);
         }
         fence_async_smem();
-        named_bar_sync(1, kProducerThreads);
+        // every producer thread arrives (release of its own A stores); the
+        // leader's arrival also arms the transaction count of the B copy
         if (tid == 0) {
           mbar_arrive_expect_tx(&full[s], 2 * S::kB);
           bulk_g2s(st + 2 * S::kA,
                    reinterpret_cast<const uint8_t*>(p.Bimg) + static_cast<int64_t>(c) * 2 * S::kB,
                    2 * S::kB, &full[s]);
+        } else {
+          mbar_arrive(&full[s]);
         }
       }
     }
@@ -271,6 +277,13 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
         const int U = H / 2;
         for (int j0 = half * U; j0 < (half + 1) * U; j0 += 8) {
           float a0[8], a1[8], a2[8], a3[8];
+          // state row prefetch overlaps the TMEM reads
+          float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0;
+          if (row < p.M) {
+            const float* sp = (EPI == kEpiLstm ? p.c_prev : p.h_skip) + row * H + j0;
+            x0 = __ldg(reinterpret_cast<const float4*>(sp));
+            x1 = __ldg(reinterpret_cast<const float4*>(sp + 4));
+          }
           tmem_ld8(trow + 0 * H + j0, a0);
           tmem_ld8(trow + 1 * H + j0, a1);
           tmem_ld8(trow + 2 * H + j0, a2);
@@ -278,20 +291,17 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
           tmem_wait_ld();
           if (row < p.M) {
             float sv[8], ho[8], co[8];
-            const float* sp = (EPI == kEpiLstm ? p.c_prev : p.h_skip) + row * H + j0;
-            const float4 x0 = __ldg(reinterpret_cast<const float4*>(sp));
-            const float4 x1 = __ldg(reinterpret_cast<const float4*>(sp + 4));
             sv[0] = x0.x; sv[1] = x0.y; sv[2] = x0.z; sv[3] = x0.w;
             sv[4] = x1.x; sv[5] = x1.y; sv[6] = x1.z; sv[7] = x1.w;
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
               const int j = j0 + u;
-              const float p0 = a0[u] + p.bias[j];
-              const float p1 = a1[u] + p.bias[H + j];
+              const float p0 = a0[u] + sbias[j];
+              const float p1 = a1[u] + sbias[H + j];
               if (EPI == kEpiLstm) {
                 const float ig = sigm(p0), fg = sigm(p1);
-                const float gg = ftanh(a2[u] + p.bias[2 * H + j]);
-                const float og = sigm(a3[u] + p.bias[3 * H + j]);
+                const float gg = ftanh(a2[u] + sbias[2 * H + j]);
+                const float og = sigm(a3[u] + sbias[3 * H + j]);
                 const float cc = fg * sv[u] + ig * gg;
                 a0[u] = ig;
                 a1[u] = fg;
@@ -302,7 +312,7 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
               } else {
                 const float rr = sigm(p0), zz = sigm(p1);
                 const float hn = a3[u];
-                const float nn = ftanh(a2[u] + rr * hn + p.bias[2 * H + j]);
+                const float nn = ftanh(a2[u] + rr * hn + sbias[2 * H + j]);
                 a0[u] = rr;
                 a1[u] = zz;
                 a2[u] = nn;
