@@ -96,7 +96,18 @@ struct RowGemmArgs {
   int n1, n2;
   float* C1;
   float* C2;
+  // profiling switches (env DGNN_UMMA_DEBUG): 1 skip epilogue math/stores,
+  // 2 skip the B copy, 4 skip the A split/stores
+  int debug;
 };
+
+int umma_debug_flags() {
+  static const int f = [] {
+    const char* e = std::getenv("DGNN_UMMA_DEBUG");
+    return e ? std::atoi(e) : 0;
+  }();
+  return f;
+}
 
 constexpr int kRgThreads = 512;  // 16 warps
 constexpr int kRgStages = 3;     // MMA operand stages (A hi/lo + B hi/lo)
@@ -201,6 +212,7 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
       {
 #pragma unroll
         for (int it = 0; it < kRawPerThread; ++it) {
+          if (p.debug & 4) break;
           const int f = tid + it * kProducerThreads;
           const int row = f / (kKC / 4), kq = f % (kKC / 4);
           float4 v;
@@ -219,7 +231,7 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
         fence_async_smem();
         // every producer thread arrives (release of its own A stores); the
         // leader's arrival also arms the transaction count of the B copy
-        if (tid == 0) {
+        if (tid == 0 && !(p.debug & 2)) {
           mbar_arrive_expect_tx(&full[s], 2 * S::kB);
           bulk_g2s(st + 2 * S::kA,
                    reinterpret_cast<const uint8_t*>(p.Bimg) + static_cast<int64_t>(c) * 2 * S::kB,
@@ -289,7 +301,7 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
           tmem_ld8(trow + 2 * H + j0, a2);
           tmem_ld8(trow + 3 * H + j0, a3);
           tmem_wait_ld();
-          if (row < p.M) {
+          if (row < p.M && !(p.debug & 1)) {
             float sv[8], ho[8], co[8];
             sv[0] = x0.x; sv[1] = x0.y; sv[2] = x0.z; sv[3] = x0.w;
             sv[4] = x1.x; sv[5] = x1.y; sv[6] = x1.z; sv[7] = x1.w;
@@ -614,6 +626,7 @@ void umma_cell_forward(bool lstm, int n, int in, int H, const float* X, const fl
   a.gates = gates;
   a.c_out = c;
   a.h_out = h;
+  a.debug = umma_debug_flags();
   const int npad = umma_npad(4 * H);
   if (lstm) dispatch_row_gemm<kEpiLstm>(npad, a, stream);
   else dispatch_row_gemm<kEpiGru>(npad, a, stream);
@@ -634,6 +647,7 @@ void umma_gemm_store2(int n, int K, const float* A, const float* Bimg, int n1, i
   a.n2 = n2;
   a.C1 = C1;
   a.C2 = C2;
+  a.debug = umma_debug_flags();
   dispatch_row_gemm<kEpiStore2>(umma_npad(n1 + n2), a, stream);
 }
 
