@@ -23,6 +23,59 @@ struct dgnn_graph {
 
 struct dgnn_synth {
   CompactGraph cg;
+  // Pinned-host mirror of the compact graph (built on first upload): the
+  // per-epoch host->HBM upload then runs at DMA speed.
+  struct Pinned {
+    void* arena = nullptr;
+    const int32_t *base_src = nullptr, *base_dst = nullptr;
+    const float* base_feats = nullptr;
+    struct Step {
+      const int32_t *del_src, *del_dst, *ins_src, *ins_dst, *changed;
+      const float* changed_feats;
+    };
+    std::vector<Step> steps;
+  } pin;
+  ~dgnn_synth() {
+    if (pin.arena) cudaFreeHost(pin.arena);
+  }
+  void ensure_pinned() {
+    if (pin.arena) return;
+    size_t bytes = 0;
+    auto add = [&](size_t b) { bytes += (b + 255) / 256 * 256; };
+    add(cg.base_src.size() * 4);
+    add(cg.base_dst.size() * 4);
+    add(cg.base_feats.size() * 4);
+    for (const auto& s : cg.steps) {
+      add(s.del_src.size() * 4);
+      add(s.del_dst.size() * 4);
+      add(s.ins_src.size() * 4);
+      add(s.ins_dst.size() * 4);
+      add(s.changed.size() * 4);
+      add(s.changed_feats.size() * 4);
+    }
+    DGNN_CUDA(cudaMallocHost(&pin.arena, bytes + 256));
+    char* cur = static_cast<char*>(pin.arena);
+    auto put = [&](const auto& v) {
+      using T = typename std::decay_t<decltype(v)>::value_type;
+      T* dst = reinterpret_cast<T*>(cur);
+      if (!v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(T));
+      cur += (v.size() * sizeof(T) + 255) / 256 * 256;
+      return const_cast<const T*>(dst);
+    };
+    pin.base_src = put(cg.base_src);
+    pin.base_dst = put(cg.base_dst);
+    pin.base_feats = put(cg.base_feats);
+    for (const auto& s : cg.steps) {
+      Pinned::Step p;
+      p.del_src = put(s.del_src);
+      p.del_dst = put(s.del_dst);
+      p.ins_src = put(s.ins_src);
+      p.ins_dst = put(s.ins_dst);
+      p.changed = put(s.changed);
+      p.changed_feats = put(s.changed_feats);
+      pin.steps.push_back(p);
+    }
+  }
 };
 
 struct dgnn_session {
@@ -253,14 +306,18 @@ int dgnn_synth_to_graph(const dgnn_synth* s, void* stream, dgnn_graph** out) {
     if (dgnn_graph_create(s->cg.num_nodes, s->cg.feature_dim, stream, &g) != 0)
       throw std::runtime_error(g_err);
     std::unique_ptr<dgnn_graph, void (*)(dgnn_graph*)> guard(g, dgnn_graph_free);
+    auto* ss = const_cast<dgnn_synth*>(s);
+    ss->ensure_pinned();
     const CompactGraph& cg = s->cg;
-    g->g->add_snapshot(cg.base_src.data(), cg.base_dst.data(),
-                       static_cast<int64_t>(cg.base_src.size()), cg.base_feats.data());
-    for (const CompactStep& st : cg.steps) {
-      g->g->add_delta(st.del_src.data(), st.del_dst.data(), static_cast<int64_t>(st.del_src.size()),
-                      st.ins_src.data(), st.ins_dst.data(), static_cast<int64_t>(st.ins_src.size()),
-                      st.changed.data(), static_cast<int64_t>(st.changed.size()),
-                      st.changed_feats.data());
+    const auto& pin = ss->pin;
+    g->g->add_snapshot(pin.base_src, pin.base_dst, static_cast<int64_t>(cg.base_src.size()),
+                       pin.base_feats);
+    for (size_t i = 0; i < cg.steps.size(); ++i) {
+      const CompactStep& st = cg.steps[i];
+      const auto& ps = pin.steps[i];
+      g->g->add_delta(ps.del_src, ps.del_dst, static_cast<int64_t>(st.del_src.size()), ps.ins_src,
+                      ps.ins_dst, static_cast<int64_t>(st.ins_src.size()), ps.changed,
+                      static_cast<int64_t>(st.changed.size()), ps.changed_feats);
     }
     DGNN_CUDA(cudaStreamSynchronize(g->stream));
     *out = guard.release();

@@ -14,7 +14,8 @@
 //              (canonical K-major UMMA layout); the leader also issues the
 //              bulk (TMA-engine) copy of the pre-split B chunk;
 //   warp 4     TMEM allocator + the single thread issuing tcgen05.mma;
-//   warps 8-15 epilogue: tcgen05.ld from TMEM, fused math, vector stores.
+//   warps 5-12 epilogue: tcgen05.ld from TMEM, fused math, stores coalesced
+//              through a per-warp smem transpose (8 rows x 64 B per store).
 // Smem stages (4 x K=16) are handed over with full/empty mbarriers
 // (expect_tx for the bulk copy, tcgen05.commit for release); the fp32
 // accumulator is double-buffered in TMEM (2 x 256 columns) so the epilogue of
@@ -109,12 +110,12 @@ int umma_debug_flags() {
   return f;
 }
 
-constexpr int kRgThreads = 512;  // 16 warps
+constexpr int kRgThreads = 416;  // 13 warps: 4 producers, 1 MMA, 8 epilogue
 constexpr int kRgStages = 3;     // MMA operand stages (A hi/lo + B hi/lo)
 constexpr int kRawSlots = 6;     // cp.async prefetch depth of raw fp32 A chunks
 constexpr int kProducerThreads = 128;
 constexpr int kMmaWarp = 4;
-constexpr int kEpiWarp0 = 8;
+constexpr int kEpiWarp0 = 5;  // warps 5..12: lane quadrant = warp % 4 covers 0..3 twice
 constexpr int kEpiWarps = 8;
 constexpr int kRawPerThread = (kTileM * kKC / 4) / kProducerThreads;  // float4 per thread per chunk
 
@@ -127,7 +128,8 @@ struct RowGemmSmem {
   static constexpr uint32_t kRawOff = kStage * kRgStages;
   static constexpr uint32_t kBars = kRawOff + kRaw * kRawSlots;  // barrier block offset
   static constexpr uint32_t kBias = kBars + 128;                 // 4H fp32 bias copy
-  static constexpr uint32_t kBytes = kBias + 1024;
+  static constexpr uint32_t kOut = kBias + 1024;                 // per-epilogue-warp store staging
+  static constexpr uint32_t kBytes = kOut + kEpiWarps * 32 * 20 * 4;
 };
 
 __device__ __forceinline__ void cp_async16_zfill(uint32_t saddr, const void* g, bool valid) {
@@ -282,31 +284,55 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
       const uint32_t b = it & 1u;
       mbar_wait(&tfull[b], (it >> 1) & 1u);
       fence_after_sync();
-      const int64_t row = static_cast<int64_t>(tile) * kTileM + q * 32 + lane;
+      const int64_t row0 = static_cast<int64_t>(tile) * kTileM + q * 32;  // this warp's 32 rows
+      const int64_t row = row0 + lane;
       const uint32_t trow = tmem + b * 256 + (static_cast<uint32_t>(q * 32) << 16);
+      // Coalesced store of a 32-row x 16-column register block (lane = row):
+      // transposed through a per-warp smem buffer so each st.global.v4 covers
+      // 8 rows x 64 contiguous bytes instead of 32 rows x 16 bytes.
+      float* wb = reinterpret_cast<float*>(smem + S::kOut) + (warp - kEpiWarp0) * (32 * 20);
+      auto stage_store = [&](const float (&v)[16], float* base, int64_t stride, int col0) {
+#pragma unroll
+        for (int u = 0; u < 16; u += 4)
+          *reinterpret_cast<float4*>(wb + lane * 20 + u) = make_float4(v[u], v[u + 1], v[u + 2], v[u + 3]);
+        __syncwarp();
+        const int i = lane >> 2, k = lane & 3;
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) {
+          const int rl = bb * 8 + i;
+          const float4 x = *reinterpret_cast<const float4*>(wb + rl * 20 + k * 4);
+          if (row0 + rl < p.M)
+            *reinterpret_cast<float4*>(base + (row0 + rl) * stride + col0 + k * 4) = x;
+        }
+        __syncwarp();
+      };
       if (EPI == kEpiLstm || EPI == kEpiGru) {
         const int H = p.H;
         const int U = H / 2;
-        for (int j0 = half * U; j0 < (half + 1) * U; j0 += 8) {
-          float a0[8], a1[8], a2[8], a3[8];
+        for (int j0 = half * U; j0 < (half + 1) * U; j0 += 16) {
+          float a0[16], a1[16], a2[16], a3[16];
           // state row prefetch overlaps the TMEM reads
-          float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0;
+          float sv[16];
           if (row < p.M) {
             const float* sp = (EPI == kEpiLstm ? p.c_prev : p.h_skip) + row * H + j0;
-            x0 = __ldg(reinterpret_cast<const float4*>(sp));
-            x1 = __ldg(reinterpret_cast<const float4*>(sp + 4));
-          }
-          tmem_ld8(trow + 0 * H + j0, a0);
-          tmem_ld8(trow + 1 * H + j0, a1);
-          tmem_ld8(trow + 2 * H + j0, a2);
-          tmem_ld8(trow + 3 * H + j0, a3);
-          tmem_wait_ld();
-          if (row < p.M && !(p.debug & 1)) {
-            float sv[8], ho[8], co[8];
-            sv[0] = x0.x; sv[1] = x0.y; sv[2] = x0.z; sv[3] = x0.w;
-            sv[4] = x1.x; sv[5] = x1.y; sv[6] = x1.z; sv[7] = x1.w;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < 16; u += 4) {
+              const float4 x = __ldg(reinterpret_cast<const float4*>(sp + u));
+              sv[u] = x.x; sv[u + 1] = x.y; sv[u + 2] = x.z; sv[u + 3] = x.w;
+            }
+          } else {
+#pragma unroll
+            for (int u = 0; u < 16; ++u) sv[u] = 0.f;
+          }
+          tmem_ld16(trow + 0 * H + j0, a0);
+          tmem_ld16(trow + 1 * H + j0, a1);
+          tmem_ld16(trow + 2 * H + j0, a2);
+          tmem_ld16(trow + 3 * H + j0, a3);
+          tmem_wait_ld();
+          if (!(p.debug & 1)) {
+            float ho[16], co[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
               const int j = j0 + u;
               const float p0 = a0[u] + sbias[j];
               const float p1 = a1[u] + sbias[H + j];
@@ -331,18 +357,22 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
                 ho[u] = (1.f - zz) * nn + zz * sv[u];
               }
             }
-            float* gr = p.gates + row * 4 * H + j0;
-#pragma unroll
-            for (int u = 0; u < 8; u += 4) {
-              *reinterpret_cast<float4*>(gr + 0 * H + u) = make_float4(a0[u], a0[u + 1], a0[u + 2], a0[u + 3]);
-              *reinterpret_cast<float4*>(gr + 1 * H + u) = make_float4(a1[u], a1[u + 1], a1[u + 2], a1[u + 3]);
-              *reinterpret_cast<float4*>(gr + 2 * H + u) = make_float4(a2[u], a2[u + 1], a2[u + 2], a2[u + 3]);
-              *reinterpret_cast<float4*>(gr + 3 * H + u) = make_float4(a3[u], a3[u + 1], a3[u + 2], a3[u + 3]);
-              if (EPI == kEpiLstm)
-                *reinterpret_cast<float4*>(p.c_out + row * H + j0 + u) = make_float4(co[u], co[u + 1], co[u + 2], co[u + 3]);
-              *reinterpret_cast<float4*>(p.h_out + row * H + j0 + u) = make_float4(ho[u], ho[u + 1], ho[u + 2], ho[u + 3]);
-            }
+            stage_store(a0, p.gates, 4 * H, 0 * H + j0);
+            stage_store(a1, p.gates, 4 * H, 1 * H + j0);
+            stage_store(a2, p.gates, 4 * H, 2 * H + j0);
+            stage_store(a3, p.gates, 4 * H, 3 * H + j0);
+            if (EPI == kEpiLstm) stage_store(co, p.c_out, H, j0);
+            stage_store(ho, p.h_out, H, j0);
           }
+        }
+      } else if (p.n1 % 16 == 0 && p.n2 % 16 == 0) {
+        const int ncol = p.n1 + p.n2;
+        for (int cb = half * 16; cb < ncol; cb += 32) {
+          float a[16];
+          tmem_ld16(trow + cb, a);
+          tmem_wait_ld();
+          if (cb < p.n1) stage_store(a, p.C1, p.n1, cb);
+          else stage_store(a, p.C2, p.n2, cb - p.n1);
         }
       } else {
         const int ncol = p.n1 + p.n2;
