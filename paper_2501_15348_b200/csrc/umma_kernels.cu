@@ -413,8 +413,13 @@ struct WgradSmem {
   static constexpr uint32_t kA = tile_bytes(MG, kKW);
   static constexpr uint32_t kB = tile_bytes(NPAD, kKW);
   static constexpr uint32_t kStage = 2 * kA + 2 * kB;
-  static constexpr int kStages = 3;
-  static constexpr uint32_t kBytes = kStages * kStage + 64;
+  static constexpr int kStages = 2;
+  // raw fp32 chunk: G rows (MG) + X rows (<= 128) + Hm rows (<= 64), cp.async ring
+  static constexpr int kRawSlots = 3;
+  static constexpr uint32_t kRaw = kKW * 4 * (MG + 192);
+  static constexpr uint32_t kRawOff = kStages * kStage;
+  static constexpr uint32_t kBars = kRawOff + kRawSlots * kRaw;
+  static constexpr uint32_t kBytes = kBars + 64;
 };
 
 template <int MG, int NPAD>
@@ -423,8 +428,8 @@ k_wgrad(int M, int in, int H, const float* __restrict__ G, const float* __restri
         const float* __restrict__ Hm, float* __restrict__ ws) {
   using S = WgradSmem<MG, NPAD>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kStages * S::kStage);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + S::kStages * S::kStage + 32);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kBars);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + S::kBars + 32);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int kHalves = MG / 128;
   constexpr uint32_t kCols = kHalves == 2 ? 512 : 256;
@@ -445,20 +450,53 @@ k_wgrad(int M, int in, int H, const float* __restrict__ G, const float* __restri
   const int64_t rb = blockIdx.x * per;
   const int64_t re = rb + per < M ? rb + per : M;
   const int nchunks = re > rb ? static_cast<int>((re - rb + kKW - 1) / kKW) : 0;
+  // raw slot layout: G [kKW][MG] | X [kKW][in] | Hm [kKW][H]
+  const uint32_t raw0 = sbase + S::kRawOff;
+  const int g4 = MG / 4, x4 = in / 4, h4 = H / 4, row4 = g4 + x4 + h4;
+  auto issue = [&](int c) {
+    if (c < nchunks) {
+      const uint32_t slot = raw0 + (c % S::kRawSlots) * S::kRaw;
+      const int64_t q0 = rb + static_cast<int64_t>(c) * kKW;
+      for (int f = tid; f < kKW * row4; f += kThreads) {
+        const int r = f / row4, col4 = f % row4;
+        const int64_t row = q0 + r;
+        const bool valid = row < re;
+        const float* src;
+        uint32_t dst;
+        if (col4 < g4) {
+          src = G + row * MG + col4 * 4;
+          dst = slot + (r * MG + col4 * 4) * 4;
+        } else if (col4 < g4 + x4) {
+          src = X + row * in + (col4 - g4) * 4;
+          dst = slot + (kKW * MG + r * in + (col4 - g4) * 4) * 4;
+        } else {
+          src = Hm + row * H + (col4 - g4 - x4) * 4;
+          dst = slot + (kKW * (MG + in) + r * H + (col4 - g4 - x4) * 4) * 4;
+        }
+        cp_async16_zfill(dst, valid ? src : G, valid);
+      }
+    }
+    cp_async_commit();
+  };
+  for (int i = 0; i < S::kRawSlots - 1; ++i) issue(i);
   for (int c = 0; c < nchunks; ++c) {
+    issue(c + S::kRawSlots - 1);
+    cp_async_wait<S::kRawSlots - 1>();
+    __syncthreads();  // raw chunk c visible to every converting thread
     const uint32_t s = c % S::kStages;
     if (c >= S::kStages) mbar_wait(&bars[s], ((c - S::kStages) / S::kStages) & 1u);
     const uint32_t st = sbase + s * S::kStage;
-    const int64_t q0 = rb + static_cast<int64_t>(c) * kKW;
+    const float* rawG = reinterpret_cast<const float*>(smem + S::kRawOff + (c % S::kRawSlots) * S::kRaw);
+    const float* rawX = rawG + kKW * MG;
+    const float* rawH = rawX + kKW * in;
+    const int64_t q0c = rb + static_cast<int64_t>(c) * kKW;
     // A' = G^T: 4x4 blocks (4 gate columns x 4 rows), transposed in registers
     for (int blk = tid; blk < (MG / 4) * (kKW / 4); blk += kThreads) {
       const int m4 = blk % (MG / 4), k4 = blk / (MG / 4);
       float v[4][4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        const int64_t row = q0 + k4 * 4 + r;
-        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (row < re) x = __ldg(reinterpret_cast<const float4*>(G + row * MG + m4 * 4));
+        const float4 x = *reinterpret_cast<const float4*>(rawG + (k4 * 4 + r) * MG + m4 * 4);
         v[r][0] = x.x; v[r][1] = x.y; v[r][2] = x.z; v[r][3] = x.w;
       }
 #pragma unroll
@@ -477,24 +515,16 @@ k_wgrad(int M, int in, int H, const float* __restrict__ G, const float* __restri
       float v[4][4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        const int64_t row = q0 + k4 * 4 + r;
-        const bool live = row < re;
+        const int rr = k4 * 4 + r;
+        const bool live = q0c + rr < re;
         const int n = n4 * 4;
         float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (live) {
-          if (n + 3 < in) {
-            x = __ldg(reinterpret_cast<const float4*>(X + row * in + n));
-          } else if (n >= in && n + 3 < KXH) {
-            x = __ldg(reinterpret_cast<const float4*>(Hm + row * H + (n - in)));
-          } else {
-            float t[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int nn = n + i;
-              t[i] = nn < in ? X[row * in + nn] : (nn < KXH ? Hm[row * H + (nn - in)] : (nn == KXH ? 1.f : 0.f));
-            }
-            x = make_float4(t[0], t[1], t[2], t[3]);
-          }
+        if (n < in) {
+          x = *reinterpret_cast<const float4*>(rawX + rr * in + n);
+        } else if (n < KXH) {
+          x = *reinterpret_cast<const float4*>(rawH + rr * H + (n - in));
+        } else if (n == KXH && live) {
+          x.x = 1.f;  // ones column -> bias gradient (in+H is a multiple of 4)
         }
         v[r][0] = x.x; v[r][1] = x.y; v[r][2] = x.z; v[r][3] = x.w;
       }
@@ -531,6 +561,7 @@ k_wgrad(int M, int in, int H, const float* __restrict__ G, const float* __restri
       commit(&bars[s]);
     }
   }
+  cp_async_wait<0>();
   float* out = ws + static_cast<int64_t>(blockIdx.x) * MG * NPAD;
   if (nchunks > 0) {
     mbar_wait(&bars[(nchunks - 1) % S::kStages], ((nchunks - 1) / S::kStages) & 1u);
@@ -617,7 +648,8 @@ bool umma_enabled() {
 }
 
 bool umma_cell_supported(int in, int H) {
-  return umma_enabled() && (H == 32 || H == 64) && in % 4 == 0 && in >= 4 && in + H + 1 <= 256;
+  // in + H <= 192: the weight-gradient kernel's raw [X | Hm] staging slot
+  return umma_enabled() && (H == 32 || H == 64) && in % 4 == 0 && in >= 4 && in + H <= 192;
 }
 
 int umma_npad(int N) { return N <= 64 ? 64 : (N <= 128 ? 128 : (N <= 192 ? 192 : 256)); }
