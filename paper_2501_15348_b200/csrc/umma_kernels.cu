@@ -129,7 +129,7 @@ struct RowGemmSmem {
   static constexpr uint32_t kBars = kRawOff + kRaw * kRawSlots;  // barrier block offset
   static constexpr uint32_t kBias = kBars + 128;                 // 4H fp32 bias copy
   static constexpr uint32_t kOut = kBias + 1024;                 // per-epilogue-warp store staging
-  static constexpr uint32_t kBytes = kOut + kEpiWarps * 32 * 20 * 4;
+  static constexpr uint32_t kBytes = kOut + kEpiWarps * 32 * 16 * 4;
 };
 
 __device__ __forceinline__ void cp_async16_zfill(uint32_t saddr, const void* g, bool valid) {
@@ -290,17 +290,21 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
       // Coalesced store of a 32-row x 16-column register block (lane = row):
       // transposed through a per-warp smem buffer so each st.global.v4 covers
       // 8 rows x 64 contiguous bytes instead of 32 rows x 16 bytes.
-      float* wb = reinterpret_cast<float*>(smem + S::kOut) + (warp - kEpiWarp0) * (32 * 20);
+      // 32 rows x 4 chunks of 16 B, chunk index XOR-swizzled by (row >> 1) & 3
+      // so both the row-per-lane writes and the 8-rows-x-64B reads are
+      // bank-conflict free.
+      float* wb = reinterpret_cast<float*>(smem + S::kOut) + (warp - kEpiWarp0) * (32 * 16);
       auto stage_store = [&](const float (&v)[16], float* base, int64_t stride, int col0) {
 #pragma unroll
         for (int u = 0; u < 16; u += 4)
-          *reinterpret_cast<float4*>(wb + lane * 20 + u) = make_float4(v[u], v[u + 1], v[u + 2], v[u + 3]);
+          *reinterpret_cast<float4*>(wb + lane * 16 + (((u >> 2) ^ ((lane >> 1) & 3)) << 2)) =
+              make_float4(v[u], v[u + 1], v[u + 2], v[u + 3]);
         __syncwarp();
         const int i = lane >> 2, k = lane & 3;
 #pragma unroll
         for (int bb = 0; bb < 4; ++bb) {
           const int rl = bb * 8 + i;
-          const float4 x = *reinterpret_cast<const float4*>(wb + rl * 20 + k * 4);
+          const float4 x = *reinterpret_cast<const float4*>(wb + rl * 16 + ((k ^ ((rl >> 1) & 3)) << 2));
           if (row0 + rl < p.M)
             *reinterpret_cast<float4*>(base + (row0 + rl) * stride + col0 + k * 4) = x;
         }
@@ -490,53 +494,34 @@ k_wgrad(int M, int in, int H, const float* __restrict__ G, const float* __restri
     const float* rawX = rawG + kKW * MG;
     const float* rawH = rawX + kKW * in;
     const int64_t q0c = rb + static_cast<int64_t>(c) * kKW;
-    // A' = G^T: 4x4 blocks (4 gate columns x 4 rows), transposed in registers
-    for (int blk = tid; blk < (MG / 4) * (kKW / 4); blk += kThreads) {
-      const int m4 = blk % (MG / 4), k4 = blk / (MG / 4);
-      float v[4][4];
+    // A' = G^T: one (column m, 4-row quad) per task; lanes take consecutive
+    // columns so the 8 lanes of a store phase fill 8 distinct 16 B bank groups
+    // of a core matrix (conflict-free), and the column reads are consecutive.
+    for (int task = tid; task < MG * (kKW / 4); task += kThreads) {
+      const int m = task % MG, k4 = task / MG;
+      float h[4], l[4];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const float4 x = *reinterpret_cast<const float4*>(rawG + (k4 * 4 + r) * MG + m4 * 4);
-        v[r][0] = x.x; v[r][1] = x.y; v[r][2] = x.z; v[r][3] = x.w;
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        float h[4], l[4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) split_tf32(v[r][i], h[r], l[r]);
-        const uint32_t off = tile_offset(MG, m4 * 4 + i, k4 * 4);
-        st_shared_v4(st + off, h[0], h[1], h[2], h[3]);
-        st_shared_v4(st + S::kA + off, l[0], l[1], l[2], l[3]);
-      }
+      for (int r = 0; r < 4; ++r) split_tf32(rawG[(k4 * 4 + r) * MG + m], h[r], l[r]);
+      const uint32_t off = tile_offset(MG, m, k4 * 4);
+      st_shared_v4(st + off, h[0], h[1], h[2], h[3]);
+      st_shared_v4(st + S::kA + off, l[0], l[1], l[2], l[3]);
     }
-    // B' = [X | Hm | 1]^T
-    for (int blk = tid; blk < (NPAD / 4) * (kKW / 4); blk += kThreads) {
-      const int n4 = blk % (NPAD / 4), k4 = blk / (NPAD / 4);
-      float v[4][4];
+    // B' = [X | Hm | 1]^T (ones column at n = in + H -> bias gradient)
+    for (int task = tid; task < NPAD * (kKW / 4); task += kThreads) {
+      const int n = task % NPAD, k4 = task / NPAD;
+      float h[4], l[4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const int rr = k4 * 4 + r;
-        const bool live = q0c + rr < re;
-        const int n = n4 * 4;
-        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (n < in) {
-          x = *reinterpret_cast<const float4*>(rawX + rr * in + n);
-        } else if (n < KXH) {
-          x = *reinterpret_cast<const float4*>(rawH + rr * H + (n - in));
-        } else if (n == KXH && live) {
-          x.x = 1.f;  // ones column -> bias gradient (in+H is a multiple of 4)
-        }
-        v[r][0] = x.x; v[r][1] = x.y; v[r][2] = x.z; v[r][3] = x.w;
+        float x = 0.f;
+        if (n < in) x = rawX[rr * in + n];
+        else if (n < KXH) x = rawH[rr * H + (n - in)];
+        else if (n == KXH && q0c + rr < re) x = 1.f;
+        split_tf32(x, h[r], l[r]);
       }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        float h[4], l[4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) split_tf32(v[r][i], h[r], l[r]);
-        const uint32_t off = tile_offset(NPAD, n4 * 4 + i, k4 * 4);
-        st_shared_v4(st + 2 * S::kA + off, h[0], h[1], h[2], h[3]);
-        st_shared_v4(st + 2 * S::kA + S::kB + off, l[0], l[1], l[2], l[3]);
-      }
+      const uint32_t off = tile_offset(NPAD, n, k4 * 4);
+      st_shared_v4(st + 2 * S::kA + off, h[0], h[1], h[2], h[3]);
+      st_shared_v4(st + 2 * S::kA + S::kB + off, l[0], l[1], l[2], l[3]);
     }
     fence_async_smem();
     __syncthreads();
