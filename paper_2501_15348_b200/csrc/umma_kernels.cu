@@ -456,37 +456,31 @@ k_wgrad(int M, int in, int H, const float* __restrict__ G, const float* __restri
   const int nchunks = re > rb ? static_cast<int>((re - rb + kKW - 1) / kKW) : 0;
   // raw slot layout: G [kKW][MG] | X [kKW][in] | Hm [kKW][H]
   const uint32_t raw0 = sbase + S::kRawOff;
-  const int g4 = MG / 4, x4 = in / 4, h4 = H / 4, row4 = g4 + x4 + h4;
+  // The 16 rows of each operand are one contiguous block in global memory, so
+  // each region is a linear copy; rows past `re` are zero-filled.
+  auto copy_region = [&](uint32_t dst, const float* src, int width, int live_rows) {
+    const int n4 = kKW * width / 4, valid4 = live_rows * width / 4;
+    for (int f = tid; f < n4; f += kThreads) {
+      const bool valid = f < valid4;
+      cp_async16_zfill(dst + f * 16, valid ? src + f * 4 : src, valid);
+    }
+  };
   auto issue = [&](int c) {
     if (c < nchunks) {
       const uint32_t slot = raw0 + (c % S::kRawSlots) * S::kRaw;
       const int64_t q0 = rb + static_cast<int64_t>(c) * kKW;
-      for (int f = tid; f < kKW * row4; f += kThreads) {
-        const int r = f / row4, col4 = f % row4;
-        const int64_t row = q0 + r;
-        const bool valid = row < re;
-        const float* src;
-        uint32_t dst;
-        if (col4 < g4) {
-          src = G + row * MG + col4 * 4;
-          dst = slot + (r * MG + col4 * 4) * 4;
-        } else if (col4 < g4 + x4) {
-          src = X + row * in + (col4 - g4) * 4;
-          dst = slot + (kKW * MG + r * in + (col4 - g4) * 4) * 4;
-        } else {
-          src = Hm + row * H + (col4 - g4 - x4) * 4;
-          dst = slot + (kKW * (MG + in) + r * H + (col4 - g4 - x4) * 4) * 4;
-        }
-        cp_async16_zfill(dst, valid ? src : G, valid);
-      }
+      const int live = static_cast<int>(re - q0 < kKW ? re - q0 : kKW);
+      copy_region(slot, G + q0 * MG, MG, live);
+      copy_region(slot + kKW * MG * 4, X + q0 * in, in, live);
+      copy_region(slot + kKW * (MG + in) * 4, Hm + q0 * H, H, live);
     }
     cp_async_commit();
   };
   for (int i = 0; i < S::kRawSlots - 1; ++i) issue(i);
+  cp_async_wait<S::kRawSlots - 2>();
+  __syncthreads();  // raw chunk 0 visible to every converting thread
   for (int c = 0; c < nchunks; ++c) {
     issue(c + S::kRawSlots - 1);
-    cp_async_wait<S::kRawSlots - 1>();
-    __syncthreads();  // raw chunk c visible to every converting thread
     const uint32_t s = c % S::kStages;
     if (c >= S::kStages) mbar_wait(&bars[s], ((c - S::kStages) / S::kStages) & 1u);
     const uint32_t st = sbase + s * S::kStage;
@@ -524,7 +518,8 @@ k_wgrad(int M, int in, int H, const float* __restrict__ G, const float* __restri
       st_shared_v4(st + 2 * S::kA + S::kB + off, l[0], l[1], l[2], l[3]);
     }
     fence_async_smem();
-    __syncthreads();
+    cp_async_wait<S::kRawSlots - 2>();  // own copies of raw chunk c+1 landed
+    __syncthreads();  // stage s complete for the MMA; raw chunk c+1 visible
     if (tid == 0) {
       fence_after_sync();
 #pragma unroll
