@@ -366,12 +366,15 @@ Buf linear_forward(DgnnModel& m, const LinearSlot& lin, NodeId n, const float* x
 void run_stack_step(DgnnModel& model, std::vector<CellSlot>& cells, const SeqSample& sample,
                     AggProvider& provider, ModelPart part, Timestep pos, Timestep t,
                     const GraphView& view, const float* x, bool x_is_data, std::vector<Buf>* h,
-                    std::vector<Buf>* c, std::vector<GraphStepTape>* tapes) {
+                    std::vector<Buf>* c, std::vector<GraphStepTape>* tapes, Lanes& lanes) {
   const int D = model.cfg_.layers;
   const int K = model.gates();
   const NodeId n = view.num_nodes;
-  cudaStream_t st = provider.stream();
   for (int l = 1; l <= D; ++l) {
+    cudaStream_t st = lanes.of(l);
+    // layer l consumes layer l-1's output of this step (other lane)
+    if (l > 1) lanes.dep(lanes.of(l - 1), st);
+    provider.set_stream(st);
     provider.begin_cell_step();
     const CellSlot& cell = cells[l - 1];
     const float* x_src = l == 1 ? x : (*h)[l - 2]->get();
@@ -396,16 +399,18 @@ void run_stack_step(DgnnModel& model, std::vector<CellSlot>& cells, const SeqSam
     if (cell.lstm) (*c)[l - 1] = tape.core.c;
     tapes->push_back(std::move(tape));
   }
+  provider.set_stream(lanes.main());
 }
 
-ForwardArtifacts seq2seq_forward(DgnnModel& model, const SeqSample& sample, AggProvider& provider) {
+ForwardArtifacts seq2seq_forward(DgnnModel& model, const SeqSample& sample, AggProvider& provider,
+                                 Lanes& lanes) {
   const ModelConfig& cfg = model.cfg_;
   check(!is_stacked(cfg.arch), "seq2seq_forward needs an integrated model");
   const Timestep L = sample.window.length, H = sample.window.horizon;
   check(static_cast<Timestep>(sample.views.size()) == L + H, "sample views must cover L+H steps");
   check(static_cast<Timestep>(sample.feats.size()) == L + H + 1,
         "sample features must cover L+H+1 snapshots");
-  cudaStream_t st = provider.stream();
+  cudaStream_t st = lanes.main();
   const NodeId n = sample.views[0].num_nodes;
   const int D = cfg.layers;
   const bool lstm = cell_kind_of(cfg.arch) == CellKind::kLstm;
@@ -415,25 +420,28 @@ ForwardArtifacts seq2seq_forward(DgnnModel& model, const SeqSample& sample, AggP
     c.resize(D);
     for (int l = 0; l < D; ++l) c[l] = zero_buf(static_cast<size_t>(n) * cfg.hidden_dim, st);
   }
+  lanes.dep(st, lanes.s[1]);  // initial states (and the caller's zeroed grads) visible to lane 1
   ForwardArtifacts out;
   out.enc_steps.resize(L);
   for (Timestep idx = 0; idx < L; ++idx) {
     run_stack_step(model, model.enc_, sample, provider, ModelPart::kEncoder, idx,
                    sample.window.snapshot_at(idx), sample.views[idx], sample.feats[idx], true, &h,
-                   &c, &out.enc_steps[idx]);
+                   &c, &out.enc_steps[idx], lanes);
   }
-  if (!cfg.teacher_forcing) out.enc_final_pred = linear_forward(model, model.head_, n, h[D - 1]->get(), false, st);
+  cudaStream_t top = lanes.of(D);  // head / feedback on the top layer's lane
+  if (!cfg.teacher_forcing) out.enc_final_pred = linear_forward(model, model.head_, n, h[D - 1]->get(), false, top);
   out.dec_steps.resize(H);
   Buf feedback = out.enc_final_pred;
   for (Timestep j = 0; j < H; ++j) {
     const Timestep t = sample.window.start + L + j;
     const bool forced = cfg.teacher_forcing;
+    if (!forced) lanes.dep(top, lanes.of(1));  // fed-back prediction -> layer 1
     const float* x = forced ? sample.feats[L + j] : feedback->get();
     out.dec_inputs.push_back(x);
     if (!forced) out.feedback_keep.push_back(feedback);
     run_stack_step(model, model.dec_, sample, provider, ModelPart::kDecoder, j, t,
-                   sample.views[L + j], x, forced, &h, &c, &out.dec_steps[j]);
-    Buf pred = linear_forward(model, model.head_, n, h[D - 1]->get(), false, st);
+                   sample.views[L + j], x, forced, &h, &c, &out.dec_steps[j], lanes);
+    Buf pred = linear_forward(model, model.head_, n, h[D - 1]->get(), false, top);
     feedback = pred;
     out.predictions.push_back(pred);
   }
@@ -609,37 +617,47 @@ void head_backward(DgnnModel& model, NodeId n, const float* h_top, const Buf& dp
 }
 
 void integrated_backward(DgnnModel& model, const SeqSample& sample, const ForwardArtifacts& fwd,
-                         const std::vector<Buf>& dpred, Grads& g, cudaStream_t st) {
+                         const std::vector<Buf>& dpred, Grads* g, Lanes& lanes) {
   const ModelConfig& cfg = model.cfg_;
   const Timestep L = sample.window.length, H = sample.window.horizon;
   const NodeId n = sample.views[0].num_nodes;
   const int D = cfg.layers;
   const bool lstm = cell_kind_of(cfg.arch) == CellKind::kLstm;
+  auto lane_of = [&](int l) { return lanes.two ? (l - 1) & 1 : 0; };
   std::vector<Buf> dh(D), dc(D);
   for (int l = 0; l < D; ++l) {
-    dh[l] = zero_buf(static_cast<size_t>(n) * cfg.hidden_dim, st);
-    if (lstm) dc[l] = zero_buf(static_cast<size_t>(n) * cfg.hidden_dim, st);
+    dh[l] = zero_buf(static_cast<size_t>(n) * cfg.hidden_dim, lanes.of(l + 1));
+    if (lstm) dc[l] = zero_buf(static_cast<size_t>(n) * cfg.hidden_dim, lanes.of(l + 1));
   }
   auto step = [&](std::vector<CellSlot>& cells, const std::vector<GraphStepTape>& tapes,
                   const GraphView& view) {
     for (int l = D; l >= 1; --l) {
+      cudaStream_t st = lanes.of(l);
       const GraphStepTape& tape = tapes[l - 1];
       StepGrads sg = cell_step_backward(cells[l - 1], tape.core, tape.agg_x->dense_values(),
                                         tape.agg_h->dense_values(), tape.agg_x.get(),
                                         tape.agg_h.get(), &view, dh[l - 1], lstm ? dc[l - 1] : nullptr,
-                                        l > 1, g, st);
+                                        l > 1, g[lane_of(l)], st);
       dh[l - 1] = sg.dh_prev;
       if (lstm) dc[l - 1] = sg.dc_prev;
-      if (l > 1) cuda::axpy(static_cast<int64_t>(n) * cfg.hidden_dim, 1.f, sg.dx->get(), dh[l - 2]->get(), st);
+      if (l > 1) {
+        // dx crosses to layer l-1's lane: ordered by an event, kept alive to the join
+        cudaStream_t down = lanes.of(l - 1);
+        lanes.dep(st, down);
+        cuda::axpy(static_cast<int64_t>(n) * cfg.hidden_dim, 1.f, sg.dx->get(), dh[l - 2]->get(), down);
+        if (down != st) lanes.keep.push_back(sg.dx);
+      }
       // layer-1 inputs are data or stop-gradient feedback: dx is never formed
     }
   };
+  cudaStream_t top = lanes.of(D);
   for (Timestep j = H - 1; j >= 0; --j) {
-    const GraphStepTape& top = fwd.dec_steps[j][D - 1];
-    head_backward(model, n, top.core.h->get(), dpred[j], dh[D - 1], g, st);
+    const GraphStepTape& ts = fwd.dec_steps[j][D - 1];
+    head_backward(model, n, ts.core.h->get(), dpred[j], dh[D - 1], g[lane_of(D)], top);
     step(model.dec_, fwd.dec_steps[j], sample.views[L + j]);
   }
   for (Timestep idx = L - 1; idx >= 0; --idx) step(model.enc_, fwd.enc_steps[idx], sample.views[idx]);
+  lanes.join();
 }
 
 void stacked_backward(DgnnModel& model, const SeqSample& sample, const ForwardArtifacts& fwd,
@@ -692,13 +710,47 @@ void stacked_backward(DgnnModel& model, const SeqSample& sample, const ForwardAr
 
 }  // namespace
 
+Lanes::~Lanes() {
+  for (cudaEvent_t e : events) cudaEventDestroy(e);
+}
+
+void Lanes::dep(cudaStream_t from, cudaStream_t to) {
+  if (from == to) return;
+  if (events.empty()) {
+    cudaEvent_t e;
+    DGNN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    events.push_back(e);
+  }
+  // a wait binds to the record preceding it, so one event can be re-recorded
+  cudaEvent_t e = events[0];
+  DGNN_CUDA(cudaEventRecord(e, from));
+  DGNN_CUDA(cudaStreamWaitEvent(to, e, 0));
+}
+
+ForwardArtifacts model_forward(DgnnModel& model, const SeqSample& sample, AggProvider& provider,
+                               Lanes& lanes) {
+  if (is_stacked(model.cfg_.arch)) return stacked_forward(model, sample, provider);
+  cudaStream_t prev = provider.stream();
+  provider.set_stream(lanes.main());
+  ForwardArtifacts out = seq2seq_forward(model, sample, provider, lanes);
+  provider.set_stream(prev);
+  return out;
+}
+
 ForwardArtifacts model_forward(DgnnModel& model, const SeqSample& sample, AggProvider& provider) {
-  return is_stacked(model.cfg_.arch) ? stacked_forward(model, sample, provider)
-                                     : seq2seq_forward(model, sample, provider);
+  Lanes lanes(provider.stream(), nullptr);
+  return model_forward(model, sample, provider, lanes);
 }
 
 void model_backward(DgnnModel& model, const SeqSample& sample, const ForwardArtifacts& fwd,
                     const std::vector<Buf>& dpred, float* grad, cudaStream_t stream) {
+  Lanes lanes(stream, nullptr);
+  model_backward(model, sample, fwd, dpred, grad, lanes);
+}
+
+void model_backward(DgnnModel& model, const SeqSample& sample, const ForwardArtifacts& fwd,
+                    const std::vector<Buf>& dpred, float* grad, Lanes& lanes) {
+  cudaStream_t stream = lanes.main();
   check(dpred.size() == fwd.predictions.size(), "model_backward: dpred arity mismatch");
   const NodeId n = sample.views[0].num_nodes;
   const int H = model.cfg_.hidden_dim;
@@ -712,14 +764,18 @@ void model_backward(DgnnModel& model, const SeqSample& sample, const ForwardArti
   for (int in : {d, H})
     if (cuda::umma_cell_supported(in, H)) ws_n = std::max(ws_n, cuda::umma_wgrad_workspace(in, H));
   cuda::DevArray<float> ws(ws_n, stream);
-  Grads g{grad, ws.get()};
   zero_cell_accumulators(model.enc_, stream);
   zero_cell_accumulators(model.dec_, stream);
   zero_cell_accumulators(model.rnn_, stream);
   if (is_stacked(model.cfg_.arch)) {
+    Grads g{grad, ws.get()};
     stacked_backward(model, sample, fwd, dpred, g, stream);
   } else {
-    integrated_backward(model, sample, fwd, dpred, g, stream);
+    // one gemm_tn workspace per lane; accumulator zeroing visible to lane 1
+    cuda::DevArray<float> ws1(lanes.two ? ws_n : 0, lanes.s[1]);
+    lanes.dep(stream, lanes.s[1]);
+    Grads g[2] = {{grad, ws.get()}, {grad, lanes.two ? ws1.get() : ws.get()}};
+    integrated_backward(model, sample, fwd, dpred, g, lanes);  // ends joined
   }
   flush_cell_grads(model.enc_, grad, stream);
   flush_cell_grads(model.dec_, grad, stream);

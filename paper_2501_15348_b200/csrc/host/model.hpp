@@ -169,11 +169,40 @@ struct ForwardArtifacts {
   std::vector<std::vector<Buf>> rnn_in, h_out;
 };
 
+// Layer pipelining of the integrated models: layer l of the GraphRNN stack
+// runs on lane (l-1) % 2 — lane 0 is the sample's stream, lane 1 an auxiliary
+// stream — so layer 2's neighbourhood SpMMs (HBM-bound) overlap layer 1's cell
+// GEMMs (tensor-bound) of the next step, and vice versa in BPTT. Cross-layer
+// data dependencies are CUDA events; buffers crossing lanes are kept alive
+// until the final two-way join, after which every stream-ordered free is safe.
+struct Lanes {
+  cudaStream_t s[2] = {nullptr, nullptr};
+  bool two = false;
+  std::vector<cudaEvent_t> events;
+  std::vector<Buf> keep;
+  Lanes(cudaStream_t main, cudaStream_t aux) : s{main, aux ? aux : main}, two(aux != nullptr) {}
+  ~Lanes();
+  Lanes(const Lanes&) = delete;
+  Lanes& operator=(const Lanes&) = delete;
+  cudaStream_t main() const { return s[0]; }
+  cudaStream_t of(int layer) const { return two ? s[(layer - 1) & 1] : s[0]; }
+  // `to` waits for everything issued so far on `from`
+  void dep(cudaStream_t from, cudaStream_t to);
+  void join() {
+    dep(s[1], s[0]);
+    dep(s[0], s[1]);
+  }
+};
+
 ForwardArtifacts model_forward(DgnnModel& model, const SeqSample& sample, AggProvider& provider);
+ForwardArtifacts model_forward(DgnnModel& model, const SeqSample& sample, AggProvider& provider,
+                               Lanes& lanes);
 
 // grad (flat, num_params) += gradients of this sample given per-horizon dpred.
 void model_backward(DgnnModel& model, const SeqSample& sample, const ForwardArtifacts& fwd,
                     const std::vector<Buf>& dpred, float* grad, cudaStream_t stream);
+void model_backward(DgnnModel& model, const SeqSample& sample, const ForwardArtifacts& fwd,
+                    const std::vector<Buf>& dpred, float* grad, Lanes& lanes);
 
 // Per-sample MAE on the seed rows of every horizon step (ref src/train.cpp:119-144):
 // writes dpred and adds the sample loss (mean over H) into *loss_slot (device).

@@ -72,16 +72,34 @@ Worker::Worker(const DeviceGraph& graph, DgnnModel& model, const TrainConfig& cf
   provider_ = std::make_unique<AggProvider>(store_.get(), &graph, model.cfg_.aggr, cfg.incremental,
                                             inc, stream);
   loss_ws_ = cuda::DevArray<double>(512, stream);
+  // Layer lanes for multi-layer integrated models (opt-in: DGNN_LAYER_STREAMS=1).
+  // Measured at C3 they lose ~7% to the single lane — both lanes are HBM-bound
+  // and the part is power-capped, so overlap only adds L2 contention. The
+  // HBM-spill level orders its copies against one compute stream, so it keeps
+  // a single lane.
+  const char* env = std::getenv("DGNN_LAYER_STREAMS");
+  const bool lanes_on = env && std::string(env) == "1";
+  if (lanes_on && !is_stacked(model.cfg_.arch) && model.cfg_.layers > 1 &&
+      cfg.hbm_cache_budget_bytes <= 0) {
+    DGNN_CUDA(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking));
+  }
 }
 
-Worker::~Worker() = default;
+Worker::~Worker() {
+  if (aux_) {
+    cudaStreamSynchronize(aux_);
+    cudaStreamDestroy(aux_);
+  }
+}
 
 void Worker::run_sample(const SequenceWindow& window, Timestep windows_remaining, int64_t batch_id,
                         std::pair<NodeId, NodeId> node_range, float* grad, double* loss_slot) {
   SeqSample sample = build_sample(graph_, model_.cfg_, window, windows_remaining, batch_id, node_range);
-  ForwardArtifacts fwd = model_forward(model_, sample, *provider_);
-  std::vector<Buf> dpred = seed_loss(sample, fwd, model_.cfg_.feature_dim, loss_slot, loss_ws_.get(), stream_);
-  model_backward(model_, sample, fwd, dpred, grad, stream_);
+  Lanes lanes(stream_, aux_);
+  ForwardArtifacts fwd = model_forward(model_, sample, *provider_, lanes);
+  std::vector<Buf> dpred = seed_loss(sample, fwd, model_.cfg_.feature_dim, loss_slot, loss_ws_.get(),
+                                     lanes.of(model_.cfg_.layers));
+  model_backward(model_, sample, fwd, dpred, grad, lanes);
 }
 
 // ---------------------------------------------------------------- seq-first

@@ -81,6 +81,7 @@ class Worker {
   DgnnModel& model_;
   TrainConfig cfg_;
   cudaStream_t stream_;
+  cudaStream_t aux_ = nullptr;  // second layer lane (null: single-stream)
   std::unique_ptr<CacheStore> store_;
   std::unique_ptr<AggProvider> provider_;
   cuda::DevArray<double> loss_ws_;
