@@ -229,7 +229,8 @@ int64_t dgnn_init_params(const dgnn_run_cfg* cfg, int32_t feature_dim, double* o
 
 /* ---------------------------------------------------------------- profiling
  * Device timing per kernel class (0 agg_scratch, 1 agg_delta, 2 agg_backward,
- * 3 cell_fwd, 4 cell_bwd, 5 weight_grad, 6 other) with algorithmic bytes. */
+ * 3 cell_fwd, 4 cell_bwd (pointwise), 5 weight_grad, 6 other, 7 cell_bwd_gemm
+ * (the dX | dHm contraction)) with algorithmic bytes. */
 int dgnn_prof_enable(int32_t on);
 int dgnn_prof_reset(void);
 int dgnn_prof_get(int32_t cls, int64_t* launches, double* ms, double* bytes, double* flops);

@@ -538,7 +538,7 @@ class TrainSession:
 
 # ------------------------------------------------------------------ profiling
 PROF_CLASSES = ["agg_scratch", "agg_delta", "agg_backward", "cell_fwd", "cell_bwd",
-                "weight_grad", "other"]
+                "weight_grad", "other", "cell_bwd_gemm"]
 
 
 def prof_enable(on=True):

@@ -19,6 +19,7 @@ struct dgnn_graph {
   std::unique_ptr<DeviceGraph> g;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  FeatRef last_feats;  // keeps the version returned by dgnn_graph_snapshot resident
 };
 
 struct dgnn_synth {
@@ -149,6 +150,7 @@ void dgnn_graph_free(dgnn_graph* g) {
   if (!g) return;
   cudaStream_t s = g->stream;
   bool own = g->own_stream;
+  g->last_feats.reset();  // leases end before their slots and stream
   g->g.reset();
   cudaStreamSynchronize(s);
   if (own) cudaStreamDestroy(s);
@@ -190,7 +192,12 @@ int dgnn_graph_snapshot(const dgnn_graph* g, int32_t t, const int64_t** in_ptr,
     if (in_src) *in_src = s.in_src.get();
     if (out_ptr) *out_ptr = s.out_ptr.get();
     if (out_dst) *out_dst = s.out_dst.get();
-    if (feats) *feats = s.feats.get();
+    if (feats) {
+      auto* mg = const_cast<dgnn_graph*>(g);
+      mg->last_feats = g->g->features(t, g->stream);
+      DGNN_CUDA(cudaStreamSynchronize(g->stream));
+      *feats = mg->last_feats->get();
+    }
   });
 }
 
@@ -384,9 +391,10 @@ int dgnn_agg_incremental(const dgnn_graph* g, int32_t t, int32_t kind, const flo
       cp(prev.mean_sums, prev_mean_sums, nw);
     }
     if (kind >= 2) cp(prev.argext, prev_argext, nw);
+    FeatRef f_prev = G.features(t - 1, st), f_cur = G.features(t, st);
     IncrementalResult r = aggregate_incremental(
-        prev, GraphView::of(G, t - 1), GraphView::of(G, t), G.snapshot(t - 1).feats.get(),
-        G.snapshot(t).feats.get(), G.delta(t), t, AggrFn{static_cast<AggrKind>(kind)},
+        prev, GraphView::of(G, t - 1), GraphView::of(G, t), f_prev->get(),
+        f_cur->get(), G.delta(t), t, AggrFn{static_cast<AggrKind>(kind)},
         IncrementalOptions{fallback_threshold, rescratch_period}, st);
     DGNN_CUDA(cudaMemcpyAsync(values, r.result->values.get(), sizeof(float) * nw, cudaMemcpyDeviceToDevice, st));
     if (kind == 1) {
@@ -672,7 +680,7 @@ int dgnn_session_sample_grads(dgnn_session* s, int32_t window_index, double* los
     auto batches = make_batches(G.num_nodes(), s->tcfg.batch_size, s->tcfg.seed, 0);
     SeqSample sample = build_sample(G, s->mcfg, windows[window_index],
                                     static_cast<Timestep>(windows.size() - 1 - window_index), 0,
-                                    batches[0]);
+                                    batches[0], st);
     ForwardArtifacts fwd = model_forward(model, sample, fresh.provider());
     cuda::DevArray<double> slot(1, st), ws(512, st);
     slot.zero(st);

@@ -4,6 +4,7 @@
 // library primitives); the graph-specific passes are the kernels below.
 #include <cub/cub.cuh>
 
+#include <cstdlib>
 #include <stdexcept>
 
 #include "common.cuh"
@@ -149,6 +150,15 @@ __global__ void k_scatter_rows(int64_t m, int32_t d, const int32_t* __restrict__
   }
 }
 
+__global__ void k_gather_rows(int64_t m, int32_t d, const int32_t* __restrict__ nodes,
+                              const float* __restrict__ feats, float* __restrict__ rows) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m * d;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / d;
+    rows[i] = feats[static_cast<int64_t>(nodes[r]) * d + (i - r * d)];
+  }
+}
+
 int grid_for(int64_t n) { return cuda::wave_grid(n, kT, 8); }
 
 // Thin CUB wrappers with a growable temp buffer.
@@ -251,9 +261,102 @@ DeviceGraph::DeviceGraph(int32_t num_nodes, int32_t feature_dim, cudaStream_t st
     : n_(num_nodes), d_(feature_dim), stream_(stream) {
   if (num_nodes <= 0) throw std::invalid_argument("snapshot needs at least one node");
   if (feature_dim <= 0) throw std::invalid_argument("feature_dim must be positive");
+  double gb = 24.0;
+  if (const char* e = std::getenv("DGNN_FEATURE_BUDGET_GB")) gb = std::atof(e);
+  const double per = 4.0 * num_nodes * feature_dim;
+  const double slots = gb * 1e9 / per;
+  max_slots_ = slots >= 1e6 ? 1000000 : (slots < 2 ? 2 : static_cast<int32_t>(slots));
 }
 
-DeviceGraph::~DeviceGraph() = default;
+DeviceGraph::~DeviceGraph() {
+  // slot buffers are freed on the graph stream: let readers on other streams finish
+  cudaDeviceSynchronize();
+}
+
+// ---------------------------------------------------------------- feature versions
+FeatSlot::~FeatSlot() {
+  if (ready) cudaEventDestroy(ready);
+  for (auto& r : readers) cudaEventDestroy(r.second);
+}
+
+FeatLease::FeatLease(std::shared_ptr<FeatSlot> slot, cudaStream_t stream)
+    : slot_(std::move(slot)), stream_(stream) {}
+
+FeatLease::~FeatLease() {
+  // the slot may be rewritten once this stream's reads are done
+  for (auto& r : slot_->readers) {
+    if (r.first == stream_) {
+      cudaEventRecord(r.second, stream_);
+      return;
+    }
+  }
+  cudaEvent_t e;
+  if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess) {
+    cudaEventRecord(e, stream_);
+    slot_->readers.emplace_back(stream_, e);
+  }
+}
+
+void DeviceGraph::order_after_write(const FeatSlot& s, cudaStream_t stream) const {
+  if (s.ready && s.writer != stream) DGNN_CUDA(cudaStreamWaitEvent(stream, s.ready, 0));
+}
+
+std::shared_ptr<FeatSlot> DeviceGraph::free_slot(cudaStream_t stream) const {
+  const int32_t resident = static_cast<int32_t>(slots_.size()) - 1;  // slots_[0] is snapshot 0
+  std::shared_ptr<FeatSlot> victim;
+  if (resident >= max_slots_) {
+    for (size_t i = 1; i < slots_.size(); ++i) {
+      const auto& s = slots_[i];
+      if (s.use_count() != 1) continue;  // leased
+      if (!victim || s->stamp < victim->stamp) victim = s;
+    }
+  }
+  if (!victim) {  // below the budget, or every slot leased: grow
+    victim = std::make_shared<FeatSlot>();
+    victim->buf = DevArray<float>(static_cast<size_t>(n_) * d_, stream_);
+    DGNN_CUDA(cudaEventCreateWithFlags(&victim->ready, cudaEventDisableTiming));
+    slots_.push_back(victim);
+    // the allocation is ordered on the graph stream
+    DGNN_CUDA(cudaEventRecord(victim->ready, stream_));
+    victim->writer = stream_;
+  }
+  order_after_write(*victim, stream);
+  for (auto& r : victim->readers) DGNN_CUDA(cudaStreamWaitEvent(stream, r.second, 0));
+  victim->t = -1;
+  return victim;
+}
+
+FeatRef DeviceGraph::features(int32_t t, cudaStream_t stream) const {
+  if (t < 0 || t >= length()) throw std::out_of_range("snapshot index out of range");
+  std::shared_ptr<FeatSlot> hit, base;
+  for (const auto& s : slots_) {
+    if (s->t == t) hit = s;
+    if (s->t >= 0 && s->t <= t && (!base || s->t > base->t)) base = s;
+  }
+  if (!hit) {
+    // nearest version <= t, then the row patches of base.t+1 .. t in order
+    auto src = std::make_shared<const FeatLease>(base, stream);  // pinned while copying
+    hit = free_slot(stream);
+    order_after_write(*base, stream);
+    const int64_t nf = static_cast<int64_t>(n_) * d_;
+    DGNN_CUDA(cudaMemcpyAsync(hit->buf.get(), base->buf.get(), sizeof(float) * nf,
+                              cudaMemcpyDeviceToDevice, stream));
+    for (int32_t k = base->t + 1; k <= t; ++k) {
+      const DevDelta& dd = deltas_[k];
+      if (dd.n_changed > 0)
+        DGNN_LAUNCH(k_scatter_rows, grid_for(dd.n_changed * d_), kT, 0, stream, dd.n_changed, d_,
+                    dd.changed.get(), patch_rows_[k].get(), hit->buf.get());
+    }
+    hit->t = t;
+    hit->writer = stream;
+    DGNN_CUDA(cudaEventRecord(hit->ready, stream));
+    ++materialisations_;
+  } else {
+    order_after_write(*hit, stream);
+  }
+  hit->stamp = ++clock_;
+  return std::make_shared<const FeatLease>(hit, stream);
+}
 
 const DevSnapshot& DeviceGraph::snapshot(int32_t t) const {
   if (t < 0 || t >= length()) throw std::out_of_range("snapshot index out of range");
@@ -268,9 +371,11 @@ const DevDelta& DeviceGraph::delta(int32_t t) const {
 int64_t DeviceGraph::device_bytes() const {
   int64_t b = 0;
   for (const auto& s : snaps_)
-    b += s.in_ptr.bytes() + s.out_ptr.bytes() + s.in_src.bytes() + s.out_dst.bytes() + s.feats.bytes();
+    b += s.in_ptr.bytes() + s.out_ptr.bytes() + s.in_src.bytes() + s.out_dst.bytes();
   for (const auto& d : deltas_)
     b += d.del.bytes() + d.ins.bytes() + d.changed.bytes() + d.rows.bytes() + d.row_ptr.bytes() + d.ent.bytes();
+  for (const auto& p : patch_rows_) b += p.bytes();
+  for (const auto& s : slots_) b += s->buf.bytes();
   return b;
 }
 
@@ -278,8 +383,29 @@ void DeviceGraph::add_snapshot(const int32_t* src, const int32_t* dst, int64_t n
                                const float* feats) {
   Cub cub(stream_);
   DevArray<uint64_t> keys = sorted_edge_keys(src, dst, num_edges, n_, cub, true);
-  DevArray<float> f = upload(feats, static_cast<int64_t>(n_) * d_, stream_);
-  finish_snapshot(std::move(keys), std::move(f));
+  const int64_t nf = static_cast<int64_t>(n_) * d_;
+  if (snaps_.empty()) {
+    auto s0 = std::make_shared<FeatSlot>();
+    s0->buf = upload(feats, nf, stream_);
+    DGNN_CUDA(cudaEventCreateWithFlags(&s0->ready, cudaEventDisableTiming));
+    DGNN_CUDA(cudaEventRecord(s0->ready, stream_));
+    s0->writer = stream_;
+    s0->t = 0;
+    slots_.push_back(s0);
+    finish_snapshot(std::move(keys), nullptr, s0->buf.get());
+    return;
+  }
+  // a full snapshot t >= 1 (Snapshot ctor per step): its features become the
+  // exact row patch against t-1
+  const int32_t t = length();
+  FeatRef prev = features(t - 1, stream_);
+  std::shared_ptr<FeatSlot> cur = free_slot(stream_);
+  DGNN_CUDA(cudaMemcpyAsync(cur->buf.get(), feats, sizeof(float) * nf, cudaMemcpyHostToDevice, stream_));
+  finish_snapshot(std::move(keys), prev->get(), cur->buf.get());
+  cur->t = t;
+  cur->writer = stream_;
+  cur->stamp = ++clock_;
+  DGNN_CUDA(cudaEventRecord(cur->ready, stream_));
 }
 
 void DeviceGraph::add_delta(const int32_t* del_src, const int32_t* del_dst, int64_t n_del,
@@ -313,25 +439,30 @@ void DeviceGraph::add_delta(const int32_t* del_src, const int32_t* del_dst, int6
     DGNN_CUDA(cudaMemcpyAsync(exact.get(), keys.get(), sizeof(uint64_t) * E1, cudaMemcpyDeviceToDevice, st));
   // features: prev rows with the changed rows replaced
   const int64_t nf = static_cast<int64_t>(n_) * d_;
-  DevArray<float> f(nf, st);
-  DGNN_CUDA(cudaMemcpyAsync(f.get(), snaps_.back().feats.get(), sizeof(float) * nf,
-                            cudaMemcpyDeviceToDevice, st));
+  const int32_t t = length();
+  FeatRef prev = features(t - 1, st);
+  std::shared_ptr<FeatSlot> cur = free_slot(st);
+  DGNN_CUDA(cudaMemcpyAsync(cur->buf.get(), prev->get(), sizeof(float) * nf, cudaMemcpyDeviceToDevice, st));
   if (n_changed > 0) {
     DevArray<int32_t> nodes = upload(changed_nodes, n_changed, st);
     DevArray<float> rows = upload(changed_feats, n_changed * d_, st);
     DGNN_LAUNCH(k_scatter_rows, grid_for(n_changed * d_), kT, 0, st, n_changed, d_, nodes.get(),
-                rows.get(), f.get());
+                rows.get(), cur->buf.get());
   }
-  finish_snapshot(std::move(exact), std::move(f));
+  finish_snapshot(std::move(exact), prev->get(), cur->buf.get());
+  cur->t = t;
+  cur->writer = st;
+  cur->stamp = ++clock_;
+  DGNN_CUDA(cudaEventRecord(cur->ready, st));
 }
 
-void DeviceGraph::finish_snapshot(DevArray<uint64_t> keys, DevArray<float> feats) {
+void DeviceGraph::finish_snapshot(DevArray<uint64_t> keys, const float* prev_feats,
+                                  const float* feats) {
   cudaStream_t st = stream_;
   Cub cub(st);
   const int64_t E = static_cast<int64_t>(keys.size());
   DevSnapshot s;
   s.num_edges = E;
-  s.feats = std::move(feats);
   // out-CSR: keys already sorted by (src, dst)
   DevArray<unsigned long long> cnt(n_ + 1, st);
   cnt.zero(st);
@@ -356,13 +487,14 @@ void DeviceGraph::finish_snapshot(DevArray<uint64_t> keys, DevArray<float> feats
   cub.exclusive_sum(reinterpret_cast<const int64_t*>(cnt.get()), s.in_ptr.get(), n_ + 1);
   snaps_.push_back(std::move(s));
   deltas_.emplace_back();
+  patch_rows_.emplace_back();
   prev_keys_ = std::move(curr_keys_);
   curr_keys_ = std::move(keys);
-  if (snaps_.size() >= 2) build_delta(static_cast<int32_t>(snaps_.size()) - 1);
+  if (snaps_.size() >= 2) build_delta(static_cast<int32_t>(snaps_.size()) - 1, prev_feats, feats);
   prev_keys_.reset();
 }
 
-void DeviceGraph::build_delta(int32_t t) {
+void DeviceGraph::build_delta(int32_t t, const float* prev_feats, const float* feats) {
   cudaStream_t st = stream_;
   Cub cub(st);
   const DevSnapshot& P = snaps_[t - 1];
@@ -372,15 +504,20 @@ void DeviceGraph::build_delta(int32_t t) {
   // changed nodes (exact row inequality), ascending
   DevArray<uint8_t> fl(n_, st);
   DGNN_LAUNCH(k_row_differs, cuda::wave_grid(static_cast<int64_t>(n_) * 32, kT, 8), kT, 0, st, n_,
-              d_, P.feats.get(), Cs.feats.get(), fl.get());
+              d_, prev_feats, feats, fl.get());
   DevArray<int32_t> iota(n_, st);
   DGNN_LAUNCH(k_iota, grid_for(n_), kT, 0, st, n_, iota.get());
   DevArray<int32_t> changed(n_, st);
   dd.n_changed = cub.select_flagged(iota.get(), fl.get(), changed.get(), n_);
   dd.changed = DevArray<int32_t>(dd.n_changed, st);
-  if (dd.n_changed)
+  if (dd.n_changed) {
     DGNN_CUDA(cudaMemcpyAsync(dd.changed.get(), changed.get(), sizeof(int32_t) * dd.n_changed,
                               cudaMemcpyDeviceToDevice, st));
+    // the version patch: changed rows at t
+    patch_rows_[t] = DevArray<float>(dd.n_changed * d_, st);
+    DGNN_LAUNCH(k_gather_rows, grid_for(dd.n_changed * d_), kT, 0, st, dd.n_changed, d_,
+                dd.changed.get(), feats, patch_rows_[t].get());
+  }
   // expansion sizes
   auto expansion = [&](const DevSnapshot& S, int64_t* total) {
     DevArray<int64_t> deg(dd.n_changed + 1, st), off(dd.n_changed + 1, st);

@@ -4,7 +4,9 @@
 // with everything built and kept in HBM:
 //   per snapshot t : in-CSR (in_ptr int64[N+1], in_src int32[E], sources
 //                    ascending per destination), out-CSR (out_ptr, out_dst,
-//                    destinations ascending per source), features fp32 N x d;
+//                    destinations ascending per source); features as
+//                    versions (snapshot 0 whole + exact per-t row patches,
+//                    see FeatSlot below);
 //   per t >= 1     : the reference's extract_delta (src/snapshot.cpp:102-130),
 //                    bit-exact: deletions / insertions (sorted unique (src,dst)
 //                    keys incl. the feature-change out-edge expansion), changed
@@ -18,7 +20,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "memory.h"
@@ -29,8 +33,39 @@ struct DevSnapshot {
   int64_t num_edges = 0;
   cuda::DevArray<int64_t> in_ptr, out_ptr;
   cuda::DevArray<int32_t> in_src, out_dst;
-  cuda::DevArray<float> feats;  // N x d (may alias the previous snapshot's rows? no: owned)
 };
+
+// Versioned node features. Snapshot 0's N x d matrix is kept whole; every
+// t >= 1 keeps only its exact changed rows (DevDelta::changed, values at t) —
+// 2% of N at C4 instead of 2 GB per snapshot. Versions are materialised on
+// demand (nearest resident version <= t, then the row patches in t order)
+// into a bounded set of HBM slots, least-recently-used unpinned slot first.
+// A lease pins its slot; cross-stream use is ordered by events (the slot's
+// materialisation, and each reader stream's last use before a slot is reused).
+struct FeatSlot {
+  int32_t t = -1;
+  uint64_t stamp = 0;
+  cuda::DevArray<float> buf;
+  cudaStream_t writer = nullptr;
+  cudaEvent_t ready = nullptr;
+  std::vector<std::pair<cudaStream_t, cudaEvent_t>> readers;
+  ~FeatSlot();
+};
+
+class FeatLease {
+ public:
+  FeatLease(std::shared_ptr<FeatSlot> slot, cudaStream_t stream);
+  ~FeatLease();
+  FeatLease(const FeatLease&) = delete;
+  FeatLease& operator=(const FeatLease&) = delete;
+  const float* get() const { return slot_->buf.get(); }
+  int32_t t() const { return slot_->t; }
+
+ private:
+  std::shared_ptr<FeatSlot> slot_;
+  cudaStream_t stream_;
+};
+using FeatRef = std::shared_ptr<const FeatLease>;
 
 struct DevDelta {
   int64_t n_del = 0, n_ins = 0, n_changed = 0;
@@ -67,18 +102,35 @@ class DeviceGraph {
   const DevDelta& delta(int32_t t) const;
   cudaStream_t stream() const { return stream_; }
 
-  // Drops the device features of snapshots < t_keep (memory at C4 scale).
+  // Features of snapshot t, resident for the lifetime of the returned lease
+  // and ordered before work later issued on `stream`.
+  FeatRef features(int32_t t, cudaStream_t stream) const;
+  // HBM slots for materialised feature versions (snapshot 0 is always
+  // resident and not counted). Default: every version if they fit
+  // DGNN_FEATURE_BUDGET_GB (default 24), else as many as fit, at least 2.
+  void set_feature_slots(int32_t slots) { max_slots_ = slots < 2 ? 2 : slots; }
+  int32_t feature_slots() const { return max_slots_; }
+  int64_t feature_materialisations() const { return materialisations_; }
+
   int64_t device_bytes() const;
 
  private:
-  void finish_snapshot(cuda::DevArray<uint64_t> keys, cuda::DevArray<float> feats);
-  void build_delta(int32_t t);
+  void finish_snapshot(cuda::DevArray<uint64_t> keys, const float* prev_feats, const float* feats);
+  void build_delta(int32_t t, const float* prev_feats, const float* feats);
+  std::shared_ptr<FeatSlot> free_slot(cudaStream_t stream) const;
+  void order_after_write(const FeatSlot& s, cudaStream_t stream) const;
 
   int32_t n_, d_;
   cudaStream_t stream_;
   std::vector<DevSnapshot> snaps_;
   std::vector<DevDelta> deltas_;  // deltas_[t], t >= 1; deltas_[0] unused
   cuda::DevArray<uint64_t> prev_keys_, curr_keys_;  // sorted (src,dst) of the last two snapshots
+  // feature versions
+  std::vector<cuda::DevArray<float>> patch_rows_;  // [t]: rows of delta(t).changed at t
+  mutable std::vector<std::shared_ptr<FeatSlot>> slots_;  // slots_[0] = snapshot 0
+  mutable uint64_t clock_ = 0;
+  mutable int64_t materialisations_ = 0;
+  int32_t max_slots_ = 0;
 };
 
 // Host copies (tests / C-ABI getters).

@@ -116,7 +116,8 @@ void aggregate_backward(const GraphView& graph, const float* upstream, int32_t d
 // wrappers bracket kernels with CUDA events and accumulate durations and
 // algorithmic bytes per class.
 enum ProfClass { kProfAggScratch = 0, kProfAggDelta = 1, kProfAggBackward = 2, kProfCellFwd = 3,
-                 kProfCellBwd = 4, kProfWeightGrad = 5, kProfOther = 6, kProfCount = 7 };
+                 kProfCellBwd = 4, kProfWeightGrad = 5, kProfOther = 6, kProfCellBwdGemm = 7,
+                 kProfCount = 8 };
 struct ProfStat {
   int64_t launches = 0;
   double ms = 0.0;

@@ -4,6 +4,7 @@
 #include "model.hpp"
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <random>
@@ -290,7 +291,7 @@ void DgnnModel::refresh_packed() {
 
 SeqSample build_sample(const DeviceGraph& graph, const ModelConfig& mcfg,
                        const SequenceWindow& window, Timestep windows_remaining, int64_t batch_id,
-                       std::pair<NodeId, NodeId> node_range) {
+                       std::pair<NodeId, NodeId> node_range, cudaStream_t stream) {
   (void)mcfg;
   SeqSample s;
   s.window = window;
@@ -301,7 +302,10 @@ SeqSample build_sample(const DeviceGraph& graph, const ModelConfig& mcfg,
   const Timestep span = window.length + window.horizon;
   for (Timestep i = 0; i < span; ++i) s.views.push_back(GraphView::of(graph, window.start + i));
   // snapshot(t) bound check reproduces the reference's .at()
-  for (Timestep i = 0; i <= span; ++i) s.feats.push_back(graph.snapshot(window.start + i).feats.get());
+  for (Timestep i = 0; i <= span; ++i) {
+    s.feat_refs.push_back(graph.features(window.start + i, stream));
+    s.feats.push_back(s.feat_refs.back()->get());
+  }
   return s;
 }
 
@@ -328,24 +332,45 @@ ExecContext make_ctx(const DgnnModel& model, const SeqSample& sample, ModelPart 
 
 double cell_flops(int64_t n, int in, int H) { return 2.0 * n * (in + H) * 4.0 * H; }
 
+}  // namespace
+
+bool gate_recompute_policy(const ModelConfig& cfg, int64_t num_nodes) {
+  if (const char* e = std::getenv("DGNN_GATE_TAPE")) return e[0] == '0';
+  // auto: drop the gates tape when it would take more than 24 GB per sample
+  // (C4: 4M nodes x 4H x 9 steps x 2 layers = 74 GB; C3 keeps its 18 GB tape,
+  // which measured ~2% faster than the recompute)
+  const double tape = 4.0 * num_nodes * 4 * cfg.hidden_dim *
+                      static_cast<double>(cfg.seq_len + cfg.horizon) * cfg.layers;
+  return tape > 24e9;
+}
+
+void DgnnModel::set_gate_recompute(bool on) {
+  for (auto* cells : {&enc_, &dec_, &rnn_})
+    for (auto& c : *cells) c.recompute = c.umma && on;
+}
+
+namespace {
+
 // cell_core_forward on device operands (ref src/cells.cpp:102-132).
 CellTape cell_forward(const CellSlot& c, NodeId n, const float* X, const float* Hm, const Buf& h_skip,
                       const Buf& c_prev, cudaStream_t st) {
   CellTape t;
-  t.gates = new_buf(static_cast<size_t>(n) * 4 * c.H, st);
+  if (!c.recompute) t.gates = new_buf(static_cast<size_t>(n) * 4 * c.H, st);
   t.h = new_buf(static_cast<size_t>(n) * c.H, st);
   t.h_skip = h_skip;
   if (c.lstm) {
     t.c_prev = c_prev;
     t.c = new_buf(static_cast<size_t>(n) * c.H, st);
   }
-  // X, Hm, W + gates, h (c, c_prev) traffic
-  const double bytes = 4.0 * n * (c.in + c.H + 4 * c.H + c.H + (c.lstm ? 2 * c.H : c.H));
+  // X, Hm, W + (gates), h (c, c_prev) traffic
+  const double bytes =
+      4.0 * n * (c.in + c.H + (c.recompute ? 0 : 4 * c.H) + c.H + (c.lstm ? 2 * c.H : c.H));
   ProfScope ps(kProfCellFwd, st, bytes, cell_flops(n, c.in, c.H));
   if (c.umma) {
     cuda::umma_cell_forward(c.lstm, n, c.in, c.H, X, Hm, h_skip->get(),
                             c.lstm ? c_prev->get() : nullptr, c.Bf.get(), c.bias.get(),
-                            t.gates->get(), c.lstm ? t.c->get() : nullptr, t.h->get(), st);
+                            t.gates ? t.gates->get() : nullptr, c.lstm ? t.c->get() : nullptr,
+                            t.h->get(), st);
   } else {
     cuda::cell_forward(c.lstm, n, c.in, c.H, X, Hm, h_skip->get(), c.lstm ? c_prev->get() : nullptr,
                        c.W.get(), c.bias.get(), t.gates->get(), c.lstm ? t.c->get() : nullptr,
@@ -533,7 +558,17 @@ StepGrads cell_step_backward(CellSlot& c, const CellTape& tape, const float* X, 
   Buf G = new_buf(static_cast<size_t>(n) * 4 * H, st);
   StepGrads out;
   Buf dh_skip;
-  {
+  if (c.recompute) {
+    // X, Hm, state, dh (dc) in; G, dc_prev / dh_skip out
+    ProfScope ps(kProfCellBwd, st, 4.0 * n * (in + H + H + H + (c.lstm && dc ? H : 0) + 4 * H + H),
+                 cell_flops(n, in, H));
+    Buf& dstate = c.lstm ? out.dc_prev : dh_skip;
+    dstate = new_buf(static_cast<size_t>(n) * H, st);
+    cuda::umma_cell_backward_recompute(c.lstm, n, in, H, X, Hm, tape.h_skip->get(),
+                                       c.lstm ? tape.c_prev->get() : nullptr, c.Bf.get(),
+                                       c.bias.get(), dh->get(), dc ? dc->get() : nullptr, G->get(),
+                                       dstate->get(), st);
+  } else {
     ProfScope ps(kProfCellBwd, st, 4.0 * n * (4 * H + 4 * H + 4 * H));
     if (c.lstm) {
       out.dc_prev = new_buf(static_cast<size_t>(n) * H, st);
@@ -560,7 +595,7 @@ StepGrads cell_step_backward(CellSlot& c, const CellTape& tape, const float* X, 
   Buf dX = need_dx ? new_buf(static_cast<size_t>(n) * in, st) : nullptr;
   Buf dHm = new_buf(static_cast<size_t>(n) * H, st);
   {
-    ProfScope ps(kProfCellBwd, st, 4.0 * n * (4 * H + (need_dx ? in : 0) + H),
+    ProfScope ps(kProfCellBwdGemm, st, 4.0 * n * (4 * H + (need_dx ? in : 0) + H),
                  2.0 * n * 4 * H * ((need_dx ? in : 0) + H));
     if (c.umma) {
       if (need_dx) {

@@ -57,6 +57,10 @@ struct ModelConfig {
 std::vector<std::string> visit_order(const ModelConfig& cfg);
 std::vector<double> initial_params_host(const ModelConfig& cfg);
 
+// Whether umma cells drop the gates tape (recompute in the fused backward):
+// env DGNN_GATE_TAPE=1 keeps it, =0 drops it, unset decides by tape size.
+bool gate_recompute_policy(const ModelConfig& cfg, int64_t num_nodes);
+
 using Buf = std::shared_ptr<cuda::DevArray<float>>;
 Buf new_buf(size_t n, cudaStream_t stream);
 Buf zero_buf(size_t n, cudaStream_t stream);
@@ -79,6 +83,9 @@ struct CellSlot {
   // tcgen05 B images (3xTF32 hi/lo, canonical UMMA layout): forward W^T,
   // backward W (dX | dHm) and its dHm-only rows.
   bool umma = false;
+  // no gates tape: the backward recomputes them inside the fused tcgen05
+  // backward kernel (umma cells; see gate_recompute_policy)
+  bool recompute = false;
   cuda::DevArray<float> Bf, Bb, Bbh;
   int64_t flat_size() const {
     return static_cast<int64_t>(lstm ? 4 : 3) * (int64_t(in) * H + int64_t(H) * H + H);
@@ -110,6 +117,7 @@ class DgnnModel {
 
   float* params() { return params_.get(); }
   void refresh_packed();  // after any parameter change
+  void set_gate_recompute(bool on);
 
   ModelConfig cfg_;
   std::vector<CellSlot> enc_, dec_, rnn_;
@@ -130,6 +138,7 @@ struct SeqSample {
   SequenceWindow window;
   std::vector<GraphView> views;       // L+H views
   std::vector<const float*> feats;    // L+H+1 feature matrices (device)
+  std::vector<FeatRef> feat_refs;     // their version leases (resident while the sample lives)
   NodeId seed_begin = 0, seed_end = 0;  // loss rows (contiguous node range)
   int64_t batch_id = 0;
   Timestep windows_remaining = 0;
@@ -137,7 +146,7 @@ struct SeqSample {
 
 SeqSample build_sample(const DeviceGraph& graph, const ModelConfig& mcfg,
                        const SequenceWindow& window, Timestep windows_remaining, int64_t batch_id,
-                       std::pair<NodeId, NodeId> node_range);
+                       std::pair<NodeId, NodeId> node_range, cudaStream_t stream);
 
 struct CellTape {
   Buf gates;      // n x 4H (LSTM i,f,g,o; GRU r,z,n,hn)

@@ -6,6 +6,7 @@
 #include <numeric>
 #include <random>
 #include <stdexcept>
+#include <type_traits>
 
 #include "aggregate.hpp"
 
@@ -63,6 +64,7 @@ class EdgeSet {
     --size_;
   }
   size_t size() const { return size_; }
+  void prefetch(uint64_t k) const { __builtin_prefetch(&slots_[hash(k)], 1); }
 
  private:
   static constexpr uint64_t kEmpty = ~0ull;  // never a valid (src,dst) key
@@ -72,18 +74,88 @@ class EdgeSet {
   size_t size_ = 0;
 };
 
-// ref random_non_edge (src/synth.cpp:23-33): Edge e{pick(rng), pick(rng)} draws src then dst.
-uint64_t random_non_edge(int32_t n, const EdgeSet& present, const EdgeSet* banned,
-                         std::mt19937_64& rng) {
-  std::uniform_int_distribution<int32_t> pick(0, n - 1);
-  while (true) {
-    const int32_t s = pick(rng);
-    const int32_t d = pick(rng);
-    if (s == d) continue;
-    const uint64_t k = key_of(s, d);
-    if (present.contains(k) || (banned && banned->contains(k))) continue;
-    return k;
+// ref random_non_edge (src/synth.cpp:23-33): Edge e{pick(rng), pick(rng)}
+// draws src then dst, retrying until the edge is new. The draws do not depend
+// on the set, so a copy of the generator running kAhead attempts in front
+// prefetches the hash slots the real attempts will probe (the real generator
+// consumes exactly the reference's sequence).
+class NonEdgeSampler {
+ public:
+  static constexpr int kAhead = 24;
+  NonEdgeSampler(int32_t n, std::mt19937_64& rng, const EdgeSet& present, const EdgeSet* banned)
+      : pick_(0, n - 1), ahead_pick_(0, n - 1), rng_(rng), ahead_(rng), present_(present),
+        banned_(banned) {
+    for (int i = 0; i < kAhead; ++i) advance_ahead();
   }
+  uint64_t next() {
+    while (true) {
+      advance_ahead();
+      const int32_t s = pick_(rng_);
+      const int32_t d = pick_(rng_);
+      if (s == d) continue;
+      const uint64_t k = key_of(s, d);
+      if (present_.contains(k) || (banned_ && banned_->contains(k))) continue;
+      return k;
+    }
+  }
+
+ private:
+  void advance_ahead() {
+    const int32_t s = ahead_pick_(ahead_);
+    const int32_t d = ahead_pick_(ahead_);
+    present_.prefetch(key_of(s, d));
+  }
+  std::uniform_int_distribution<int32_t> pick_, ahead_pick_;
+  std::mt19937_64& rng_;
+  std::mt19937_64 ahead_;
+  const EdgeSet& present_;
+  const EdgeSet* banned_;
+};
+
+// std::shuffle, bit-exact with libstdc++'s algorithm (stl_algo.h: for a range
+// n with n*n <= the generator range, positions for two successive elements
+// come from one draw, x in [0, b0*b1) -> (x / b1, x % b1); for even n the
+// first swap is drawn alone from {0, 1}). The positions of a block of swaps
+// are drawn first and the swaps then applied in order with the random slots
+// prefetched — same draws, same swap order, a fraction of the miss latency.
+template <class T>
+void shuffle_exact(std::vector<T>& v, std::mt19937_64& g) {
+#if defined(__GLIBCXX__)
+  using uc = unsigned long;
+  static_assert(std::is_same_v<std::mt19937_64::result_type, uc>, "generator width");
+  const size_t n = v.size();
+  if (n == 0) return;
+  const uc urngrange = g.max() - g.min();
+  const uc urange = n;
+  if (urngrange / urange < urange) {
+    std::shuffle(v.begin(), v.end(), g);
+    return;
+  }
+  size_t i = 1;
+  if (urange % 2 == 0) {
+    std::uniform_int_distribution<uc> d{0, 1};
+    std::swap(v[i], v[d(g)]);
+    ++i;
+  }
+  constexpr size_t kBlock = 8192, kDist = 32;
+  static thread_local std::vector<uc> pos(kBlock);
+  while (i < n) {
+    size_t cnt = 0;
+    for (size_t j = i; j < n && cnt < kBlock; j += 2) {
+      const uc r = static_cast<uc>(j) + 1;  // swap range of element j: [0, j]
+      const uc x = std::uniform_int_distribution<uc>{0, r * (r + 1) - 1}(g);
+      pos[cnt++] = x / (r + 1);
+      pos[cnt++] = x % (r + 1);
+    }
+    for (size_t k = 0; k < cnt; ++k) {
+      if (k + kDist < cnt) __builtin_prefetch(&v[pos[k + kDist]], 1);
+      std::swap(v[i + k], v[pos[k]]);
+    }
+    i += cnt;
+  }
+#else
+  std::shuffle(v.begin(), v.end(), g);
+#endif
 }
 
 }  // namespace
@@ -109,10 +181,13 @@ CompactGraph synthesize_compact(const SynthParams& p) {
   EdgeSet edges(static_cast<size_t>(target) + 16);
   std::vector<uint64_t> sorted;
   sorted.reserve(target);
-  while (static_cast<int64_t>(edges.size()) < target) {
-    const uint64_t k = random_non_edge(p.num_nodes, edges, nullptr, rng);
-    edges.insert(k);
-    sorted.push_back(k);
+  {
+    NonEdgeSampler sampler(p.num_nodes, rng, edges, nullptr);
+    while (static_cast<int64_t>(edges.size()) < target) {
+      const uint64_t k = sampler.next();
+      edges.insert(k);
+      sorted.push_back(k);
+    }
   }
   std::sort(sorted.begin(), sorted.end());
   const int64_t nd = static_cast<int64_t>(p.num_nodes) * p.feature_dim;
@@ -139,7 +214,7 @@ CompactGraph synthesize_compact(const SynthParams& p) {
     const int64_t n_del = changes / 2;
     const int64_t n_ins = changes - n_del;
     pool = sorted;
-    std::shuffle(pool.begin(), pool.end(), rng);
+    shuffle_exact(pool, rng);
     const int64_t take = std::min<int64_t>(n_del, static_cast<int64_t>(pool.size()));
     std::vector<uint64_t> removed(pool.begin(), pool.begin() + take);
     std::sort(removed.begin(), removed.end());
@@ -150,15 +225,18 @@ CompactGraph synthesize_compact(const SynthParams& p) {
     }
     std::vector<uint64_t> inserted;
     inserted.reserve(n_ins);
-    for (int64_t i = 0; i < n_ins; ++i) {
-      const uint64_t k = random_non_edge(p.num_nodes, edges, &banned, rng);
-      edges.insert(k);
-      inserted.push_back(k);
+    if (n_ins > 0) {
+      NonEdgeSampler sampler(p.num_nodes, rng, edges, &banned);
+      for (int64_t i = 0; i < n_ins; ++i) {
+        const uint64_t k = sampler.next();
+        edges.insert(k);
+        inserted.push_back(k);
+      }
     }
     std::sort(inserted.begin(), inserted.end());
     const auto n_feat = static_cast<int32_t>(std::ceil(feat_ratio * static_cast<double>(p.num_nodes)));
     std::iota(nodes.begin(), nodes.end(), 0);
-    std::shuffle(nodes.begin(), nodes.end(), rng);
+    shuffle_exact(nodes, rng);
     std::uniform_real_distribution<double> unit(-1.0, 1.0);
     for (int32_t i = 0; i < n_feat; ++i) {
       double* row = feats.data() + static_cast<int64_t>(nodes[i]) * p.feature_dim;

@@ -72,6 +72,7 @@ Worker::Worker(const DeviceGraph& graph, DgnnModel& model, const TrainConfig& cf
   provider_ = std::make_unique<AggProvider>(store_.get(), &graph, model.cfg_.aggr, cfg.incremental,
                                             inc, stream);
   loss_ws_ = cuda::DevArray<double>(512, stream);
+  model.set_gate_recompute(gate_recompute_policy(model.cfg_, graph.num_nodes()));
   // Layer lanes for multi-layer integrated models (opt-in: DGNN_LAYER_STREAMS=1).
   // Measured at C3 they lose ~7% to the single lane — both lanes are HBM-bound
   // and the part is power-capped, so overlap only adds L2 contention. The
@@ -94,7 +95,8 @@ Worker::~Worker() {
 
 void Worker::run_sample(const SequenceWindow& window, Timestep windows_remaining, int64_t batch_id,
                         std::pair<NodeId, NodeId> node_range, float* grad, double* loss_slot) {
-  SeqSample sample = build_sample(graph_, model_.cfg_, window, windows_remaining, batch_id, node_range);
+  SeqSample sample =
+      build_sample(graph_, model_.cfg_, window, windows_remaining, batch_id, node_range, stream_);
   Lanes lanes(stream_, aux_);
   ForwardArtifacts fwd = model_forward(model_, sample, *provider_, lanes);
   std::vector<Buf> dpred = seed_loss(sample, fwd, model_.cfg_.feature_dim, loss_slot, loss_ws_.get(),

@@ -78,7 +78,17 @@ __global__ void k_pack_b(const float* __restrict__ M, int ld, int trans, int n0,
 }
 
 // ------------------------------------------------------------- row GEMM
-enum { kEpiLstm = 0, kEpiGru = 1, kEpiStore2 = 2 };
+// kEpiLstmBwd / kEpiGruBwd recompute the forward gates from the same operands
+// (bit-identical to the forward epilogue: same MMA order, same math) and
+// apply the pointwise cell backward (ref src/cells.cpp:134-166) in place of a
+// gates tape: the forward then stores only its state, the backward reads
+// X | Hm instead of the 4H-wide gates (+ c).
+enum { kEpiLstm = 0, kEpiGru = 1, kEpiStore2 = 2, kEpiLstmBwd = 3, kEpiGruBwd = 4 };
+
+template <int EPI>
+constexpr bool kEpiCell = EPI == kEpiLstm || EPI == kEpiGru || EPI == kEpiLstmBwd || EPI == kEpiGruBwd;
+template <int EPI>
+constexpr bool kEpiLstmLike = EPI == kEpiLstm || EPI == kEpiLstmBwd;
 
 struct RowGemmArgs {
   int M, k1, k2, K, nchunks;
@@ -90,9 +100,15 @@ struct RowGemmArgs {
   const float* bias;
   const float* c_prev;
   const float* h_skip;
-  float* gates;
+  float* gates;  // may be null (recompute mode: no gates tape)
   float* c_out;
   float* h_out;
+  // backward cell epilogue: upstream dh (dc), outputs G (n x 4H) and
+  // dstate = dc_prev (LSTM) / dh_skip (GRU)
+  const float* dh;
+  const float* dc;
+  float* G;
+  float* dstate;
   // store2 epilogue
   int n1, n2;
   float* C1;
@@ -165,7 +181,7 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
     fence_barrier_init();
   }
   float* sbias = reinterpret_cast<float*>(smem + S::kBias);
-  if ((EPI == kEpiLstm || EPI == kEpiGru) && tid < 4 * p.H) sbias[tid] = p.bias[tid];
+  if (kEpiCell<EPI> && tid < 4 * p.H) sbias[tid] = p.bias[tid];
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
@@ -310,24 +326,88 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
         }
         __syncwarp();
       };
-      if (EPI == kEpiLstm || EPI == kEpiGru) {
+      auto load16 = [&](const float* base, int j0, float (&v)[16]) {
+        if (base != nullptr && row < p.M) {
+          const float* sp = base + row * p.H + j0;
+#pragma unroll
+          for (int u = 0; u < 16; u += 4) {
+            const float4 x = __ldg(reinterpret_cast<const float4*>(sp + u));
+            v[u] = x.x; v[u + 1] = x.y; v[u + 2] = x.z; v[u + 3] = x.w;
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < 16; ++u) v[u] = 0.f;
+        }
+      };
+      if (EPI == kEpiLstmBwd || EPI == kEpiGruBwd) {
+        const int H = p.H;
+        const int U = H / 2;
+        for (int j0 = half * U; j0 < (half + 1) * U; j0 += 16) {
+          float a0[16], a1[16], a2[16], a3[16];
+          float cv[16];  // out: dc_prev (LSTM) / dh_skip (GRU)
+          tmem_ld16(trow + 0 * H + j0, a0);
+          tmem_ld16(trow + 1 * H + j0, a1);
+          tmem_ld16(trow + 2 * H + j0, a2);
+          tmem_ld16(trow + 3 * H + j0, a3);
+          tmem_wait_ld();
+          // per-row operands 4 columns at a time (register budget of 152)
+          const float* sp = (EPI == kEpiLstmBwd ? p.c_prev : p.h_skip) + row * H + j0;
+          const float* dp = p.dh + row * H + j0;
+          const float* cp = p.dc ? p.dc + row * H + j0 : nullptr;
+#pragma unroll
+          for (int u4 = 0; u4 < 16; u4 += 4) {
+            float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f), d4 = s4, c4 = s4;
+            if (row < p.M) {
+              s4 = __ldg(reinterpret_cast<const float4*>(sp + u4));
+              d4 = __ldg(reinterpret_cast<const float4*>(dp + u4));
+              if (EPI == kEpiLstmBwd && cp) c4 = __ldg(reinterpret_cast<const float4*>(cp + u4));
+            }
+            const float sv[4] = {s4.x, s4.y, s4.z, s4.w};
+            const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
+            const float ci[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int u = u4 + e;
+              const int j = j0 + u;
+              const float d = dv[e];
+              if (EPI == kEpiLstmBwd) {
+                const float ig = sigm(a0[u] + sbias[j]), fg = sigm(a1[u] + sbias[H + j]);
+                const float gg = ftanh(a2[u] + sbias[2 * H + j]);
+                const float og = sigm(a3[u] + sbias[3 * H + j]);
+                const float tc = ftanh(fg * sv[e] + ig * gg);
+                const float dct = (1.f - tc * tc) * (d * og) + ci[e];
+                a0[u] = ig * (1.f - ig) * (dct * gg);
+                a1[u] = fg * (1.f - fg) * (dct * sv[e]);
+                a2[u] = (1.f - gg * gg) * (dct * ig);
+                a3[u] = og * (1.f - og) * (d * tc);
+                cv[u] = dct * fg;
+              } else {
+                const float rr = sigm(a0[u] + sbias[j]), zz = sigm(a1[u] + sbias[H + j]);
+                const float hn = a3[u];
+                const float nn = ftanh(a2[u] + rr * hn + sbias[2 * H + j]);
+                const float dpre_n = (1.f - nn * nn) * (d * (1.f - zz));
+                a0[u] = rr * (1.f - rr) * (dpre_n * hn);
+                a1[u] = zz * (1.f - zz) * (d * (sv[e] - nn));
+                a2[u] = dpre_n;
+                a3[u] = dpre_n * rr;
+                cv[u] = d * zz;
+              }
+            }
+          }
+          stage_store(a0, p.G, 4 * H, 0 * H + j0);
+          stage_store(a1, p.G, 4 * H, 1 * H + j0);
+          stage_store(a2, p.G, 4 * H, 2 * H + j0);
+          stage_store(a3, p.G, 4 * H, 3 * H + j0);
+          stage_store(cv, p.dstate, H, j0);
+        }
+      } else if (EPI == kEpiLstm || EPI == kEpiGru) {
         const int H = p.H;
         const int U = H / 2;
         for (int j0 = half * U; j0 < (half + 1) * U; j0 += 16) {
           float a0[16], a1[16], a2[16], a3[16];
           // state row prefetch overlaps the TMEM reads
           float sv[16];
-          if (row < p.M) {
-            const float* sp = (EPI == kEpiLstm ? p.c_prev : p.h_skip) + row * H + j0;
-#pragma unroll
-            for (int u = 0; u < 16; u += 4) {
-              const float4 x = __ldg(reinterpret_cast<const float4*>(sp + u));
-              sv[u] = x.x; sv[u + 1] = x.y; sv[u + 2] = x.z; sv[u + 3] = x.w;
-            }
-          } else {
-#pragma unroll
-            for (int u = 0; u < 16; ++u) sv[u] = 0.f;
-          }
+          load16(EPI == kEpiLstm ? p.c_prev : p.h_skip, j0, sv);
           tmem_ld16(trow + 0 * H + j0, a0);
           tmem_ld16(trow + 1 * H + j0, a1);
           tmem_ld16(trow + 2 * H + j0, a2);
@@ -361,10 +441,12 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
                 ho[u] = (1.f - zz) * nn + zz * sv[u];
               }
             }
-            stage_store(a0, p.gates, 4 * H, 0 * H + j0);
-            stage_store(a1, p.gates, 4 * H, 1 * H + j0);
-            stage_store(a2, p.gates, 4 * H, 2 * H + j0);
-            stage_store(a3, p.gates, 4 * H, 3 * H + j0);
+            if (p.gates != nullptr) {
+              stage_store(a0, p.gates, 4 * H, 0 * H + j0);
+              stage_store(a1, p.gates, 4 * H, 1 * H + j0);
+              stage_store(a2, p.gates, 4 * H, 2 * H + j0);
+              stage_store(a3, p.gates, 4 * H, 3 * H + j0);
+            }
             if (EPI == kEpiLstm) stage_store(co, p.c_out, H, j0);
             stage_store(ho, p.h_out, H, j0);
           }
@@ -672,6 +754,33 @@ void umma_cell_forward(bool lstm, int n, int in, int H, const float* X, const fl
   const int npad = umma_npad(4 * H);
   if (lstm) dispatch_row_gemm<kEpiLstm>(npad, a, stream);
   else dispatch_row_gemm<kEpiGru>(npad, a, stream);
+}
+
+void umma_cell_backward_recompute(bool lstm, int n, int in, int H, const float* X, const float* Hm,
+                                  const float* h_skip, const float* c_prev, const float* Bimg,
+                                  const float* bias, const float* dh, const float* dc, float* G,
+                                  float* dstate, cudaStream_t stream) {
+  RowGemmArgs a{};
+  a.M = n;
+  a.k1 = in;
+  a.k2 = H;
+  a.K = in + H;
+  a.nchunks = (a.K + kKC - 1) / kKC;
+  a.A1 = X;
+  a.A2 = Hm;
+  a.Bimg = Bimg;
+  a.H = H;
+  a.bias = bias;
+  a.c_prev = c_prev;
+  a.h_skip = h_skip;
+  a.dh = dh;
+  a.dc = dc;
+  a.G = G;
+  a.dstate = dstate;
+  a.debug = umma_debug_flags();
+  const int npad = umma_npad(4 * H);
+  if (lstm) dispatch_row_gemm<kEpiLstmBwd>(npad, a, stream);
+  else dispatch_row_gemm<kEpiGruBwd>(npad, a, stream);
 }
 
 void umma_gemm_store2(int n, int K, const float* A, const float* Bimg, int n1, int n2, float* C1,

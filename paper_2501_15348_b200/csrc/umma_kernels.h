@@ -26,6 +26,15 @@ void umma_cell_forward(bool lstm, int n, int in, int H, const float* X, const fl
                        const float* h_skip, const float* c_prev, const float* Bimg,
                        const float* bias, float* gates, float* c, float* h, cudaStream_t stream);
 
+// Gate recompute + pointwise cell backward (no gates tape): the same
+// contraction as umma_cell_forward, epilogue writes G (n x 4H, the gate
+// pre-activation gradients) and dstate = dc_prev (LSTM) / dh_skip (GRU).
+// dc may be null (zero upstream cell gradient).
+void umma_cell_backward_recompute(bool lstm, int n, int in, int H, const float* X, const float* Hm,
+                                  const float* h_skip, const float* c_prev, const float* Bimg,
+                                  const float* bias, const float* dh, const float* dc, float* G,
+                                  float* dstate, cudaStream_t stream);
+
 // [C1 | C2] = A (n x K) * B^T with B the packed (n1+n2) x K image.
 void umma_gemm_store2(int n, int K, const float* A, const float* Bimg, int n1, int n2, float* C1,
                       float* C2, cudaStream_t stream);

@@ -66,6 +66,23 @@ def test_graph_store_bitwise(pair):
         assert g.change_ratio(t) == g_ref.change_ratio(t)
 
 
+def test_feature_versions_under_two_slots(ref, api, monkeypatch):
+    """Versioned features with the HBM slot budget forced to 2: every version
+    (materialised from snapshot 0 / the nearest resident version plus the
+    exact row patches) equals the reference's snapshot features, in any
+    access order, and a training run on it matches the reference."""
+    monkeypatch.setenv("DGNN_FEATURE_BUDGET_GB", "1e-9")
+    g_ref, g = make_pair(ref, api, n=300, avg_degree=4, dim=8, T=12, edge=0.05, feat=0.3, seed=5)
+    for t in [11, 0, 5, 6, 2, 11, 3, 10, 1]:
+        assert np.abs(g.feats(t) - g_ref.feats(t)).max() < 1e-7, t
+    cfg_r = ref.RunCfg(arch="tgcn", hidden=16, epochs=1, cache_frac=0.5)
+    r = g_ref.run(cfg_r)
+    s = api.TrainSession(g, api.TrainConfig(arch="tgcn", hidden=16, cache_frac=0.5))
+    losses = s.run_epoch()["sample_losses"]
+    assert nrel(losses, r.losses) < 1e-4
+    assert np.array_equal(s.invocations(), r.invocations[:, 1:])
+
+
 def test_graph_store_rejects_like_reference(api):
     g = api.DynamicGraph(4, 2)
     f = np.zeros((4, 2), np.float32)
@@ -281,8 +298,11 @@ def test_sharded_epoch_emulated_ranks(ref, api, pair, workers):
 
 
 @pytest.mark.parametrize("arch", ARCHS)
-def test_sample_grads_tensor_core_cells(ref, api, pair, arch):
-    """hidden 64: the cell GEMMs run on the tcgen05 3xTF32 kernels."""
+@pytest.mark.parametrize("gate_tape", [False, True])
+def test_sample_grads_tensor_core_cells(ref, api, pair, monkeypatch, arch, gate_tape):
+    """hidden 64: the cell GEMMs run on the tcgen05 3xTF32 kernels, with the
+    gates recomputed in the fused backward (default) or read from a tape."""
+    monkeypatch.setenv("DGNN_GATE_TAPE", "1" if gate_tape else "0")
     g_ref, g = pair
     cfg_r = ref.RunCfg(arch=arch, hidden=64)
     s = api.TrainSession(g, api.TrainConfig(arch=arch, hidden=64))
@@ -292,6 +312,31 @@ def test_sample_grads_tensor_core_cells(ref, api, pair, arch):
         assert abs(loss - loss_r) <= 1e-5 * abs(loss_r), (loss, loss_r)
         assert nrel(pred, pred_r) < 1e-5
         assert nrel(grads, grads_r) < 1e-4
+
+
+@pytest.mark.parametrize("arch", ["gcrn_m2", "tgcn"])
+def test_layer_lanes_match_reference(ref, api, pair, monkeypatch, arch):
+    """Two-stream layer pipelining (DGNN_LAYER_STREAMS=1) computes exactly what
+    the single stream computes (same kernels, same per-buffer order; a race
+    would show as a bit difference), with the reference's invocation sequence
+    and cache trace."""
+    g_ref, g = pair
+    cfg_r = ref.RunCfg(arch=arch, hidden=64, epochs=2, cache_frac=0.5)
+    r = g_ref.run(cfg_r)
+
+    def run(lanes):
+        monkeypatch.setenv("DGNN_LAYER_STREAMS", "1" if lanes else "0")
+        s = api.TrainSession(g, api.TrainConfig(arch=arch, hidden=64, cache_frac=0.5, record_events=True))
+        losses = np.concatenate([s.run_epoch()["sample_losses"] for _ in range(2)])
+        return s, losses
+
+    s0, l0 = run(False)
+    s1, l1 = run(True)
+    assert np.array_equal(l0, l1)
+    assert np.array_equal(s0.params(), s1.params())
+    assert nrel(l1, r.losses) < 1e-3
+    assert np.array_equal(s1.invocations(), r.invocations[:, 1:])
+    _events_match(s1.cache_events(), r.events)
 
 
 def test_spmm_column_slices_match_reference(ref):

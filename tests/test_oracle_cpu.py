@@ -196,7 +196,10 @@ def test_product_synth_is_bit_exact_with_golden():
         assert np.array_equal(f, GOLD[f"feats_{t}"])
 
 
-@pytest.mark.parametrize("n,deg,dim,T,er,fr,seed", [(500, 6, 3, 6, 0.03, 0.0, 1), (257, 2.5, 5, 5, 0.2, 1.0, 4)])
+@pytest.mark.parametrize("n,deg,dim,T,er,fr,seed", [
+    (500, 6, 3, 6, 0.03, 0.0, 1), (257, 2.5, 5, 5, 0.2, 1.0, 4),
+    # edge pools of 60000 / 60005 keys: many prefetched shuffle blocks, even and odd n
+    (12000, 5, 2, 4, 0.05, 0.01, 2), (12001, 5, 2, 3, 0.05, 0.01, 3)])
 def test_product_synth_matches_reference(ref, n, deg, dim, T, er, fr, seed):
     from paper_2501_15348_b200 import api
     s = api.Synth(n, deg, dim, T, er, fr, seed=seed)
