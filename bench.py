@@ -261,6 +261,17 @@ def main():
     roofline = roof(dom)
     delta_roof = roof("agg_delta")
 
+    free_b, total_b = torch.cuda.mem_get_info()
+    st = sess.stats()
+    memory = {"hbm_in_use_gb": round((total_b - free_b) / 1e9, 1),
+              "graph_store_gb": round(graph.device_bytes() / 1e9, 1),
+              "feature_versions": graph.feature_stats(),
+              "cache": {k: st[k] for k in ("hits", "misses", "evictions", "expirations", "spills",
+                                           "refills", "resident_peak_units")}}
+    # the e2e leg builds its own graph + session: release the timed ones first (C4 is ~150 GB)
+    del sess, graph
+    torch.cuda.synchronize()
+
     # ---------------- end to end through the public API from host buffers
     e2e = None
     if not args.no_e2e:
@@ -316,10 +327,11 @@ def main():
                        "seq_len": L, "horizon": H, "nodes": wl["n"],
                        "edges": int(synth.sizes[0]), "snapshots": wl["T"],
                        "parallelism": f"window-shard x{world} (consecutive_block)",
-                       "l2": "inputs (features 16 GB, CSRs 5.6 GB) exceed the 126 MB L2"},
+                       "l2": f"inputs exceed the 126 MB L2 (graph store {memory['graph_store_gb']} GB; "
+                             f"one feature matrix {wl['n'] * wl['dim'] * 4 / 1e9:.2f} GB)"},
             "roofline": roofline, "roofline_delta_spmm": delta_roof,
             "kernel_ms_by_class": {k: round(v["ms"] / args.steps, 2) for k, v in prof.items()},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "memory": memory,
             "clocks": clocks.summary(), "epoch_loss": float(losses.mean()) if len(losses) else None,
             "setup_s": {"synth": round(t_synth, 1), "device_graph_build": round(t_build, 2)},
         }

@@ -56,6 +56,10 @@ int dgnn_graph_add_delta(dgnn_graph* g, const int32_t* del_src, const int32_t* d
                          const float* changed_feats);
 int32_t dgnn_graph_length(const dgnn_graph* g);
 int64_t dgnn_graph_num_edges(const dgnn_graph* g, int32_t t);
+/* HBM held by the graph store (CSRs, deltas, feature versions and patches);
+ * the feature-version slot budget and how many versions were materialised. */
+int64_t dgnn_graph_device_bytes(const dgnn_graph* g);
+int dgnn_graph_feature_stats(const dgnn_graph* g, int32_t* slots, int64_t* materialisations);
 /* Device pointers of snapshot t (GraphView, inc/snapshot.hpp:20-35, plus the out-CSR). */
 int dgnn_graph_snapshot(const dgnn_graph* g, int32_t t, const int64_t** in_ptr,
                         const int32_t** in_src, const int64_t** out_ptr, const int32_t** out_dst,

@@ -48,6 +48,8 @@ SIGNATURES = {
     "dgnn_graph_add_delta": (C.c_int, [P, P, P, I64, P, P, I64, P, I64, P]),
     "dgnn_graph_length": (I32, [P]),
     "dgnn_graph_num_edges": (I64, [P, I32]),
+    "dgnn_graph_device_bytes": (I64, [P]),
+    "dgnn_graph_feature_stats": (C.c_int, [P, C.POINTER(I32), C.POINTER(I64)]),
     "dgnn_graph_snapshot": (C.c_int, [P, I32, PP, PP, PP, PP, PP]),
     "dgnn_graph_delta_sizes": (C.c_int, [P, I32] + [C.POINTER(I64)] * 6),
     "dgnn_graph_delta_copy": (C.c_int, [P, I32, P, P, P, P, P]),

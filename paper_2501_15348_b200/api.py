@@ -205,6 +205,14 @@ class DynamicGraph:
     def length(self) -> int:
         return lib().dgnn_graph_length(self.h)
 
+    def device_bytes(self) -> int:
+        return lib().dgnn_graph_device_bytes(self.h)
+
+    def feature_stats(self) -> dict:
+        s, m = C.c_int32(), C.c_int64()
+        check(lib().dgnn_graph_feature_stats(self.h, C.byref(s), C.byref(m)))
+        return {"slots": s.value, "materialisations": m.value}
+
     def num_edges(self, t) -> int:
         n = lib().dgnn_graph_num_edges(self.h, t)
         if n < 0:

@@ -183,6 +183,22 @@ int64_t dgnn_graph_num_edges(const dgnn_graph* g, int32_t t) {
   }
 }
 
+int64_t dgnn_graph_device_bytes(const dgnn_graph* g) {
+  try {
+    return g->g->device_bytes();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+int dgnn_graph_feature_stats(const dgnn_graph* g, int32_t* slots, int64_t* materialisations) {
+  return guarded([&] {
+    if (slots) *slots = g->g->feature_slots();
+    if (materialisations) *materialisations = g->g->feature_materialisations();
+  });
+}
+
 int dgnn_graph_snapshot(const dgnn_graph* g, int32_t t, const int64_t** in_ptr,
                         const int32_t** in_src, const int64_t** out_ptr, const int32_t** out_dst,
                         const float** feats) {
