@@ -263,7 +263,10 @@ def main():
 
     free_b, total_b = torch.cuda.mem_get_info()
     st = sess.stats()
+    pool = api.mem_stats()
     memory = {"hbm_in_use_gb": round((total_b - free_b) / 1e9, 1),
+              "pool_used_high_gb": round(pool["used_high"] / 1e9, 1),
+              "pool_reserved_high_gb": round(pool["reserved_high"] / 1e9, 1),
               "graph_store_gb": round(graph.device_bytes() / 1e9, 1),
               "feature_versions": graph.feature_stats(),
               "cache": {k: st[k] for k in ("hits", "misses", "evictions", "expirations", "spills",

@@ -107,6 +107,12 @@ int dgnn_agg_delta(int32_t kind, int32_t n_rows, int32_t w, const int32_t* rows,
                    const int32_t* row_ptr, const int32_t* ent, const float* f_prev,
                    const float* f_curr, float* values, float* degree, float* mean_sums,
                    int32_t* argext, void* stream);
+/* K2 on the graph's own delta(t) (aggregate_incremental's update step,
+ * src/aggregate.cpp:170-205, without the fallback checks): values (and mean /
+ * extremal state) hold Agg_{t-1} of the graph features (w = feature_dim) and
+ * become Agg_t in place; uses the compact changed-row block. */
+int dgnn_graph_apply_delta(const dgnn_graph* g, int32_t t, int32_t kind, float* values,
+                           float* degree, float* mean_sums, int32_t* argext, void* stream);
 int dgnn_agg_backward(int32_t kind, int32_t n, int32_t w, const int64_t* out_ptr,
                       const int32_t* out_dst, const float* upstream, const float* degree,
                       const int32_t* argext, float* grad, void* stream);
@@ -234,10 +240,15 @@ int64_t dgnn_init_params(const dgnn_run_cfg* cfg, int32_t feature_dim, double* o
 /* ---------------------------------------------------------------- profiling
  * Device timing per kernel class (0 agg_scratch, 1 agg_delta, 2 agg_backward,
  * 3 cell_fwd, 4 cell_bwd (pointwise), 5 weight_grad, 6 other, 7 cell_bwd_gemm
- * (the dX | dHm contraction)) with algorithmic bytes. */
+ * (the dX | dHm contraction), 8 sample = one whole (window, batch) sample)
+ * with algorithmic bytes; dgnn_prof_get_max = the longest single scope. */
+/* Device memory pool (stream-ordered allocations of every buffer above):
+ * reserved / used bytes, current and high-water. */
+int dgnn_mem_stats(int64_t* reserved, int64_t* used, int64_t* reserved_high, int64_t* used_high);
 int dgnn_prof_enable(int32_t on);
 int dgnn_prof_reset(void);
 int dgnn_prof_get(int32_t cls, int64_t* launches, double* ms, double* bytes, double* flops);
+int dgnn_prof_get_max(int32_t cls, double* max_ms);
 
 #ifdef __cplusplus
 }

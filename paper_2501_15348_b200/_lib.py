@@ -63,6 +63,7 @@ SIGNATURES = {
     "dgnn_synth_to_graph": (C.c_int, [P, P, PP]),
     "dgnn_agg_scratch": (C.c_int, [I32, I32, I32, P, P, P, P, P, P, P, P]),
     "dgnn_agg_delta": (C.c_int, [I32, I32, I32, P, P, P, P, P, P, P, P, P, P]),
+    "dgnn_graph_apply_delta": (C.c_int, [P, I32, I32, P, P, P, P, P]),
     "dgnn_agg_backward": (C.c_int, [I32, I32, I32, P, P, P, P, P, P, P]),
     "dgnn_agg_incremental": (C.c_int, [P, I32, I32, P, P, P, P, I32, I64, D, I32, P, P, P, P, P]),
     "dgnn_pack_cell": (C.c_int, [I32, I32, I32, P, P, P, P]),
@@ -91,6 +92,8 @@ SIGNATURES = {
     "dgnn_key_hash": (U64, [I32, I32, I32, I32, I64, I64]),
     "dgnn_make_batches": (I64, [I32, I32, U64, I64, P, I64]),
     "dgnn_init_params": (I64, [C.POINTER(RunCfg), I32, P]),
+    "dgnn_mem_stats": (C.c_int, [C.POINTER(I64)] * 4),
+    "dgnn_prof_get_max": (C.c_int, [I32, C.POINTER(D)]),
     "dgnn_prof_enable": (C.c_int, [I32]),
     "dgnn_prof_reset": (C.c_int, []),
     "dgnn_prof_get": (C.c_int, [I32, C.POINTER(I64), C.POINTER(D), C.POINTER(D), C.POINTER(D)]),

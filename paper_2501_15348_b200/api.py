@@ -313,6 +313,16 @@ def aggregate_delta_inplace(graph: DynamicGraph, t: int, agg: dict, f_prev, f_cu
     return agg
 
 
+def apply_graph_delta(graph: DynamicGraph, t: int, agg: dict, kind="sum", stream=None):
+    """K2 on the graph's own delta(t) and feature versions (compact changed-row
+    block): agg holds Agg_{t-1} of the graph features and becomes Agg_t."""
+    check(lib().dgnn_graph_apply_delta(graph.h, t, AGGR[kind], _ptr(agg["values"]),
+                                       _ptr(agg.get("degree")), _ptr(agg.get("mean_sums")),
+                                       _ptr(agg.get("argext")),
+                                       _stream_handle(stream or current_stream())))
+    return agg
+
+
 def aggregate_incremental(graph: DynamicGraph, t: int, prev: dict, kind="sum", prev_depth=0,
                           prev_num_edges=None, fallback_threshold=0.5, rescratch_period=64):
     """aggregate_incremental with the reference's fallback logic (src/aggregate.cpp:117-207)."""
@@ -547,6 +557,15 @@ class TrainSession:
 # ------------------------------------------------------------------ profiling
 PROF_CLASSES = ["agg_scratch", "agg_delta", "agg_backward", "cell_fwd", "cell_bwd",
                 "weight_grad", "other", "cell_bwd_gemm"]
+# non-kernel scopes (not part of kernel-time sums)
+PROF_SCOPES = ["sample", "sample_host"]
+
+
+def mem_stats() -> dict:
+    """Device pool occupancy in bytes (reserved / used, current and high-water)."""
+    v = [C.c_int64() for _ in range(4)]
+    check(lib().dgnn_mem_stats(*[C.byref(x) for x in v]))
+    return dict(zip(["reserved", "used", "reserved_high", "used_high"], [x.value for x in v]))
 
 
 def prof_enable(on=True):
@@ -557,10 +576,16 @@ def prof_reset():
     check(lib().dgnn_prof_reset())
 
 
-def prof_get() -> dict:
+def prof_get(scopes=False) -> dict:
+    """Per kernel class: launches, device ms, algorithmic bytes / flops, longest
+    launch. scopes=True returns the non-kernel scopes (whole samples) instead."""
     out = {}
-    for i, name in enumerate(PROF_CLASSES):
-        n, ms, b, f = C.c_int64(), C.c_double(), C.c_double(), C.c_double()
-        check(lib().dgnn_prof_get(i, C.byref(n), C.byref(ms), C.byref(b), C.byref(f)))
-        out[name] = {"launches": n.value, "ms": ms.value, "bytes": b.value, "flops": f.value}
+    names = PROF_SCOPES if scopes else PROF_CLASSES
+    base = len(PROF_CLASSES) if scopes else 0
+    for i, name in enumerate(names):
+        n, ms, b, f, mx = C.c_int64(), C.c_double(), C.c_double(), C.c_double(), C.c_double()
+        check(lib().dgnn_prof_get(base + i, C.byref(n), C.byref(ms), C.byref(b), C.byref(f)))
+        check(lib().dgnn_prof_get_max(base + i, C.byref(mx)))
+        out[name] = {"launches": n.value, "ms": ms.value, "bytes": b.value, "flops": f.value,
+                     "max_ms": mx.value}
     return out

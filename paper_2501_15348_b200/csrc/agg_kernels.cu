@@ -17,6 +17,8 @@
 #include "common.cuh"
 
 #include <cfloat>
+#include <cstdint>
+#include <cstdlib>
 
 namespace dgnn {
 namespace cuda {
@@ -258,6 +260,137 @@ k_agg_delta(int n_rows, int w, const int32_t* __restrict__ rows, const int32_t* 
   }
 }
 
+// L2 eviction-priority policies for the delta gathers: the compact
+// changed-row block is re-read ~20x (every out-edge of a changed node appears
+// in G- and G+) and is kept (evict_last); destination rows and structural
+// source rows are touched once (evict_first).
+__device__ __forceinline__ uint64_t l2_policy_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float4 ld_nc_hint(const float* p, uint64_t pol) {
+  float4 r;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ float4 ld_hint(const float* p, uint64_t pol) {
+  float4 r;
+  asm volatile("ld.global.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+
+// K2, pipelined (sum / mean, w <= 128, 16 B-aligned rows). One destination
+// row per group of G lanes (4 columns per lane), 32 / G rows per warp step.
+// The dependent index chain (row meta -> entries -> source rows) is software
+// pipelined across steps: each step issues the row metadata two steps ahead
+// and the first G entries one step ahead together with this step's
+// destination-row and source-row loads, so a step costs one memory round trip
+// instead of three. Entries are applied in the reference's order (deletions,
+// then insertions, ascending source), exactly as in k_agg_delta.
+template <int G, bool MEAN>
+__global__ void __launch_bounds__(kThreads)
+k_agg_delta_v4(int n_rows, int w, int32_t num_nodes, const int32_t* __restrict__ rows,
+               const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ ent,
+               const float* __restrict__ Fp, const float* __restrict__ Fc,
+               const float* __restrict__ Cp, const float* __restrict__ Cc,
+               float* __restrict__ values, float* __restrict__ degree, float* __restrict__ msum) {
+  constexpr int R = 32 / G;
+  const int lane = threadIdx.x & 31, gl = lane & (G - 1), sub = lane / G;
+  const int64_t wg = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+  const int64_t step = ((static_cast<int64_t>(gridDim.x) * kThreads) >> 5) * R;
+  const int c = gl * 4;
+  const bool cact = c < w;
+  const uint64_t keep = l2_policy_last(), once = l2_policy_first();
+  struct Meta {
+    int32_t v, beg, cnt;
+  };
+  auto meta = [&](int64_t rb) {
+    Meta m{0, 0, 0};
+    const int64_t r = rb + sub;
+    if (r < n_rows) {
+      m.v = rows[r];
+      m.beg = row_ptr[r];
+      m.cnt = row_ptr[r + 1] - m.beg;
+    }
+    return m;
+  };
+  auto first_ent = [&](const Meta& m) { return gl < m.cnt ? ent[m.beg + gl] : 0; };
+  int64_t rb = wg * R;
+  Meta m0 = meta(rb), m1 = meta(rb + step);
+  int32_t e0 = first_ent(m0);
+  float d0 = MEAN && rb + sub < n_rows ? degree[m0.v] : 0.f;
+  for (; rb < n_rows; rb += step) {
+    const Meta m2 = meta(rb + 2 * step);
+    const int32_t e1 = first_ent(m1);
+    const float d1 = MEAN && rb + step + sub < n_rows ? degree[m1.v] : 0.f;
+    const bool valid = rb + sub < n_rows;
+    float* accp = (MEAN ? msum : values) + static_cast<int64_t>(m0.v) * w + c;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (valid && cact) acc = ld_hint(accp, once);
+    const int maxcnt = __reduce_max_sync(0xffffffffu, m0.cnt);
+    int dnet = 0;
+    for (int eb = 0; eb < maxcnt; eb += G) {
+      const int32_t my_s = eb == 0 ? e0 : (eb + gl < m0.cnt ? ent[m0.beg + eb + gl] : 0);
+      const int cnt = min(G, maxcnt - eb);
+      for (int j0 = 0; j0 < cnt; j0 += kUnroll) {
+        float4 x[kUnroll];
+        int32_t s[kUnroll];
+#pragma unroll
+        for (int q = 0; q < kUnroll; ++q) {
+          s[q] = __shfl_sync(0xffffffffu, my_s, (j0 + q) & (G - 1), G);
+          if (valid && cact && j0 + q < cnt && eb + j0 + q < m0.cnt) {
+            const int32_t u = s[q] < 0 ? ~s[q] : s[q];
+            if (u >= num_nodes) {
+              x[q] = ld_nc_hint((s[q] < 0 ? Cp : Cc) + static_cast<int64_t>(u - num_nodes) * w + c, keep);
+            } else {
+              x[q] = ld_nc_hint((s[q] < 0 ? Fp : Fc) + static_cast<int64_t>(u) * w + c, once);
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kUnroll; ++q) {
+          if (!(valid && j0 + q < cnt && eb + j0 + q < m0.cnt)) continue;
+          if (MEAN) dnet += s[q] < 0 ? -1 : 1;
+          if (!cact) continue;
+          if (s[q] < 0) {
+            acc.x -= x[q].x; acc.y -= x[q].y; acc.z -= x[q].z; acc.w -= x[q].w;
+          } else {
+            acc.x += x[q].x; acc.y += x[q].y; acc.z += x[q].z; acc.w += x[q].w;
+          }
+        }
+      }
+    }
+    if (valid && cact) {
+      if (MEAN) {
+        // renormalise the touched row (ref src/aggregate.cpp:195-205)
+        const float dg = d0 + static_cast<float>(dnet);
+        const bool live = dg > 1e-12f;
+        const float4 ms = live ? acc : make_float4(0.f, 0.f, 0.f, 0.f);
+        *reinterpret_cast<float4*>(accp) = ms;
+        *reinterpret_cast<float4*>(values + static_cast<int64_t>(m0.v) * w + c) =
+            live ? make_float4(acc.x / dg, acc.y / dg, acc.z / dg, acc.w / dg) : ms;
+        if (gl == 0) degree[m0.v] = live ? dg : 0.f;
+      } else {
+        *reinterpret_cast<float4*>(accp) = acc;
+      }
+    }
+    m0 = m1;
+    m1 = m2;
+    e0 = e1;
+    d0 = d1;
+  }
+}
+
 // Deleted-contributor test for max/min (ref src/aggregate.cpp:145-153).
 __global__ void k_deleted_contributor(int64_t n_del, int w, const uint64_t* __restrict__ del_keys,
                                       const int32_t* __restrict__ argext, int32_t* flag) {
@@ -438,9 +571,35 @@ void agg_scratch(int kind, int n, int w, const int64_t* in_ptr, const int32_t* i
 
 void agg_delta(int kind, int n_rows, int w, const int32_t* rows, const int32_t* row_ptr,
                const int32_t* ent, const float* f_prev, const float* f_curr, float* values,
-               float* degree, float* mean_sums, int32_t* argext, cudaStream_t stream) {
+               float* degree, float* mean_sums, int32_t* argext, cudaStream_t stream,
+               const int32_t* ent_c, int32_t num_nodes, int64_t n_changed, const float* compact) {
   if (n_rows <= 0 || w <= 0) return;
   const int vec = pick_vec(w, f_prev, values);
+  const bool aligned = pick_vec(w, f_curr, mean_sums) == 4 && pick_vec(w, compact, nullptr) == 4;
+  static const bool pipe_off = [] {
+    const char* e = std::getenv("DGNN_DELTA_PIPE");
+    return e && e[0] == '0';
+  }();
+  if (ent_c == nullptr) {  // no compact block: every source is a full-matrix row
+    ent_c = ent;
+    num_nodes = INT32_MAX;
+  }
+  if (!pipe_off && (kind == kAggSum || kind == kAggMean) && vec == 4 && aligned && w <= 128) {
+    const int g = pick_group(w, 4);
+    const int grid = rows_grid(n_rows, g);
+    const float* cp = compact;
+    const float* cc = compact ? compact + n_changed * w : nullptr;
+    if (kind == kAggMean) {
+      DGNN_DISPATCH_G(g, DGNN_LAUNCH((k_agg_delta_v4<G, true>), grid, kThreads, 0, stream, n_rows, w,
+                                     num_nodes, rows, row_ptr, ent_c, f_prev, f_curr, cp, cc, values,
+                                     degree, mean_sums));
+    } else {
+      DGNN_DISPATCH_G(g, DGNN_LAUNCH((k_agg_delta_v4<G, false>), grid, kThreads, 0, stream, n_rows, w,
+                                     num_nodes, rows, row_ptr, ent_c, f_prev, f_curr, cp, cc, values,
+                                     degree, mean_sums));
+    }
+    return;
+  }
   const int g = pick_group(w, vec);
   const int grid = rows_grid(n_rows, g);
   DGNN_DISPATCH_KIND(kind, DGNN_DISPATCH_V(vec, DGNN_DISPATCH_G(g,

@@ -23,9 +23,15 @@ void agg_scratch(int kind, int n, int w, const int64_t* in_ptr, const int32_t* i
 // are deletions (~src, gathered from f_prev) then insertions (src, from f_curr).
 // sum: values +=/-=; mean: mean_sums and degree updated, values renormalised;
 // max/min: insertions only (deleted contributors must have been ruled out).
+// With ent_c (sum / mean, 128-bit aligned rows, w <= 128) the pipelined
+// kernel reads sources >= num_nodes from the compact changed-row block:
+// deletions from compact[(s - N) * w], insertions from compact[(n_changed +
+// s - N) * w] — the same values, so the same results.
 void agg_delta(int kind, int n_rows, int w, const int32_t* rows, const int32_t* row_ptr,
                const int32_t* ent, const float* f_prev, const float* f_curr, float* values,
-               float* degree, float* mean_sums, int32_t* argext, cudaStream_t stream);
+               float* degree, float* mean_sums, int32_t* argext, cudaStream_t stream,
+               const int32_t* ent_c = nullptr, int32_t num_nodes = 0, int64_t n_changed = 0,
+               const float* compact = nullptr);
 
 // flag |= 1 if any deleted edge (sorted src << 32 | dst keys) is a recorded
 // max/min contributor.

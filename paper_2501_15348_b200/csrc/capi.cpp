@@ -369,6 +369,20 @@ int dgnn_agg_delta(int32_t kind, int32_t n_rows, int32_t w, const int32_t* rows,
   });
 }
 
+int dgnn_graph_apply_delta(const dgnn_graph* g, int32_t t, int32_t kind, float* values,
+                           float* degree, float* mean_sums, int32_t* argext, void* stream) {
+  return guarded([&] {
+    check(kind >= 0 && kind <= 3, "unknown aggregation kind");
+    const DeviceGraph& G = *g->g;
+    const DevDelta& dd = G.delta(t);
+    cudaStream_t st = as_stream(stream);
+    FeatRef fp = G.features(t - 1, st), fc = G.features(t, st);
+    cuda::agg_delta(kind, dd.n_rows, G.feature_dim(), dd.rows.get(), dd.row_ptr.get(), dd.ent.get(),
+                    fp->get(), fc->get(), values, degree, mean_sums, argext, st, dd.ent_c.get(),
+                    G.num_nodes(), dd.n_changed, dd.compact.get());
+  });
+}
+
 int dgnn_agg_backward(int32_t kind, int32_t n, int32_t w, const int64_t* out_ptr,
                       const int32_t* out_dst, const float* upstream, const float* degree,
                       const int32_t* argext, float* grad, void* stream) {
@@ -827,6 +841,9 @@ int64_t dgnn_init_params(const dgnn_run_cfg* cfg, int32_t feature_dim, double* o
 }
 
 // ---------------------------------------------------------------- profiling
+int dgnn_mem_stats(int64_t* reserved, int64_t* used, int64_t* reserved_high, int64_t* used_high) {
+  return guarded([&] { cuda::pool_stats(reserved, used, reserved_high, used_high); });
+}
 int dgnn_prof_enable(int32_t on) {
   return guarded([&] { prof_enable(on != 0); });
 }
@@ -841,6 +858,13 @@ int dgnn_prof_get(int32_t cls, int64_t* launches, double* ms, double* bytes, dou
     if (ms) *ms = p.ms;
     if (bytes) *bytes = p.bytes;
     if (flops) *flops = p.flops;
+  });
+}
+
+int dgnn_prof_get_max(int32_t cls, double* max_ms) {
+  return guarded([&] {
+    prof_flush();
+    if (max_ms) *max_ms = prof_get(cls).max_ms;
   });
 }
 

@@ -159,6 +159,26 @@ __global__ void k_gather_rows(int64_t m, int32_t d, const int32_t* __restrict__ 
   }
 }
 
+// ent_c[i] = ent[i] with a source found in `changed` (ascending) replaced by
+// N + its position, keeping the deletion (~) / insertion encoding
+__global__ void k_remap_compact(int64_t m, const int32_t* __restrict__ ent, int64_t n_changed,
+                                const int32_t* __restrict__ changed, int32_t num_nodes,
+                                int32_t* __restrict__ ent_c) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t e = ent[i];
+    const int32_t s = e < 0 ? ~e : e;
+    int64_t lo = 0, hi = n_changed;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (changed[mid] < s) lo = mid + 1; else hi = mid;
+    }
+    int32_t r = s;
+    if (lo < n_changed && changed[lo] == s) r = num_nodes + static_cast<int32_t>(lo);
+    ent_c[i] = e < 0 ? ~r : r;
+  }
+}
+
 int grid_for(int64_t n) { return cuda::wave_grid(n, kT, 8); }
 
 // Thin CUB wrappers with a growable temp buffer.
@@ -345,7 +365,7 @@ FeatRef DeviceGraph::features(int32_t t, cudaStream_t stream) const {
       const DevDelta& dd = deltas_[k];
       if (dd.n_changed > 0)
         DGNN_LAUNCH(k_scatter_rows, grid_for(dd.n_changed * d_), kT, 0, stream, dd.n_changed, d_,
-                    dd.changed.get(), patch_rows_[k].get(), hit->buf.get());
+                    dd.changed.get(), dd.compact.get() + dd.n_changed * d_, hit->buf.get());
     }
     hit->t = t;
     hit->writer = stream;
@@ -373,8 +393,8 @@ int64_t DeviceGraph::device_bytes() const {
   for (const auto& s : snaps_)
     b += s.in_ptr.bytes() + s.out_ptr.bytes() + s.in_src.bytes() + s.out_dst.bytes();
   for (const auto& d : deltas_)
-    b += d.del.bytes() + d.ins.bytes() + d.changed.bytes() + d.rows.bytes() + d.row_ptr.bytes() + d.ent.bytes();
-  for (const auto& p : patch_rows_) b += p.bytes();
+    b += d.del.bytes() + d.ins.bytes() + d.changed.bytes() + d.rows.bytes() + d.row_ptr.bytes() +
+         d.ent.bytes() + d.ent_c.bytes() + d.compact.bytes();
   for (const auto& s : slots_) b += s->buf.bytes();
   return b;
 }
@@ -487,7 +507,6 @@ void DeviceGraph::finish_snapshot(DevArray<uint64_t> keys, const float* prev_fea
   cub.exclusive_sum(reinterpret_cast<const int64_t*>(cnt.get()), s.in_ptr.get(), n_ + 1);
   snaps_.push_back(std::move(s));
   deltas_.emplace_back();
-  patch_rows_.emplace_back();
   prev_keys_ = std::move(curr_keys_);
   curr_keys_ = std::move(keys);
   if (snaps_.size() >= 2) build_delta(static_cast<int32_t>(snaps_.size()) - 1, prev_feats, feats);
@@ -513,10 +532,12 @@ void DeviceGraph::build_delta(int32_t t, const float* prev_feats, const float* f
   if (dd.n_changed) {
     DGNN_CUDA(cudaMemcpyAsync(dd.changed.get(), changed.get(), sizeof(int32_t) * dd.n_changed,
                               cudaMemcpyDeviceToDevice, st));
-    // the version patch: changed rows at t
-    patch_rows_[t] = DevArray<float>(dd.n_changed * d_, st);
+    // [F_{t-1}[changed] | F_t[changed]]; the second half is the version patch of t
+    dd.compact = DevArray<float>(2 * dd.n_changed * d_, st);
     DGNN_LAUNCH(k_gather_rows, grid_for(dd.n_changed * d_), kT, 0, st, dd.n_changed, d_,
-                dd.changed.get(), feats, patch_rows_[t].get());
+                dd.changed.get(), prev_feats, dd.compact.get());
+    DGNN_LAUNCH(k_gather_rows, grid_for(dd.n_changed * d_), kT, 0, st, dd.n_changed, d_,
+                dd.changed.get(), feats, dd.compact.get() + dd.n_changed * d_);
   }
   // expansion sizes
   auto expansion = [&](const DevSnapshot& S, int64_t* total) {
@@ -586,6 +607,11 @@ void DeviceGraph::build_delta(int32_t t, const float* prev_feats, const float* f
     DGNN_CUDA(cudaMemsetAsync(counts.get() + nr, 0, sizeof(int32_t), st));
   }
   cub.exclusive_sum(counts.get(), dd.row_ptr.get(), nr + 1);
+  // sources re-indexed into the compact changed-row block
+  dd.ent_c = DevArray<int32_t>(ne, st);
+  if (ne)
+    DGNN_LAUNCH(k_remap_compact, grid_for(ne), kT, 0, st, ne, dd.ent.get(), dd.n_changed,
+                dd.changed.get(), n_, dd.ent_c.get());
   DGNN_CUDA(cudaStreamSynchronize(st));
   deltas_[t] = std::move(dd);
 }

@@ -75,6 +75,14 @@ struct DevDelta {
   int32_t n_rows = 0;
   int64_t n_ent = 0;
   cuda::DevArray<int32_t> rows, row_ptr, ent;
+  // Feature-changed sources, compacted: compact = [F_{t-1}[changed] |
+  // F_t[changed]] (2 x n_changed x d; the second half is also the version
+  // patch of t), and ent_c = ent with every source in `changed` re-indexed to
+  // N + (its position in changed). A changed node contributes all its
+  // out-edges to both G- and G+, so ~2/3 of the delta's gathers at C4 hit this
+  // small L2-resident block instead of random rows of two 2 GB matrices.
+  cuda::DevArray<int32_t> ent_c;
+  cuda::DevArray<float> compact;
   // distinct deletion / insertion sources (algorithmic-byte accounting)
   int64_t u_minus = 0, u_plus = 0;
   int64_t change_count() const { return n_del + n_ins; }
@@ -125,8 +133,7 @@ class DeviceGraph {
   std::vector<DevSnapshot> snaps_;
   std::vector<DevDelta> deltas_;  // deltas_[t], t >= 1; deltas_[0] unused
   cuda::DevArray<uint64_t> prev_keys_, curr_keys_;  // sorted (src,dst) of the last two snapshots
-  // feature versions
-  std::vector<cuda::DevArray<float>> patch_rows_;  // [t]: rows of delta(t).changed at t
+  // feature versions (the per-t patch is the second half of delta(t).compact)
   mutable std::vector<std::shared_ptr<FeatSlot>> slots_;  // slots_[0] = snapshot 0
   mutable uint64_t clock_ = 0;
   mutable int64_t materialisations_ = 0;

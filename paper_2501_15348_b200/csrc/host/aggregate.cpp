@@ -42,6 +42,23 @@ void init_pool() {
 }
 }  // namespace
 
+void pool_stats(int64_t* reserved, int64_t* used, int64_t* reserved_high, int64_t* used_high) {
+  std::call_once(g_pool_once, init_pool);
+  int dev = 0;
+  DGNN_CUDA(cudaGetDevice(&dev));
+  cudaMemPool_t pool;
+  DGNN_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  auto get = [&](cudaMemPoolAttr a, int64_t* out) {
+    uint64_t v = 0;
+    DGNN_CUDA(cudaMemPoolGetAttribute(pool, a, &v));
+    if (out) *out = static_cast<int64_t>(v);
+  };
+  get(cudaMemPoolAttrReservedMemCurrent, reserved);
+  get(cudaMemPoolAttrUsedMemCurrent, used);
+  get(cudaMemPoolAttrReservedMemHigh, reserved_high);
+  get(cudaMemPoolAttrUsedMemHigh, used_high);
+}
+
 void* dev_alloc(size_t bytes, cudaStream_t stream) {
   std::call_once(g_pool_once, init_pool);
   void* p = nullptr;
@@ -136,6 +153,7 @@ void prof_flush() {
     DGNN_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
     g_stats[p.cls].launches += 1;
     g_stats[p.cls].ms += ms;
+    g_stats[p.cls].max_ms = std::max(g_stats[p.cls].max_ms, static_cast<double>(ms));
     g_stats[p.cls].bytes += p.bytes;
     g_stats[p.cls].flops += p.flops;
     g_event_pool.push_back(p.a);
@@ -144,6 +162,12 @@ void prof_flush() {
   g_pending.clear();
 }
 ProfStat prof_get(int cls) { return (cls >= 0 && cls < kProfCount) ? g_stats[cls] : ProfStat{}; }
+void prof_add_host(int cls, double ms) {
+  if (!g_prof || cls < 0 || cls >= kProfCount) return;
+  g_stats[cls].launches += 1;
+  g_stats[cls].ms += ms;
+  g_stats[cls].max_ms = std::max(g_stats[cls].max_ms, ms);
+}
 
 ProfScope::ProfScope(int cls, cudaStream_t s, double bytes, double flops) : cls_(cls), s_(s) {
   if (!g_prof) return;
@@ -266,7 +290,8 @@ IncrementalResult aggregate_incremental(const AggResult& prev, const GraphView& 
     ProfScope ps(kProfAggDelta, stream, bytes);
     cuda::agg_delta(kind_i(fn.kind), delta.n_rows, dim, delta.rows.get(), delta.row_ptr.get(),
                     delta.ent.get(), prev_feats, curr_feats, r->values.get(), r->degree.get(),
-                    r->mean_sums.get(), r->argext.get(), stream);
+                    r->mean_sums.get(), r->argext.get(), stream, delta.ent_c.get(),
+                    curr_graph.num_nodes, delta.n_changed, delta.compact.get());
   }
   refresh_dense(*r, stream);
   return {std::move(r), false, FallbackReason::kNone};

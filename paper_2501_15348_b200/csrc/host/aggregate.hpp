@@ -117,18 +117,22 @@ void aggregate_backward(const GraphView& graph, const float* upstream, int32_t d
 // algorithmic bytes per class.
 enum ProfClass { kProfAggScratch = 0, kProfAggDelta = 1, kProfAggBackward = 2, kProfCellFwd = 3,
                  kProfCellBwd = 4, kProfWeightGrad = 5, kProfOther = 6, kProfCellBwdGemm = 7,
-                 kProfCount = 8 };
+                 kProfSample = 8,      // one whole (window, batch) sample, first to last op
+                 kProfSampleHost = 9,  // host time to issue one sample (no events)
+                 kProfCount = 10 };
 struct ProfStat {
   int64_t launches = 0;
   double ms = 0.0;
   double bytes = 0.0;
   double flops = 0.0;
+  double max_ms = 0.0;
 };
 void prof_enable(bool on);
 bool prof_enabled();
 void prof_reset();
 void prof_flush();  // resolves pending events (synchronises them)
 ProfStat prof_get(int cls);
+void prof_add_host(int cls, double ms);  // a host-timed scope
 class ProfScope {
  public:
   ProfScope(int cls, cudaStream_t s, double bytes, double flops = 0.0);

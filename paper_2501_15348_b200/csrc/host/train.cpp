@@ -3,6 +3,7 @@
 #include "train.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <random>
 
@@ -95,13 +96,19 @@ Worker::~Worker() {
 
 void Worker::run_sample(const SequenceWindow& window, Timestep windows_remaining, int64_t batch_id,
                         std::pair<NodeId, NodeId> node_range, float* grad, double* loss_slot) {
-  SeqSample sample =
-      build_sample(graph_, model_.cfg_, window, windows_remaining, batch_id, node_range, stream_);
-  Lanes lanes(stream_, aux_);
-  ForwardArtifacts fwd = model_forward(model_, sample, *provider_, lanes);
-  std::vector<Buf> dpred = seed_loss(sample, fwd, model_.cfg_.feature_dim, loss_slot, loss_ws_.get(),
-                                     lanes.of(model_.cfg_.layers));
-  model_backward(model_, sample, fwd, dpred, grad, lanes);
+  const auto h0 = std::chrono::steady_clock::now();
+  {
+    ProfScope whole(kProfSample, stream_, 0.0);
+    SeqSample sample =
+        build_sample(graph_, model_.cfg_, window, windows_remaining, batch_id, node_range, stream_);
+    Lanes lanes(stream_, aux_);
+    ForwardArtifacts fwd = model_forward(model_, sample, *provider_, lanes);
+    std::vector<Buf> dpred = seed_loss(sample, fwd, model_.cfg_.feature_dim, loss_slot,
+                                       loss_ws_.get(), lanes.of(model_.cfg_.layers));
+    model_backward(model_, sample, fwd, dpred, grad, lanes);
+  }
+  prof_add_host(kProfSampleHost,
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());
 }
 
 // ---------------------------------------------------------------- seq-first

@@ -18,6 +18,9 @@ namespace cuda {
 
 void* dev_alloc(size_t bytes, cudaStream_t stream);
 void dev_free(void* p, cudaStream_t stream);
+// Stream-ordered pool occupancy: bytes reserved from the device / in live
+// allocations, current and high-water.
+void pool_stats(int64_t* reserved, int64_t* used, int64_t* reserved_high, int64_t* used_high);
 // Bytes currently held by live DevArray allocations (for memory reporting).
 int64_t& dev_bytes_live();
 

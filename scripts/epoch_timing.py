@@ -1,14 +1,16 @@
-"""Per-epoch device time at a bench workload, with the per-class profiler on
-and off (diagnoses run-to-run variance of the C3 bench line)."""
+"""Per-epoch device time at a bench workload, with per-epoch kernel-time sums
+(profiler on) and SM clocks sampled during each epoch — diagnoses run-to-run
+variance of the bench line (GPU idle vs slower kernels vs clock dips)."""
 import json
 import os
+import statistics
 import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
-from bench import WORKLOADS  # noqa: E402
+from bench import WORKLOADS, ClockSampler  # noqa: E402
 from paper_2501_15348_b200 import api  # noqa: E402
 from paper_2501_15348_b200.sharding import run_sharded_epoch  # noqa: E402
 
@@ -21,23 +23,31 @@ sess = api.TrainSession(graph, api.TrainConfig(arch=wl["arch"], hidden=wl["hidde
 grad = torch.empty(sess.num_params, device="cuda")
 run_sharded_epoch(sess, grad)
 torch.cuda.synchronize()
-out = {}
-for prof in (False, True, False):
+api.prof_enable(True)
+rows = []
+for _ in range(epochs):
     api.prof_reset()
-    api.prof_enable(prof)
-    ts = []
-    for _ in range(epochs):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    with ClockSampler(0) as clk:
         h0 = time.perf_counter()
         e0.record(stream)
         run_sharded_epoch(sess, grad)
         e1.record(stream)
         torch.cuda.synchronize()
-        ts.append((round(e0.elapsed_time(e1), 1), round((time.perf_counter() - h0) * 1e3, 1)))
-    api.prof_enable(False)
+        wall = (time.perf_counter() - h0) * 1e3
     p = api.prof_get()
-    out[f"prof={prof}"] = {"epochs_ms_dev_wall": ts,
-                           "kernel_ms": round(sum(v["ms"] for v in p.values()) / epochs, 1)}
-    print(json.dumps(out[f"prof={prof}"]), flush=True)
-print(json.dumps({"mem_gb": round(torch.cuda.mem_get_info()[1] / 1e9 - torch.cuda.mem_get_info()[0] / 1e9, 1)}))
+    sc = api.prof_get(scopes=True)
+    smp, host = sc["sample"], sc["sample_host"]
+    c = clk.summary()
+    rows.append({"dev_ms": round(e0.elapsed_time(e1), 1), "wall_ms": round(wall, 1),
+                 "kernel_ms": round(sum(v["ms"] for v in p.values()), 1),
+                 "by_class": {k: round(v["ms"], 1) for k, v in p.items()},
+                 "samples": smp["launches"], "sample_ms_sum": round(smp["ms"], 1),
+                 "sample_ms_max": round(smp["max_ms"], 1),
+                 "host_ms_sum": round(host["ms"], 1), "host_ms_max": round(host["max_ms"], 1),
+                 "sm_mhz": c["sm_mhz"], "reasons": c["reasons"]})
+    print(json.dumps(rows[-1]), flush=True)
+api.prof_enable(False)
+print(json.dumps({"dev_ms_median": statistics.median(r["dev_ms"] for r in rows),
+                  "mem": api.mem_stats()}))

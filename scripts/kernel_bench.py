@@ -59,6 +59,16 @@ def main():
             ms = timeit(lambda: api.aggregate_delta_inplace(g, 1, agg, f0, f1, "sum"), args.iters)
             alg = 8 * nent + 4 * d * (sz["u_minus"] + sz["u_plus"]) + 8 * d * sz["n_rows"]
             res["agg_delta"] = {"ms": ms, "GBps_alg": alg / ms / 1e6, "entries": nent, **sz}
+    if want("agg_delta_feat"):
+        # C4-like delta: 2% structural churn + 2% feature-changed nodes (out-edge expansion)
+        s = api.Synth(n, 20, d, 2, 0.02, 0.02, seed=1)
+        g = s.to_graph()
+        agg = api.aggregate_scratch(g, 0, g.feats_tensor(0), "sum")
+        sz = g.delta_sizes(1)
+        nent = sz["n_del"] + sz["n_ins"]
+        ms = timeit(lambda: api.apply_graph_delta(g, 1, agg, "sum"), args.iters)
+        alg = 8 * nent + 4 * d * (sz["u_minus"] + sz["u_plus"]) + 8 * d * sz["n_rows"]
+        res["agg_delta_feat"] = {"ms": ms, "GBps_alg": alg / ms / 1e6, "alg_bytes": alg, **sz}
     for lstm in (True, False):
         name = "cell_fwd_lstm" if lstm else "cell_fwd_gru"
         if not want(name) and not want("cell_bwd") and not want("wgrad"):

@@ -146,6 +146,26 @@ def test_agg_delta_kernel_inplace(pair, api):
         assert nrel(agg["values"].cpu().numpy(), want) < 1e-5, t
 
 
+@pytest.mark.parametrize("kind", ["sum", "mean"])
+def test_graph_delta_compact_block(ref, api, kind):
+    """K2 on the graph's own delta with the compact changed-row block (heavy
+    feature churn): equals scratch at t, and is bitwise the plain-index
+    kernel's result (same values gathered in the same order)."""
+    import torch
+    g_ref, g = make_pair(ref, api, n=500, avg_degree=6, dim=16, T=5, edge=0.05, feat=0.2, seed=9)
+    for t in range(1, g_ref.T):
+        a = api.aggregate_scratch(g, t - 1, g.feats_tensor(t - 1), kind)
+        b = {k: v.clone() for k, v in a.items() if hasattr(v, "clone")}
+        api.apply_graph_delta(g, t, a, kind)
+        api.aggregate_delta_inplace(g, t, b, g.feats_tensor(t - 1), g.feats_tensor(t), kind)
+        torch.cuda.synchronize()
+        want = g_ref.agg_scratch(t, kind, g_ref.feats(t))
+        assert nrel(a["values"].cpu().numpy(), want["values"]) < 1e-5, t
+        assert torch.equal(a["values"], b["values"]), t
+        if kind == "mean":
+            assert np.array_equal(a["degree"].cpu().numpy(), want["degree"].astype(np.float32))
+
+
 @pytest.mark.parametrize("kind", KINDS)
 def test_agg_backward(pair, api, kind):
     import torch
