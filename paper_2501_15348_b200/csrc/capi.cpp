@@ -153,7 +153,11 @@ void dgnn_graph_free(dgnn_graph* g) {
   g->last_feats.reset();  // leases end before their slots and stream
   g->g.reset();
   cudaStreamSynchronize(s);
-  if (own) cudaStreamDestroy(s);
+  if (own) {
+    cuda::release_stream_blocks(s);
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  }
   delete g;
 }
 

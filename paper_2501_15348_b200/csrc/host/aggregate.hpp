@@ -119,7 +119,9 @@ enum ProfClass { kProfAggScratch = 0, kProfAggDelta = 1, kProfAggBackward = 2, k
                  kProfCellBwd = 4, kProfWeightGrad = 5, kProfOther = 6, kProfCellBwdGemm = 7,
                  kProfSample = 8,      // one whole (window, batch) sample, first to last op
                  kProfSampleHost = 9,  // host time to issue one sample (no events)
-                 kProfCount = 10 };
+                 kProfHostBuild = 10, kProfHostFwd = 11, kProfHostBwd = 12,  // its phases
+                 kProfHostAlloc = 13,  // host time inside device allocations
+                 kProfCount = 14 };
 struct ProfStat {
   int64_t launches = 0;
   double ms = 0.0;

@@ -90,25 +90,35 @@ Worker::Worker(const DeviceGraph& graph, DgnnModel& model, const TrainConfig& cf
 Worker::~Worker() {
   if (aux_) {
     cudaStreamSynchronize(aux_);
+    cuda::release_stream_blocks(aux_);
+    cudaStreamSynchronize(aux_);
     cudaStreamDestroy(aux_);
   }
 }
 
 void Worker::run_sample(const SequenceWindow& window, Timestep windows_remaining, int64_t batch_id,
                         std::pair<NodeId, NodeId> node_range, float* grad, double* loss_slot) {
-  const auto h0 = std::chrono::steady_clock::now();
+  using clk = std::chrono::steady_clock;
+  auto since = [](clk::time_point t) {
+    return std::chrono::duration<double, std::milli>(clk::now() - t).count();
+  };
+  const auto h0 = clk::now();
   {
     ProfScope whole(kProfSample, stream_, 0.0);
     SeqSample sample =
         build_sample(graph_, model_.cfg_, window, windows_remaining, batch_id, node_range, stream_);
+    prof_add_host(kProfHostBuild, since(h0));
+    const auto h1 = clk::now();
     Lanes lanes(stream_, aux_);
     ForwardArtifacts fwd = model_forward(model_, sample, *provider_, lanes);
     std::vector<Buf> dpred = seed_loss(sample, fwd, model_.cfg_.feature_dim, loss_slot,
                                        loss_ws_.get(), lanes.of(model_.cfg_.layers));
+    prof_add_host(kProfHostFwd, since(h1));
+    const auto h2 = clk::now();
     model_backward(model_, sample, fwd, dpred, grad, lanes);
+    prof_add_host(kProfHostBwd, since(h2));
   }
-  prof_add_host(kProfSampleHost,
-                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());
+  prof_add_host(kProfSampleHost, since(h0));
 }
 
 // ---------------------------------------------------------------- seq-first

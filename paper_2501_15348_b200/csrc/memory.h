@@ -17,7 +17,12 @@ namespace dgnn {
 namespace cuda {
 
 void* dev_alloc(size_t bytes, cudaStream_t stream);
-void dev_free(void* p, cudaStream_t stream);
+void dev_free(void* p, size_t bytes, cudaStream_t stream);
+// Blocks held by the per-stream free lists (see aggregate.cpp) / return them
+// to the pool (callers must not have work pending that uses them).
+int64_t cached_block_bytes();
+void release_cached_blocks();
+void release_stream_blocks(cudaStream_t stream);  // before destroying `stream`
 // Stream-ordered pool occupancy: bytes reserved from the device / in live
 // allocations, current and high-water.
 void pool_stats(int64_t* reserved, int64_t* used, int64_t* reserved_high, int64_t* used_high);
@@ -47,7 +52,7 @@ class DevArray {
     return *this;
   }
   void reset() {
-    if (p_) dev_free(p_, stream_);
+    if (p_) dev_free(p_, n_ * sizeof(T), stream_);
     p_ = nullptr;
     n_ = 0;
   }

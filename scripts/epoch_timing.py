@@ -1,6 +1,7 @@
 """Per-epoch device time at a bench workload, with per-epoch kernel-time sums
 (profiler on) and SM clocks sampled during each epoch — diagnoses run-to-run
 variance of the bench line (GPU idle vs slower kernels vs clock dips)."""
+import contextlib
 import json
 import os
 import statistics
@@ -13,6 +14,11 @@ import torch  # noqa: E402
 from bench import WORKLOADS, ClockSampler  # noqa: E402
 from paper_2501_15348_b200 import api  # noqa: E402
 from paper_2501_15348_b200.sharding import run_sharded_epoch  # noqa: E402
+
+class NullClk:
+    def summary(self):
+        return {"sm_mhz": None, "reasons": []}
+
 
 wl = WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "c3"]
 epochs = int(sys.argv[2]) if len(sys.argv) > 2 else 4
@@ -29,7 +35,7 @@ for _ in range(epochs):
     api.prof_reset()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    with ClockSampler(0) as clk:
+    with (ClockSampler(0) if not os.environ.get("NO_CLOCKS") else contextlib.nullcontext(NullClk())) as clk:
         h0 = time.perf_counter()
         e0.record(stream)
         run_sharded_epoch(sess, grad)
@@ -46,6 +52,11 @@ for _ in range(epochs):
                  "samples": smp["launches"], "sample_ms_sum": round(smp["ms"], 1),
                  "sample_ms_max": round(smp["max_ms"], 1),
                  "host_ms_sum": round(host["ms"], 1), "host_ms_max": round(host["max_ms"], 1),
+                 "host_max_at": int(host["flops"]),
+                 "phase_max": {k: (round(sc[k]["max_ms"], 1), int(sc[k]["flops"]))
+                               for k in ("host_build", "host_fwd", "host_bwd", "host_alloc")},
+                 "alloc_ms_sum": round(sc["host_alloc"]["ms"], 1),
+                 "allocs": sc["host_alloc"]["launches"],
                  "sm_mhz": c["sm_mhz"], "reasons": c["reasons"]})
     print(json.dumps(rows[-1]), flush=True)
 api.prof_enable(False)
