@@ -1,15 +1,18 @@
 """Benchmark: training snapshots/sec of the ReInc dynamic-GNN hot path on B200.
 
-Workload (BASELINE.json configs[2], SURVEY §8d "C3"): integrated GraphRNN
-GCRN-M2 (LSTM, 2 layers, hidden 64) on a synthetic dynamic graph of 1M nodes /
-20M edges, 32 snapshots, 2% edge churn with deletions, feature dim 128,
-L=8, H=1, S=1, sum aggregation, REINC cache at capacity 1.0, incremental
-aggregation on. One "step" = one training epoch over all W = 23 executable
-windows with the reference's distributed semantics (per-window gradients,
-ordered sum / W, one Adam step; src/distsim.cpp:197-272); with N GPUs the
-windows are split into consecutive blocks (plan(), src/distsim.cpp:52-70) and
-the flat gradient is all-reduced over NCCL. Total work is fixed as N grows
-("strong" scaling). snapshots/sec = W * (L + H) / epoch seconds.
+Default workload (BASELINE.json configs[3] / configs[4], SURVEY §8d "C4"/"C5",
+the graph the metric's 1/2/4/8-GPU numbers are quoted on; it fits one B200):
+integrated GraphRNN GCRN-GRU (tgcn, 2 layers, hidden 64) on a synthetic
+dynamic graph of 4M nodes / 80M edges, 64 snapshots, 2% edge churn with
+deletions and 2% feature-changed nodes per step, feature dim 128, L=8, H=1,
+S=1, sum aggregation, REINC cache at capacity 1.0, incremental aggregation
+on. `--workload c3` runs the 1M-node GC-LSTM config (configs[2]). One "step"
+= one training epoch over all W executable windows (55 at C4) with the
+reference's distributed semantics (per-window gradients, ordered sum / W, one
+Adam step; src/distsim.cpp:197-272); with N GPUs the windows are split into
+consecutive blocks (plan(), src/distsim.cpp:52-70) and the flat gradient is
+all-reduced over NCCL. Total work is fixed as N grows ("strong" scaling).
+snapshots/sec = W * (L + H) / epoch seconds.
 
 `--impl reference` times the reference's own CPU implementation (oracle/_ref,
 compiled from /root/reference/proj/src) on a bounded sample of the same
@@ -159,7 +162,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -229,6 +232,10 @@ def main():
         barrier()
     api.prof_enable(False)
     launches = api.launch_count() - launches0
+    if world > 1:  # whole-job kernel launches (every rank's)
+        lt = torch.tensor([launches], device="cuda", dtype=torch.int64)
+        dist.all_reduce(lt)
+        launches = int(lt.item())
     ms_total = ev0.elapsed_time(ev1)
     t = torch.tensor([ms_total], device="cuda", dtype=torch.float64)
     if world > 1:

@@ -347,6 +347,8 @@ int dgnn_synth_to_graph(const dgnn_synth* s, void* stream, dgnn_graph** out) {
                       static_cast<int64_t>(st.changed.size()), ps.changed_feats);
     }
     DGNN_CUDA(cudaStreamSynchronize(g->stream));
+    // build temporaries (sort buffers, CUB scratch) go back to the pool
+    cuda::release_stream_blocks(g->stream);
     *out = guard.release();
   });
 }

@@ -401,6 +401,7 @@ int64_t DeviceGraph::device_bytes() const {
 
 void DeviceGraph::add_snapshot(const int32_t* src, const int32_t* dst, int64_t num_edges,
                                const float* feats) {
+  cuda::release_stream_blocks(stream_);
   Cub cub(stream_);
   DevArray<uint64_t> keys = sorted_edge_keys(src, dst, num_edges, n_, cub, true);
   const int64_t nf = static_cast<int64_t>(n_) * d_;
@@ -434,6 +435,9 @@ void DeviceGraph::add_delta(const int32_t* del_src, const int32_t* del_dst, int6
                             const float* changed_feats) {
   if (snaps_.empty()) throw std::invalid_argument("add_delta needs a previous snapshot");
   cudaStream_t st = stream_;
+  // the previous build step's temporaries (sizes drift per snapshot) go back
+  // to the pool instead of accumulating in the per-size free lists
+  cuda::release_stream_blocks(st);
   Cub cub(st);
   DevArray<uint64_t> del = sorted_edge_keys(del_src, del_dst, n_del, n_, cub, false);
   DevArray<uint64_t> ins = sorted_edge_keys(ins_src, ins_dst, n_ins, n_, cub, true);

@@ -79,10 +79,15 @@ BlockCache& block_cache() {
   static BlockCache* c = new BlockCache();  // never destroyed: frees may run at exit
   return *c;
 }
+// Size classes: 4 KB granules below 1 MB, then 8 classes per octave (at most
+// 12.5% slack), so buffers whose sizes drift slightly (per-snapshot edge
+// counts) still share a class.
 size_t round_block(size_t bytes) {
-  constexpr size_t kSmall = size_t{1} << 20, kPage = size_t{2} << 20;
+  constexpr size_t kSmall = size_t{1} << 20;
   if (bytes < kSmall) return (bytes + 4095) / 4096 * 4096;
-  return (bytes + kPage - 1) / kPage * kPage;
+  int top = 63 - __builtin_clzll(static_cast<unsigned long long>(bytes));
+  const size_t step = size_t{1} << (top - 3);
+  return (bytes + step - 1) / step * step;
 }
 void release_cached_locked(BlockCache& c) {
   for (auto& [st, lists] : c.free)
@@ -257,17 +262,26 @@ void prof_add_host(int cls, double ms) {
   }
 }
 
-ProfScope::ProfScope(int cls, cudaStream_t s, double bytes, double flops) : cls_(cls), s_(s) {
+ProfScope::ProfScope(int cls, cudaStream_t s, double bytes, double flops)
+    : cls_(cls), s_(s), bytes_(bytes), flops_(flops) {
   if (!g_prof) return;
   a_ = take_event();
   b_ = take_event();
   DGNN_CUDA(cudaEventRecord(a_, s_));
-  g_pending.push_back({cls, a_, b_, bytes, flops});
 }
 ProfScope::~ProfScope() {
   if (!a_) return;
+  // queued only once both ends are recorded: a flush triggered by an inner
+  // scope must never see an open (unrecorded) outer scope
   cudaEventRecord(b_, s_);
-  if (g_pending.size() > 4096) prof_flush();
+  g_pending.push_back({cls_, a_, b_, bytes_, flops_});
+  if (g_pending.size() > 4096) {
+    try {
+      prof_flush();
+    } catch (...) {
+      g_pending.clear();
+    }
+  }
 }
 
 // ---------------------------------------------------------------- helpers

@@ -143,6 +143,7 @@ class ProfScope {
  private:
   int cls_;
   cudaStream_t s_;
+  double bytes_, flops_;
   cudaEvent_t a_ = nullptr, b_ = nullptr;
 };
 
