@@ -182,10 +182,12 @@ def test_agg_backward(pair, api, kind):
 
 
 @pytest.mark.parametrize("lstm", [True, False])
-@pytest.mark.parametrize("H,n_in", [(16, 8), (64, 128), (64, 64)])
-def test_cell_fwd_bwd(ref, api, lstm, H, n_in):
+@pytest.mark.parametrize("H,n_in,n", [(16, 8, 777), (64, 128, 777), (64, 64, 777),
+                                      (64, 128, 40013), (32, 96, 40013)])
+def test_cell_fwd_bwd(ref, api, lstm, H, n_in, n):
+    """Cell forward / backward against the reference; H in {32, 64} runs the
+    tcgen05 kernels (40013 rows: many chunks per CTA in the weight gradient)."""
     import torch
-    n = 777
     rng = np.random.default_rng(11)
     params = ref.cell_init(0 if lstm else 1, n_in, H, 5)
     X = rng.uniform(-2, 2, (n, n_in))
