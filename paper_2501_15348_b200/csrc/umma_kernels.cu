@@ -128,7 +128,11 @@ int umma_debug_flags() {
 
 constexpr int kRgThreads = 416;  // 13 warps: 4 producers, 1 MMA, 8 epilogue
 constexpr int kRgStages = 3;     // MMA operand stages (A hi/lo + B hi/lo)
-constexpr int kRawSlots = 6;     // cp.async prefetch depth of raw fp32 A chunks
+// cp.async prefetch depth of raw fp32 A chunks: as deep as shared memory
+// allows (the producers are latency-bound on 128 separate 64 B row segments
+// per chunk; small-N contractions have little MMA work to hide it behind)
+template <int NPAD>
+constexpr int kRawSlotsFor = NPAD <= 128 ? 12 : (NPAD <= 192 ? 8 : 6);
 constexpr int kProducerThreads = 128;
 constexpr int kMmaWarp = 4;
 constexpr int kEpiWarp0 = 5;  // warps 5..12: lane quadrant = warp % 4 covers 0..3 twice
@@ -142,6 +146,7 @@ struct RowGemmSmem {
   static constexpr uint32_t kStage = 2 * kA + 2 * kB;
   static constexpr uint32_t kRaw = kTileM * kKC * 4;      // one raw fp32 A chunk
   static constexpr uint32_t kRawOff = kStage * kRgStages;
+  static constexpr int kRawSlots = kRawSlotsFor<NPAD>;
   static constexpr uint32_t kBars = kRawOff + kRaw * kRawSlots;  // barrier block offset
   static constexpr uint32_t kBias = kBars + 128;                 // 4H fp32 bias copy
   static constexpr uint32_t kOut = kBias + 1024;                 // per-epilogue-warp store staging
@@ -202,7 +207,7 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
         const int tile = blockIdx.x + (item / p.nchunks) * gridDim.x;
         const int kc0 = (item % p.nchunks) * kKC;
         const int64_t r0 = static_cast<int64_t>(tile) * kTileM;
-        const uint32_t slot = raw0 + (item % kRawSlots) * S::kRaw;
+        const uint32_t slot = raw0 + (item % S::kRawSlots) * S::kRaw;
 #pragma unroll
         for (int it = 0; it < kRawPerThread; ++it) {
           const int f = tid + it * kProducerThreads;
@@ -217,16 +222,16 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
       }
       cp_async_commit();  // one group per item (possibly empty) keeps the accounting uniform
     };
-    for (int i = 0; i < kRawSlots - 1; ++i) issue(i);
+    for (int i = 0; i < S::kRawSlots - 1; ++i) issue(i);
     for (int item = 0; item < total; ++item) {
-      issue(item + kRawSlots - 1);
-      cp_async_wait<kRawSlots - 1>();
+      issue(item + S::kRawSlots - 1);
+      cp_async_wait<S::kRawSlots - 1>();
       const uint32_t g = static_cast<uint32_t>(item);
       const int c = item % p.nchunks;
       const uint32_t s = g % kRgStages, ph = (g / kRgStages) & 1u;
       mbar_wait(&empty[s], ph ^ 1u);
       const uint32_t st = sbase + s * S::kStage;
-      const uint32_t slot = raw0 + (item % kRawSlots) * S::kRaw;
+      const uint32_t slot = raw0 + (item % S::kRawSlots) * S::kRaw;
       {
 #pragma unroll
         for (int it = 0; it < kRawPerThread; ++it) {
