@@ -127,12 +127,17 @@ int umma_debug_flags() {
 }
 
 constexpr int kRgThreads = 416;  // 13 warps: 4 producers, 1 MMA, 8 epilogue
-constexpr int kRgStages = 3;     // MMA operand stages (A hi/lo + B hi/lo)
+// MMA operand stages (A hi/lo + B hi/lo): the producer -> tcgen05 -> commit
+// round trip is latency-bound (ncu: producers wait on `empty`, the MMA thread
+// on `full`, the tensor pipe < 20% busy), so small-N contractions get more
+// stages in the smem their smaller B tiles leave free
+template <int NPAD>
+constexpr int kRgStagesFor = NPAD <= 64 ? 6 : (NPAD <= 128 ? 5 : (NPAD <= 192 ? 4 : 3));
 // cp.async prefetch depth of raw fp32 A chunks: as deep as shared memory
 // allows (the producers are latency-bound on 128 separate 64 B row segments
 // per chunk; small-N contractions have little MMA work to hide it behind)
 template <int NPAD>
-constexpr int kRawSlotsFor = NPAD <= 128 ? 12 : (NPAD <= 192 ? 8 : 6);
+constexpr int kRawSlotsFor = NPAD <= 64 ? 7 : (NPAD <= 192 ? 5 : 6);
 constexpr int kProducerThreads = 128;
 constexpr int kMmaWarp = 4;
 constexpr int kEpiWarp0 = 5;  // warps 5..12: lane quadrant = warp % 4 covers 0..3 twice
@@ -145,10 +150,11 @@ struct RowGemmSmem {
   static constexpr uint32_t kB = tile_bytes(NPAD, kKC);
   static constexpr uint32_t kStage = 2 * kA + 2 * kB;
   static constexpr uint32_t kRaw = kTileM * kKC * 4;      // one raw fp32 A chunk
-  static constexpr uint32_t kRawOff = kStage * kRgStages;
+  static constexpr int kStages = kRgStagesFor<NPAD>;
+  static constexpr uint32_t kRawOff = kStage * kStages;
   static constexpr int kRawSlots = kRawSlotsFor<NPAD>;
   static constexpr uint32_t kBars = kRawOff + kRaw * kRawSlots;  // barrier block offset
-  static constexpr uint32_t kBias = kBars + 128;                 // 4H fp32 bias copy
+  static constexpr uint32_t kBias = kBars + 256;                 // 4H fp32 bias copy
   static constexpr uint32_t kOut = kBias + 1024;                 // per-epilogue-warp store staging
   static constexpr uint32_t kBytes = kOut + kEpiWarps * 32 * 16 * 4;
 };
@@ -168,14 +174,14 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
   using S = RowGemmSmem<NPAD>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kBars);
-  uint64_t* empty = full + kRgStages;
-  uint64_t* tfull = empty + kRgStages;
+  uint64_t* empty = full + S::kStages;
+  uint64_t* tfull = empty + S::kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == kMmaWarp) tmem_alloc(tmem_slot, 512);
   if (tid == 0) {
-    for (int s = 0; s < kRgStages; ++s) {
+    for (int s = 0; s < S::kStages; ++s) {
       mbar_init(&full[s], kProducerThreads);
       mbar_init(&empty[s], 1);
     }
@@ -202,52 +208,58 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
     const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const int total = my_tiles * p.nchunks;
     const uint32_t raw0 = sbase + S::kRawOff;
-    auto issue = [&](int item) {
-      if (item < total) {
-        const int tile = blockIdx.x + (item / p.nchunks) * gridDim.x;
-        const int kc0 = (item % p.nchunks) * kKC;
-        const int64_t r0 = static_cast<int64_t>(tile) * kTileM;
-        const uint32_t slot = raw0 + (item % S::kRawSlots) * S::kRaw;
+    // This thread's units of every chunk: rows prow + 32 * it, K quad kq
+    // (f = tid + 128 * it). Issue / consume positions are advanced
+    // incrementally — no per-item integer division (the producers are the
+    // kernel's critical path).
+    const int kq = tid & 3, prow = tid >> 2;
+    int is_tile = 0, is_chunk = 0, is_slot = 0;  // next (tile, chunk) to fetch
+    auto issue = [&]() {
+      if (is_tile < my_tiles) {
+        const int64_t r0 = static_cast<int64_t>(blockIdx.x + is_tile * gridDim.x) * kTileM + prow;
+        const int k = is_chunk * kKC + kq * 4;
+        const bool kin = k < p.K;
+        const float* base = k < p.k1 ? p.A1 + k : p.A2 + (k - p.k1);
+        const int64_t ld = k < p.k1 ? p.k1 : p.k2;
+        const uint32_t slot = raw0 + is_slot * S::kRaw + tid * 16;
 #pragma unroll
         for (int it = 0; it < kRawPerThread; ++it) {
-          const int f = tid + it * kProducerThreads;
-          const int row = f / (kKC / 4), kq = f % (kKC / 4);
-          const int64_t grow = r0 + row;
-          const int k = kc0 + kq * 4;
-          const bool valid = grow < p.M && k < p.K;
-          const float* src = !valid ? p.A1
-                                    : (k < p.k1 ? p.A1 + grow * p.k1 + k : p.A2 + grow * p.k2 + (k - p.k1));
-          cp_async16_zfill(slot + f * 16, src, valid);
+          const int64_t grow = r0 + 32 * it;
+          const bool valid = kin && grow < p.M;
+          cp_async16_zfill(slot + it * kProducerThreads * 16, valid ? base + grow * ld : p.A1, valid);
         }
+        if (++is_chunk == p.nchunks) {
+          is_chunk = 0;
+          ++is_tile;
+        }
+        if (++is_slot == S::kRawSlots) is_slot = 0;
       }
       cp_async_commit();  // one group per item (possibly empty) keeps the accounting uniform
     };
-    for (int i = 0; i < S::kRawSlots - 1; ++i) issue(i);
+    for (int i = 0; i < S::kRawSlots - 1; ++i) issue();
+    int c = 0, slot_i = 0;
+    uint32_t s = 0, ph = 0;
     for (int item = 0; item < total; ++item) {
-      issue(item + S::kRawSlots - 1);
+      issue();
       cp_async_wait<S::kRawSlots - 1>();
-      const uint32_t g = static_cast<uint32_t>(item);
-      const int c = item % p.nchunks;
-      const uint32_t s = g % kRgStages, ph = (g / kRgStages) & 1u;
       mbar_wait(&empty[s], ph ^ 1u);
       const uint32_t st = sbase + s * S::kStage;
-      const uint32_t slot = raw0 + (item % S::kRawSlots) * S::kRaw;
+      const uint8_t* slotp = smem + S::kRawOff + slot_i * S::kRaw + tid * 16;
       {
+        // all four loads first, then split + store (exposes one LDS latency, not four)
+        float4 v[kRawPerThread];
+#pragma unroll
+        for (int it = 0; it < kRawPerThread; ++it)
+          v[it] = *reinterpret_cast<const float4*>(slotp + it * kProducerThreads * 16);
 #pragma unroll
         for (int it = 0; it < kRawPerThread; ++it) {
           if (p.debug & 4) break;
-          const int f = tid + it * kProducerThreads;
-          const int row = f / (kKC / 4), kq = f % (kKC / 4);
-          float4 v;
-          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                       : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                       : "r"(slot + f * 16));
           float h0, l0, h1, l1, h2, l2, h3, l3;
-          split_tf32(v.x, h0, l0);
-          split_tf32(v.y, h1, l1);
-          split_tf32(v.z, h2, l2);
-          split_tf32(v.w, h3, l3);
-          const uint32_t off = tile_offset(kTileM, row, kq * 4);
+          split_tf32(v[it].x, h0, l0);
+          split_tf32(v[it].y, h1, l1);
+          split_tf32(v[it].z, h2, l2);
+          split_tf32(v[it].w, h3, l3);
+          const uint32_t off = tile_offset(kTileM, prow + 32 * it, kq * 4);
           st_shared_v4(st + off, h0, h1, h2, h3);
           st_shared_v4(st + S::kA + off, l0, l1, l2, l3);
         }
@@ -263,6 +275,12 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
           mbar_arrive(&full[s]);
         }
       }
+      if (++c == p.nchunks) c = 0;
+      if (++slot_i == S::kRawSlots) slot_i = 0;
+      if (++s == S::kStages) {
+        s = 0;
+        ph ^= 1u;
+      }
     }
     cp_async_wait<0>();
   } else if (warp == kMmaWarp) {
@@ -276,7 +294,7 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
       fence_after_sync();
       const uint32_t d = tmem + b * 256;
       for (int c = 0; c < p.nchunks; ++c, ++g) {
-        const uint32_t s = g % kRgStages, ph = (g / kRgStages) & 1u;
+        const uint32_t s = g % S::kStages, ph = (g / S::kStages) & 1u;
         mbar_wait(&full[s], ph);
         fence_after_sync();
         const uint32_t st = sbase + s * S::kStage;
