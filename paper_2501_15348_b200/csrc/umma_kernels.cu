@@ -514,7 +514,13 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
 // ------------------------------------------------------------- weight gradient
 // Partial D'_cta (Mg x Npad) = sum over this CTA's rows of G^T(:, rows) *
 // [X | Hm | 1](rows, :), with Mg = 4H in {128, 256} and Npad >= in + H + 1.
-constexpr int kThreads = 256;
+// Warps 0-7 copy raw 16-row chunks (cp.async, two chunks ahead) and write
+// the transposed, 3xTF32-split operands; warp 8 issues the MMAs. Hand-offs
+// are mbarriers only (no block-wide barrier per chunk): raw chunk landed
+// (cp.async.mbarrier.arrive.noinc from every copier), raw slot consumed,
+// operand stage full (every converter), stage free (tcgen05.commit).
+constexpr int kWgConv = 256;               // copy + convert threads
+constexpr int kThreads = kWgConv + 32;     // + the MMA warp
 constexpr int kKW = 16;  // rows (the MMA K) per staged chunk
 
 template <int MG, int NPAD>
@@ -528,8 +534,12 @@ struct WgradSmem {
   static constexpr uint32_t kRaw = kKW * 4 * (MG + 192);
   static constexpr uint32_t kRawOff = kStages * kStage;
   static constexpr uint32_t kBars = kRawOff + kRawSlots * kRaw;
-  static constexpr uint32_t kBytes = kBars + 64;
+  static constexpr uint32_t kBytes = kBars + 128;
 };
+
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 
 template <int MG, int NPAD>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -537,14 +547,26 @@ k_wgrad(int M, int in, int H, const float* __restrict__ G, const float* __restri
         const float* __restrict__ Hm, float* __restrict__ ws) {
   using S = WgradSmem<MG, NPAD>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kBars);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + S::kBars + 32);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kBars);
+  uint64_t* empty = full + S::kStages;
+  uint64_t* rawfull = empty + S::kStages;
+  uint64_t* rawempty = rawfull + S::kRawSlots;
+  uint64_t* done = rawempty + S::kRawSlots;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int kHalves = MG / 128;
   constexpr uint32_t kCols = kHalves == 2 ? 512 : 256;
   if (warp == 0) tmem_alloc(tmem_slot, kCols);
   if (tid == 0) {
-    for (int s = 0; s < S::kStages; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < S::kStages; ++s) {
+      mbar_init(&full[s], kWgConv);
+      mbar_init(&empty[s], 1);
+    }
+    for (int r = 0; r < S::kRawSlots; ++r) {
+      mbar_init(&rawfull[r], kWgConv);
+      mbar_init(&rawempty[r], kWgConv);
+    }
+    mbar_init(done, 1);
     fence_barrier_init();
   }
   fence_before_sync();
@@ -552,81 +574,90 @@ k_wgrad(int M, int in, int H, const float* __restrict__ G, const float* __restri
   fence_after_sync();
   const uint32_t tmem = *tmem_slot;
   const uint32_t sbase = smem_u32(smem);
-  constexpr uint32_t idesc = idesc_tf32(128, NPAD);
-  constexpr uint32_t lboA = tile_lbo(MG), lboB = tile_lbo(NPAD);
   const int KXH = in + H;
   const int64_t per = (static_cast<int64_t>(M) + gridDim.x - 1) / gridDim.x;
   const int64_t rb = blockIdx.x * per;
   const int64_t re = rb + per < M ? rb + per : M;
   const int nchunks = re > rb ? static_cast<int>((re - rb + kKW - 1) / kKW) : 0;
-  // raw slot layout: G [kKW][MG] | X [kKW][in] | Hm [kKW][H]
-  const uint32_t raw0 = sbase + S::kRawOff;
-  // The 16 rows of each operand are one contiguous block in global memory, so
-  // each region is a linear copy; rows past `re` are zero-filled.
-  auto copy_region = [&](uint32_t dst, const float* src, int width, int live_rows) {
-    const int n4 = kKW * width / 4, valid4 = live_rows * width / 4;
-    for (int f = tid; f < n4; f += kThreads) {
-      const bool valid = f < valid4;
-      cp_async16_zfill(dst + f * 16, valid ? src + f * 4 : src, valid);
-    }
-  };
-  auto issue = [&](int c) {
-    if (c < nchunks) {
-      const uint32_t slot = raw0 + (c % S::kRawSlots) * S::kRaw;
+
+  if (warp < 8) {
+    // ---------------- copy + convert
+    // raw slot layout: G [kKW][MG] | X [kKW][in] | Hm [kKW][H]
+    const uint32_t raw0 = sbase + S::kRawOff;
+    // The 16 rows of each operand are one contiguous block in global memory, so
+    // each region is a linear copy; rows past `re` are zero-filled.
+    auto copy_region = [&](uint32_t dst, const float* src, int width, int live_rows) {
+      const int n4 = kKW * width / 4, valid4 = live_rows * width / 4;
+      for (int f = tid; f < n4; f += kWgConv) {
+        const bool valid = f < valid4;
+        cp_async16_zfill(dst + f * 16, valid ? src + f * 4 : src, valid);
+      }
+    };
+    auto issue = [&](int c) {
+      const int r = c % S::kRawSlots;
+      if (c >= S::kRawSlots) mbar_wait(&rawempty[r], ((c - S::kRawSlots) / S::kRawSlots) & 1u);
+      const uint32_t slot = raw0 + r * S::kRaw;
       const int64_t q0 = rb + static_cast<int64_t>(c) * kKW;
       const int live = static_cast<int>(re - q0 < kKW ? re - q0 : kKW);
       copy_region(slot, G + q0 * MG, MG, live);
       copy_region(slot + kKW * MG * 4, X + q0 * in, in, live);
       copy_region(slot + kKW * (MG + in) * 4, Hm + q0 * H, H, live);
-    }
-    cp_async_commit();
-  };
-  for (int i = 0; i < S::kRawSlots - 1; ++i) issue(i);
-  cp_async_wait<S::kRawSlots - 2>();
-  __syncthreads();  // raw chunk 0 visible to every converting thread
-  for (int c = 0; c < nchunks; ++c) {
-    issue(c + S::kRawSlots - 1);
-    const uint32_t s = c % S::kStages;
-    if (c >= S::kStages) mbar_wait(&bars[s], ((c - S::kStages) / S::kStages) & 1u);
-    const uint32_t st = sbase + s * S::kStage;
-    const float* rawG = reinterpret_cast<const float*>(smem + S::kRawOff + (c % S::kRawSlots) * S::kRaw);
-    const float* rawX = rawG + kKW * MG;
-    const float* rawH = rawX + kKW * in;
-    const int64_t q0c = rb + static_cast<int64_t>(c) * kKW;
-    // A' = G^T: one (column m, 4-row quad) per task; lanes take consecutive
-    // columns so the 8 lanes of a store phase fill 8 distinct 16 B bank groups
-    // of a core matrix (conflict-free), and the column reads are consecutive.
-    for (int task = tid; task < MG * (kKW / 4); task += kThreads) {
-      const int m = task % MG, k4 = task / MG;
-      float h[4], l[4];
+      cp_async_mbar_arrive_noinc(&rawfull[r]);  // completes when every copier's copies landed
+    };
+    for (int c = 0; c < S::kRawSlots - 1 && c < nchunks; ++c) issue(c);
+    for (int c = 0; c < nchunks; ++c) {
+      if (c + S::kRawSlots - 1 < nchunks) issue(c + S::kRawSlots - 1);
+      const int r = c % S::kRawSlots;
+      mbar_wait(&rawfull[r], (c / S::kRawSlots) & 1u);
+      const uint32_t s = c % S::kStages;
+      if (c >= S::kStages) mbar_wait(&empty[s], ((c - S::kStages) / S::kStages) & 1u);
+      const uint32_t st = sbase + s * S::kStage;
+      const float* rawG = reinterpret_cast<const float*>(smem + S::kRawOff + r * S::kRaw);
+      const float* rawX = rawG + kKW * MG;
+      const float* rawH = rawX + kKW * in;
+      const int64_t q0c = rb + static_cast<int64_t>(c) * kKW;
+      // A' = G^T: one (column m, 4-row quad) per task; lanes take consecutive
+      // columns so the 8 lanes of a store phase fill 8 distinct 16 B bank groups
+      // of a core matrix (conflict-free), and the column reads are consecutive.
+      for (int task = tid; task < MG * (kKW / 4); task += kWgConv) {
+        const int m = task % MG, k4 = task / MG;
+        float h[4], l[4];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) split_tf32(rawG[(k4 * 4 + r) * MG + m], h[r], l[r]);
-      const uint32_t off = tile_offset(MG, m, k4 * 4);
-      st_shared_v4(st + off, h[0], h[1], h[2], h[3]);
-      st_shared_v4(st + S::kA + off, l[0], l[1], l[2], l[3]);
-    }
-    // B' = [X | Hm | 1]^T (ones column at n = in + H -> bias gradient)
-    for (int task = tid; task < NPAD * (kKW / 4); task += kThreads) {
-      const int n = task % NPAD, k4 = task / NPAD;
-      float h[4], l[4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int rr = k4 * 4 + r;
-        float x = 0.f;
-        if (n < in) x = rawX[rr * in + n];
-        else if (n < KXH) x = rawH[rr * H + (n - in)];
-        else if (n == KXH && q0c + rr < re) x = 1.f;
-        split_tf32(x, h[r], l[r]);
+        for (int q = 0; q < 4; ++q) split_tf32(rawG[(k4 * 4 + q) * MG + m], h[q], l[q]);
+        const uint32_t off = tile_offset(MG, m, k4 * 4);
+        st_shared_v4(st + off, h[0], h[1], h[2], h[3]);
+        st_shared_v4(st + S::kA + off, l[0], l[1], l[2], l[3]);
       }
-      const uint32_t off = tile_offset(NPAD, n, k4 * 4);
-      st_shared_v4(st + 2 * S::kA + off, h[0], h[1], h[2], h[3]);
-      st_shared_v4(st + 2 * S::kA + S::kB + off, l[0], l[1], l[2], l[3]);
+      // B' = [X | Hm | 1]^T (ones column at n = in + H -> bias gradient)
+      for (int task = tid; task < NPAD * (kKW / 4); task += kWgConv) {
+        const int n = task % NPAD, k4 = task / NPAD;
+        float h[4], l[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int rr = k4 * 4 + q;
+          float x = 0.f;
+          if (n < in) x = rawX[rr * in + n];
+          else if (n < KXH) x = rawH[rr * H + (n - in)];
+          else if (n == KXH && q0c + rr < re) x = 1.f;
+          split_tf32(x, h[q], l[q]);
+        }
+        const uint32_t off = tile_offset(NPAD, n, k4 * 4);
+        st_shared_v4(st + 2 * S::kA + off, h[0], h[1], h[2], h[3]);
+        st_shared_v4(st + 2 * S::kA + S::kB + off, l[0], l[1], l[2], l[3]);
+      }
+      fence_async_smem();
+      mbar_arrive(&full[s]);
+      mbar_arrive(&rawempty[r]);
     }
-    fence_async_smem();
-    cp_async_wait<S::kRawSlots - 2>();  // own copies of raw chunk c+1 landed
-    __syncthreads();  // stage s complete for the MMA; raw chunk c+1 visible
-    if (tid == 0) {
+  } else if (lane == 0) {
+    // ---------------- MMA issuer (warp 8)
+    constexpr uint32_t idesc = idesc_tf32(128, NPAD);
+    constexpr uint32_t lboA = tile_lbo(MG), lboB = tile_lbo(NPAD);
+    for (int c = 0; c < nchunks; ++c) {
+      const uint32_t s = c % S::kStages;
+      mbar_wait(&full[s], (c / S::kStages) & 1u);
       fence_after_sync();
+      const uint32_t st = sbase + s * S::kStage;
 #pragma unroll
       for (int ks = 0; ks < kKW / 8; ++ks) {
         const uint64_t bhi = make_desc(st + 2 * S::kA + 2 * ks * lboB, lboB, 128);
@@ -643,35 +674,37 @@ k_wgrad(int M, int in, int H, const float* __restrict__ G, const float* __restri
           mma_tf32(d, alo, bhi, idesc, 1u);
         }
       }
-      commit(&bars[s]);
+      commit(&empty[s]);
     }
+    if (nchunks > 0) commit(done);
   }
-  cp_async_wait<0>();
-  float* out = ws + static_cast<int64_t>(blockIdx.x) * MG * NPAD;
-  if (nchunks > 0) {
-    mbar_wait(&bars[(nchunks - 1) % S::kStages], ((nchunks - 1) / S::kStages) & 1u);
-    fence_after_sync();
-  }
-  const int q = warp & 3, half = warp >> 2;
-  for (int hf = 0; hf < kHalves; ++hf) {
-    const int m = hf * 128 + q * 32 + lane;
-    const uint32_t trow = tmem + hf * 256 + (static_cast<uint32_t>(q * 32) << 16);
-    for (int cb = half * 16; cb < NPAD; cb += 32) {
-      float a[16];
-      if (nchunks > 0) {
-        tmem_ld16(trow + cb, a);
-        tmem_wait_ld();
-      } else {
+  // ---------------- TMEM partial -> workspace (warps 0-7)
+  if (warp < 8) {
+    float* out = ws + static_cast<int64_t>(blockIdx.x) * MG * NPAD;
+    if (nchunks > 0) {
+      mbar_wait(done, 0);
+      fence_after_sync();
+    }
+    const int q = warp & 3, half = warp >> 2;
+    for (int hf = 0; hf < kHalves; ++hf) {
+      const int m = hf * 128 + q * 32 + lane;
+      const uint32_t trow = tmem + hf * 256 + (static_cast<uint32_t>(q * 32) << 16);
+      for (int cb = half * 16; cb < NPAD; cb += 32) {
+        float a[16];
+        if (nchunks > 0) {
+          tmem_ld16(trow + cb, a);
+          tmem_wait_ld();
+        } else {
 #pragma unroll
-        for (int u = 0; u < 16; ++u) a[u] = 0.f;
+          for (int u = 0; u < 16; ++u) a[u] = 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 16; u += 4)
+          *reinterpret_cast<float4*>(out + static_cast<int64_t>(m) * NPAD + cb + u) =
+              make_float4(a[u], a[u + 1], a[u + 2], a[u + 3]);
       }
-#pragma unroll
-      for (int u = 0; u < 16; u += 4)
-        *reinterpret_cast<float4*>(out + static_cast<int64_t>(m) * NPAD + cb + u) =
-            make_float4(a[u], a[u + 1], a[u + 2], a[u + 3]);
     }
   }
-  tmem_wait_ld();
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
