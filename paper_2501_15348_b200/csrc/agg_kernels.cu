@@ -16,6 +16,7 @@
 #include "agg_kernels.h"
 #include "common.cuh"
 
+#include <algorithm>
 #include <cfloat>
 #include <cstdint>
 #include <cstdlib>
@@ -410,7 +411,7 @@ template <int V, int G, bool MEAN>
 __global__ void __launch_bounds__(kThreads)
 k_agg_backward(int n, int w, int c0, int wc, const int64_t* __restrict__ ptr,
                const int32_t* __restrict__ idx, const float* __restrict__ up,
-               const float* __restrict__ degree, float* __restrict__ grad) {
+               const float* __restrict__ degree, float* grad, const float* addend) {
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
   constexpr int kRowsPerWarp = 32 / G;
@@ -428,8 +429,12 @@ k_agg_backward(int n, int w, int c0, int wc, const int64_t* __restrict__ ptr,
       const int c = c0 + (k * G + gl) * V;
       const bool cact = valid && c < cend;
       float acc[V];
+      if (addend != nullptr && cact) {  // addend may alias grad: same element, same thread
+        VecLoad<V>::ld_rw(acc, addend + u * w + c);
+      } else {
 #pragma unroll
-      for (int i = 0; i < V; ++i) acc[i] = 0.f;
+        for (int i = 0; i < V; ++i) acc[i] = 0.f;
+      }
       for (int eb = 0; eb < maxdeg; eb += G) {
         const int my_e = eb + gl;
         const int32_t my_v = my_e < deg ? idx[beg + my_e] : 0;
@@ -616,16 +621,21 @@ void agg_deleted_contributor(int64_t n_del, int w, const uint64_t* del_keys,
 
 void agg_backward(int kind, int n, int w, const int64_t* out_ptr, const int32_t* out_dst,
                   const float* up, const float* degree, const int32_t* argext, float* grad,
-                  cudaStream_t stream) {
+                  cudaStream_t stream, const float* addend) {
   if (n <= 0 || w <= 0) return;
   if (kind == kAggMax || kind == kAggMin) {
-    DGNN_CUDA(cudaMemsetAsync(grad, 0, sizeof(float) * static_cast<size_t>(n) * w, stream));
+    if (addend == nullptr) {
+      DGNN_CUDA(cudaMemsetAsync(grad, 0, sizeof(float) * static_cast<size_t>(n) * w, stream));
+    } else if (addend != grad) {
+      DGNN_CUDA(cudaMemcpyAsync(grad, addend, sizeof(float) * static_cast<size_t>(n) * w,
+                                cudaMemcpyDeviceToDevice, stream));
+    }
     const int64_t total = static_cast<int64_t>(n) * w;
     DGNN_LAUNCH(k_agg_backward_ext, wave_grid(total, 256, 8), 256, 0, stream, total, w, up, argext,
                 grad);
     return;
   }
-  const int vec = pick_vec(w, up, grad);
+  const int vec = std::min(pick_vec(w, up, grad), pick_vec(w, addend, nullptr));
   const int wc = spmm_slice_width(n, w, vec);
   const int g = pick_group(wc, vec);
   const int grid = rows_grid(n, g);
@@ -633,11 +643,11 @@ void agg_backward(int kind, int n, int w, const int64_t* out_ptr, const int32_t*
     if (kind == kAggMean) {
       DGNN_DISPATCH_V(vec, DGNN_DISPATCH_G(g,
           DGNN_LAUNCH((k_agg_backward<V, G, true>), grid, kThreads, 0, stream, n, w, c0, wc,
-                      out_ptr, out_dst, up, degree, grad)));
+                      out_ptr, out_dst, up, degree, grad, addend)));
     } else {
       DGNN_DISPATCH_V(vec, DGNN_DISPATCH_G(g,
           DGNN_LAUNCH((k_agg_backward<V, G, false>), grid, kThreads, 0, stream, n, w, c0, wc,
-                      out_ptr, out_dst, up, degree, grad)));
+                      out_ptr, out_dst, up, degree, grad, addend)));
     }
   }
 }

@@ -39,10 +39,13 @@ void agg_deleted_contributor(int64_t n_del, int w, const uint64_t* del_keys,
                              const int32_t* argext, int32_t* flag, cudaStream_t stream);
 
 // grad[u] = sum over out-neighbours v of u of s_v * up[v] (sum: s=1, mean:
-// s=1/degree[v]); max/min scatter up[v,d] to argext[v,d].
+// s=1/degree[v]); max/min scatter up[v,d] to argext[v,d]. With `addend`
+// (may alias grad) the result is added to it: grad = addend + ... — the GRU
+// skip gradient and the layer-input gradient accumulate without a separate
+// read-modify-write pass.
 void agg_backward(int kind, int n, int w, const int64_t* out_ptr, const int32_t* out_dst,
                   const float* up, const float* degree, const int32_t* argext, float* grad,
-                  cudaStream_t stream);
+                  cudaStream_t stream, const float* addend = nullptr);
 
 // out = in with rows whose argext[v,0] < 0 zeroed (AggResult::dense_values,
 // ref src/aggregate.cpp:30-37, and the empty-row gradient stop, src/cells.cpp:222-229).

@@ -336,6 +336,54 @@ k_mae(int n, int d, int r0, int r1, const float* __restrict__ pred, const float*
   if (threadIdx.x == 0) ws[blockIdx.x] = red[0];
 }
 
+// 128-bit variant (d % 4 == 0, aligned): four float4 pairs in flight per
+// thread per iteration — the scalar loop left too few bytes in flight to
+// stream 2 x 2 GB at C4 (4 ms per call, now bandwidth-bound).
+__global__ void __launch_bounds__(512)
+k_mae4(int64_t total4, int d4, int64_t lo4, int64_t hi4, const float4* __restrict__ pred,
+       const float4* __restrict__ target, float4* __restrict__ dpred, float gscale,
+       double* __restrict__ ws) {
+  __shared__ double red[512];
+  double acc = 0.0;
+  constexpr int U = 4;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i0 < total4;
+       i0 += stride * U) {
+    float4 pv[U], tv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < total4) {
+        pv[u] = __ldg(pred + i);
+        tv[u] = __ldg(target + i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i >= total4) continue;
+      float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i >= lo4 && i < hi4) {
+        const float dx = pv[u].x - tv[u].x, dy = pv[u].y - tv[u].y;
+        const float dz = pv[u].z - tv[u].z, dw = pv[u].w - tv[u].w;
+        acc += fabs(static_cast<double>(dx)) + fabs(static_cast<double>(dy)) +
+               fabs(static_cast<double>(dz)) + fabs(static_cast<double>(dw));
+        auto sg = [&](float v) { return v > 0.f ? gscale : (v < 0.f ? -gscale : 0.f); };
+        g = make_float4(sg(dx), sg(dy), sg(dz), sg(dw));
+      }
+      dpred[i] = g;
+    }
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 256; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) ws[blockIdx.x] = red[0];
+  (void)d4;
+}
+
 __global__ void k_mae_finish(int nblocks, const double* __restrict__ ws, double scale,
                              double* __restrict__ loss_out) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
@@ -543,7 +591,15 @@ void mae_loss(int n, int d, int r0, int r1, const float* pred, const float* targ
               double inv_h, double* loss_out, double* ws, cudaStream_t stream) {
   const double n_el = static_cast<double>(r1 - r0) * d;
   const float gscale = static_cast<float>(1.0 / n_el * inv_h);
-  DGNN_LAUNCH(k_mae, kLossBlocks, 256, 0, stream, n, d, r0, r1, pred, target, dpred, gscale, ws);
+  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  if (d % 4 == 0 && al16(pred) && al16(target) && al16(dpred)) {
+    const int64_t d4 = d / 4;
+    DGNN_LAUNCH(k_mae4, kLossBlocks, 512, 0, stream, static_cast<int64_t>(n) * d4, static_cast<int>(d4),
+                r0 * d4, r1 * d4, reinterpret_cast<const float4*>(pred),
+                reinterpret_cast<const float4*>(target), reinterpret_cast<float4*>(dpred), gscale, ws);
+  } else {
+    DGNN_LAUNCH(k_mae, kLossBlocks, 256, 0, stream, n, d, r0, r1, pred, target, dpred, gscale, ws);
+  }
   DGNN_LAUNCH(k_mae_finish, 1, 32, 0, stream, kLossBlocks, ws, inv_h / n_el, loss_out);
 }
 

@@ -401,7 +401,7 @@ IncrementalResult aggregate_incremental(const AggResult& prev, const GraphView& 
 
 void aggregate_backward(const GraphView& graph, const float* upstream, int32_t dim,
                         const AggrFn& fn, const AggResult& forward, float* grad,
-                        cudaStream_t stream) {
+                        cudaStream_t stream, const float* addend) {
   check(!fn.edge_weighted, "edge-weighted aggregation over an unweighted view");
   if (fn.kind == AggrKind::kMean) {
     check(forward.degree.size() == static_cast<size_t>(graph.num_nodes),
@@ -412,10 +412,11 @@ void aggregate_backward(const GraphView& graph, const float* upstream, int32_t d
           "max/min backward needs forward argext");
   }
   const double bytes = 8.0 * (graph.num_nodes + 1) + 4.0 * graph.num_edges +
-                       4.0 * dim * graph.num_edges + 4.0 * dim * graph.num_nodes;
+                       4.0 * dim * graph.num_edges + 4.0 * dim * graph.num_nodes +
+                       (addend ? 4.0 * dim * graph.num_nodes : 0.0);
   ProfScope ps(kProfAggBackward, stream, bytes);
   cuda::agg_backward(kind_i(fn.kind), graph.num_nodes, dim, graph.out_ptr, graph.out_dst, upstream,
-                     forward.degree.get(), forward.argext.get(), grad, stream);
+                     forward.degree.get(), forward.argext.get(), grad, stream, addend);
 }
 
 }  // namespace dgnn

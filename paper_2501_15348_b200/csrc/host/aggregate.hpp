@@ -110,7 +110,7 @@ IncrementalResult aggregate_incremental(const AggResult& prev, const GraphView& 
 // (ref src/aggregate.cpp:209-246).
 void aggregate_backward(const GraphView& graph, const float* upstream, int32_t dim,
                         const AggrFn& fn, const AggResult& forward, float* grad,
-                        cudaStream_t stream);
+                        cudaStream_t stream, const float* addend = nullptr);
 
 // Per-kernel-class device timing (bench.py roofline): when enabled, the
 // wrappers bracket kernels with CUDA events and accumulate durations and

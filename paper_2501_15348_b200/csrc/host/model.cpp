@@ -552,7 +552,10 @@ struct StepGrads {
 // route dX/dHm back through aggregate_backward; null for dense steps.
 StepGrads cell_step_backward(CellSlot& c, const CellTape& tape, const float* X, const float* Hm,
                              const AggResult* agg_x, const AggResult* agg_h, const GraphView* view,
-                             const Buf& dh, const Buf& dc, bool need_dx, Grads& g, cudaStream_t st) {
+                             const Buf& dh, const Buf& dc, bool need_dx, Grads& g, cudaStream_t st,
+                             float* dx_into = nullptr) {
+  // dx_into (graph steps): accumulate the input gradient straight into the
+  // layer below's running dh instead of returning dx
   const NodeId n = view ? view->num_nodes : static_cast<NodeId>(tape.h->size() / c.H);
   const int H = c.H, in = c.in;
   Buf G = new_buf(static_cast<size_t>(n) * 4 * H, st);
@@ -621,12 +624,17 @@ StepGrads cell_step_backward(CellSlot& c, const CellTape& tape, const float* X, 
   if (agg_x->extremal() && need_dx)
     cuda::mask_empty_rows(n, in, agg_x->argext.get(), dX->get(), dX->get(), st);
   if (agg_h->extremal()) cuda::mask_empty_rows(n, H, agg_h->argext.get(), dHm->get(), dHm->get(), st);
+  // GRU: dh_prev = A^T dHm + dh_skip, the skip term added inside the SpMM
   out.dh_prev = new_buf(static_cast<size_t>(n) * H, st);
-  aggregate_backward(*view, dHm->get(), H, AggrFn{agg_h->kind}, *agg_h, out.dh_prev->get(), st);
-  if (!c.lstm) cuda::axpy(static_cast<int64_t>(n) * H, 1.f, dh_skip->get(), out.dh_prev->get(), st);
+  aggregate_backward(*view, dHm->get(), H, AggrFn{agg_h->kind}, *agg_h, out.dh_prev->get(), st,
+                     c.lstm ? nullptr : dh_skip->get());
   if (need_dx) {
-    out.dx = new_buf(static_cast<size_t>(n) * in, st);
-    aggregate_backward(*view, dX->get(), in, AggrFn{agg_x->kind}, *agg_x, out.dx->get(), st);
+    if (dx_into != nullptr) {
+      aggregate_backward(*view, dX->get(), in, AggrFn{agg_x->kind}, *agg_x, dx_into, st, dx_into);
+    } else {
+      out.dx = new_buf(static_cast<size_t>(n) * in, st);
+      aggregate_backward(*view, dX->get(), in, AggrFn{agg_x->kind}, *agg_x, out.dx->get(), st);
+    }
   }
   return out;
 }
@@ -669,19 +677,19 @@ void integrated_backward(DgnnModel& model, const SeqSample& sample, const Forwar
     for (int l = D; l >= 1; --l) {
       cudaStream_t st = lanes.of(l);
       const GraphStepTape& tape = tapes[l - 1];
+      // layer l's input gradient accumulates straight into the layer below's
+      // running dh inside the transposed SpMM (no dx buffer, no axpy); with
+      // two lanes that buffer belongs to layer l-1's lane, so the SpMM is
+      // ordered after its last write and before its next use
+      float* dx_into = l > 1 ? dh[l - 2]->get() : nullptr;
+      if (l > 1) lanes.dep(lanes.of(l - 1), st);
       StepGrads sg = cell_step_backward(cells[l - 1], tape.core, tape.agg_x->dense_values(),
                                         tape.agg_h->dense_values(), tape.agg_x.get(),
                                         tape.agg_h.get(), &view, dh[l - 1], lstm ? dc[l - 1] : nullptr,
-                                        l > 1, g[lane_of(l)], st);
+                                        l > 1, g[lane_of(l)], st, dx_into);
+      if (l > 1) lanes.dep(st, lanes.of(l - 1));
       dh[l - 1] = sg.dh_prev;
       if (lstm) dc[l - 1] = sg.dc_prev;
-      if (l > 1) {
-        // dx crosses to layer l-1's lane: ordered by an event, kept alive to the join
-        cudaStream_t down = lanes.of(l - 1);
-        lanes.dep(st, down);
-        cuda::axpy(static_cast<int64_t>(n) * cfg.hidden_dim, 1.f, sg.dx->get(), dh[l - 2]->get(), down);
-        if (down != st) lanes.keep.push_back(sg.dx);
-      }
       // layer-1 inputs are data or stop-gradient feedback: dx is never formed
     }
   };
