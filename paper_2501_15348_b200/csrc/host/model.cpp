@@ -250,6 +250,15 @@ std::unique_ptr<DgnnModel> DgnnModel::create(const ModelConfig& cfg, cudaStream_
   m->head_.off_b = off;
   add_slot("head/b");
   m->head_.WT = cuda::DevArray<float>(static_cast<size_t>(H) * d, stream);
+  {
+    LinearSlot& h = m->head_;
+    h.umma = cuda::umma_enabled() && h.in % 16 == 0 && h.out % 16 == 0 && h.out <= 256;
+    h.umma_wgrad = h.umma && (h.out == 128 || h.out == 256) && h.in % 4 == 0 && h.in + h.out / 4 <= 192;
+    if (h.umma) {
+      h.Bf = cuda::DevArray<float>(cuda::umma_bimage_floats(h.out, h.in), stream);
+      h.Bb = cuda::DevArray<float>(cuda::umma_bimage_floats(h.in, h.out), stream);
+    }
+  }
   m->num_params_ = off;
   m->params_ = cuda::DevArray<float>(off, stream);
   m->unflatten_params(m->init_);
@@ -287,6 +296,11 @@ void DgnnModel::refresh_packed() {
   for (auto& c : rnn_) pack(c);
   for (auto& g : gcn_) cuda::transpose(g.in, g.out, params_.get() + g.off_w, g.WT.get(), stream_);
   cuda::transpose(head_.in, head_.out, params_.get() + head_.off_w, head_.WT.get(), stream_);
+  if (head_.umma) {
+    const float* W = params_.get() + head_.off_w;  // in x out, row-major
+    cuda::umma_pack_b(W, head_.out, true, 0, head_.out, head_.in, head_.Bf.get(), stream_);   // W^T
+    cuda::umma_pack_b(W, head_.out, false, 0, head_.in, head_.out, head_.Bb.get(), stream_);  // W
+  }
 }
 
 SeqSample build_sample(const DeviceGraph& graph, const ModelConfig& mcfg,
@@ -383,8 +397,13 @@ Buf linear_forward(DgnnModel& m, const LinearSlot& lin, NodeId n, const float* x
                    cudaStream_t st) {
   Buf y = new_buf(static_cast<size_t>(n) * lin.out, st);
   ProfScope ps(kProfOther, st, 4.0 * n * (lin.in + lin.out), 2.0 * n * lin.in * lin.out);
-  cuda::gemm_nn(n, lin.in, 0, lin.out, 0, x, nullptr, m.params() + lin.off_w, lin.out,
-                m.params() + lin.off_b, relu, false, y->get(), nullptr, st);
+  if (lin.umma && !relu) {
+    cuda::umma_gemm_store2(n, lin.in, x, lin.Bf.get(), lin.out, 0, y->get(), nullptr, st,
+                           m.params() + lin.off_b);
+  } else {
+    cuda::gemm_nn(n, lin.in, 0, lin.out, 0, x, nullptr, m.params() + lin.off_w, lin.out,
+                  m.params() + lin.off_b, relu, false, y->get(), nullptr, st);
+  }
   return y;
 }
 
@@ -538,8 +557,13 @@ struct Grads {
 void linear_param_grads(DgnnModel& m, const LinearSlot& lin, NodeId n, const float* x,
                         const float* dy, Grads& g, cudaStream_t st) {
   ProfScope ps(kProfWeightGrad, st, 4.0 * n * (lin.in + lin.out), 2.0 * n * lin.in * lin.out);
-  cuda::gemm_tn_acc(n, lin.in, 0, lin.out, x, nullptr, dy, g.flat + lin.off_w, lin.out,
-                    g.flat + lin.off_b, g.ws, st);
+  if (lin.umma_wgrad) {  // dW (in x out) += x^T dy, db += colsum(dy): out = 4 * (out / 4)
+    cuda::umma_wgrad(n, lin.in, lin.out / 4, dy, x, nullptr, g.flat + lin.off_w, lin.out,
+                     g.flat + lin.off_b, g.ws, st);
+  } else {
+    cuda::gemm_tn_acc(n, lin.in, 0, lin.out, x, nullptr, dy, g.flat + lin.off_w, lin.out,
+                      g.flat + lin.off_b, g.ws, st);
+  }
   (void)m;
 }
 
@@ -655,8 +679,13 @@ void head_backward(DgnnModel& model, NodeId n, const float* h_top, const Buf& dp
   linear_param_grads(model, model.head_, n, h_top, dpred->get(), g, st);
   // dh += dpred * W_head^T
   ProfScope ps(kProfOther, st, 4.0 * n * (model.head_.out + 2 * model.head_.in));
-  cuda::gemm_nn(n, model.head_.out, 0, model.head_.in, 0, dpred->get(), nullptr,
-                model.head_.WT.get(), model.head_.in, nullptr, false, true, dh->get(), nullptr, st);
+  if (model.head_.umma) {
+    cuda::umma_gemm_store2(n, model.head_.out, dpred->get(), model.head_.Bb.get(), model.head_.in, 0,
+                           dh->get(), nullptr, st, nullptr, /*accumulate=*/true);
+  } else {
+    cuda::gemm_nn(n, model.head_.out, 0, model.head_.in, 0, dpred->get(), nullptr,
+                  model.head_.WT.get(), model.head_.in, nullptr, false, true, dh->get(), nullptr, st);
+  }
 }
 
 void integrated_backward(DgnnModel& model, const SeqSample& sample, const ForwardArtifacts& fwd,
@@ -806,6 +835,8 @@ void model_backward(DgnnModel& model, const SeqSample& sample, const ForwardArti
   ws_n = std::max(ws_n, cuda::gemm_tn_workspace(n, H, d));             // head
   for (int in : {d, H})
     if (cuda::umma_cell_supported(in, H)) ws_n = std::max(ws_n, cuda::umma_wgrad_workspace(in, H));
+  if (model.head_.umma_wgrad)
+    ws_n = std::max(ws_n, cuda::umma_wgrad_workspace(model.head_.in, model.head_.out / 4));
   cuda::DevArray<float> ws(ws_n, stream);
   zero_cell_accumulators(model.enc_, stream);
   zero_cell_accumulators(model.dec_, stream);

@@ -97,6 +97,11 @@ struct LinearSlot {
   int64_t off_w = 0, off_b = 0;
   int in = 0, out = 0;
   cuda::DevArray<float> WT;  // out x in
+  // tcgen05 path (the prediction head): B images of W^T (forward, bias in the
+  // epilogue) and W (input gradient, accumulated in the epilogue); the
+  // weight / bias gradient through the weight-gradient kernel
+  bool umma = false, umma_wgrad = false;
+  cuda::DevArray<float> Bf, Bb;
 };
 
 class DgnnModel {

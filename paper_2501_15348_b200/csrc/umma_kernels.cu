@@ -109,10 +109,11 @@ struct RowGemmArgs {
   const float* dc;
   float* G;
   float* dstate;
-  // store2 epilogue
+  // store2 epilogue (optional bias over C1's columns, C1 += result)
   int n1, n2;
   float* C1;
   float* C2;
+  int store_accumulate;
   // profiling switches (env DGNN_UMMA_DEBUG): 1 skip epilogue math/stores,
   // 2 skip the B copy, 4 skip the A split/stores
   int debug;
@@ -193,6 +194,7 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
   }
   float* sbias = reinterpret_cast<float*>(smem + S::kBias);
   if (kEpiCell<EPI> && tid < 4 * p.H) sbias[tid] = p.bias[tid];
+  if (EPI == kEpiStore2 && p.bias != nullptr && tid < p.n1) sbias[tid] = p.bias[tid];
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
@@ -480,8 +482,23 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
           float a[16];
           tmem_ld16(trow + cb, a);
           tmem_wait_ld();
-          if (cb < p.n1) stage_store(a, p.C1, p.n1, cb);
-          else stage_store(a, p.C2, p.n2, cb - p.n1);
+          if (cb < p.n1) {
+            if (p.bias != nullptr) {
+#pragma unroll
+              for (int u = 0; u < 16; ++u) a[u] += sbias[cb + u];
+            }
+            if (p.store_accumulate && row < p.M) {
+              const float* ep = p.C1 + row * p.n1 + cb;
+#pragma unroll
+              for (int u = 0; u < 16; u += 4) {
+                const float4 e = *reinterpret_cast<const float4*>(ep + u);
+                a[u] += e.x; a[u + 1] += e.y; a[u + 2] += e.z; a[u + 3] += e.w;
+              }
+            }
+            stage_store(a, p.C1, p.n1, cb);
+          } else {
+            stage_store(a, p.C2, p.n2, cb - p.n1);
+          }
         }
       } else {
         const int ncol = p.n1 + p.n2;
@@ -601,7 +618,8 @@ k_wgrad(int M, int in, int H, const float* __restrict__ G, const float* __restri
       const int live = static_cast<int>(re - q0 < kKW ? re - q0 : kKW);
       copy_region(slot, G + q0 * MG, MG, live);
       copy_region(slot + kKW * MG * 4, X + q0 * in, in, live);
-      copy_region(slot + kKW * (MG + in) * 4, Hm + q0 * H, H, live);
+      // Hm absent (a plain linear layer's weight gradient): zero columns
+      copy_region(slot + kKW * (MG + in) * 4, Hm ? Hm + q0 * H : G, H, Hm ? live : 0);
       cp_async_mbar_arrive_noinc(&rawfull[r]);  // completes when every copier's copies landed
     };
     for (int c = 0; c < S::kRawSlots - 1 && c < nchunks; ++c) issue(c);
@@ -712,8 +730,9 @@ k_wgrad(int M, int in, int H, const float* __restrict__ G, const float* __restri
 }
 
 // dW[k][m] += sum_cta D'[cta][m][k] (k < in+H); db[m] += sum_cta D'[cta][m][in+H] (m < nb)
-__global__ void k_wgrad_reduce(int nctas, int MG, int NPAD, int KXH, int nb, const float* __restrict__ ws,
-                               float* __restrict__ dW, float* __restrict__ db) {
+__global__ void k_wgrad_reduce(int nctas, int MG, int NPAD, int KXH, int wrows, int nb,
+                               const float* __restrict__ ws, float* __restrict__ dW,
+                               float* __restrict__ db) {
   const int64_t total = static_cast<int64_t>(MG) * (KXH + 1);
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -722,7 +741,7 @@ __global__ void k_wgrad_reduce(int nctas, int MG, int NPAD, int KXH, int nb, con
     float acc = 0.f;
     for (int c = 0; c < nctas; ++c) acc += ws[(static_cast<int64_t>(c) * MG + m) * NPAD + k];
     if (k < KXH) {
-      dW[static_cast<int64_t>(k) * MG + m] += acc;
+      if (k < wrows) dW[static_cast<int64_t>(k) * MG + m] += acc;
     } else if (m < nb) {
       db[m] += acc;
     }
@@ -840,8 +859,12 @@ void umma_cell_backward_recompute(bool lstm, int n, int in, int H, const float* 
 }
 
 void umma_gemm_store2(int n, int K, const float* A, const float* Bimg, int n1, int n2, float* C1,
-                      float* C2, cudaStream_t stream) {
+                      float* C2, cudaStream_t stream, const float* bias, bool accumulate) {
+  if ((bias || accumulate) && !(n1 % 16 == 0 && n2 % 16 == 0 && n1 <= 256))
+    throw std::invalid_argument("umma_gemm_store2: bias / accumulate need 16-column blocks");
   RowGemmArgs a{};
+  a.bias = bias;
+  a.store_accumulate = accumulate ? 1 : 0;
   a.M = n;
   a.k1 = K;
   a.k2 = 0;
@@ -889,8 +912,8 @@ void umma_wgrad(int n, int in, int H, const float* G, const float* X, const floa
     else go(std::integral_constant<int, 128>{}, std::integral_constant<int, 256>{});
   }
   const int64_t total = static_cast<int64_t>(4 * H) * (in + H + 1);
-  DGNN_LAUNCH(k_wgrad_reduce, wave_grid(total, 256, 4), 256, 0, stream, grid, 4 * H, npad, in + H, nb,
-              ws, dW, db);
+  DGNN_LAUNCH(k_wgrad_reduce, wave_grid(total, 256, 4), 256, 0, stream, grid, 4 * H, npad, in + H,
+              Hm ? in + H : in, nb, ws, dW, db);
 }
 
 }  // namespace cuda

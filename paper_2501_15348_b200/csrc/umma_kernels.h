@@ -35,11 +35,15 @@ void umma_cell_backward_recompute(bool lstm, int n, int in, int H, const float* 
                                   const float* bias, const float* dh, const float* dc, float* G,
                                   float* dstate, cudaStream_t stream);
 
-// [C1 | C2] = A (n x K) * B^T with B the packed (n1+n2) x K image.
+// [C1 | C2] = A (n x K) * B^T with B the packed (n1+n2) x K image; with
+// `bias` (n1 entries) C1 gets + bias, with `accumulate` C1 += the product
+// (both need 16-column blocks).
 void umma_gemm_store2(int n, int K, const float* A, const float* Bimg, int n1, int n2, float* C1,
-                      float* C2, cudaStream_t stream);
+                      float* C2, cudaStream_t stream, const float* bias = nullptr,
+                      bool accumulate = false);
 
 // dW ((in+H) x 4H) += [X|Hm]^T G, db (nb) += colsum(G[:, :nb]); deterministic.
+// Hm == nullptr: a plain linear layer's gradient, dW (in x 4H) += X^T G.
 int64_t umma_wgrad_workspace(int in, int H);
 void umma_wgrad(int n, int in, int H, const float* G, const float* X, const float* Hm, float* dW,
                 int nb, float* db, float* ws, cudaStream_t stream);

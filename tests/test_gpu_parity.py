@@ -361,6 +361,23 @@ def test_layer_lanes_match_reference(ref, api, pair, monkeypatch, arch):
     _events_match(s1.cache_events(), r.events)
 
 
+@pytest.mark.parametrize("arch", ["gcrn_m2", "tgcn"])
+@pytest.mark.parametrize("dim", [32, 128])
+def test_sample_grads_tensor_core_head(ref, api, arch, dim):
+    """Feature dims 32 / 128: the prediction head runs on tcgen05 (bias and
+    accumulate epilogues; at 128 its weight / bias gradient too), C3/C4
+    feature width included."""
+    g_ref, g = make_pair(ref, api, n=257, avg_degree=5, dim=dim, T=11, edge=0.05, feat=0.05, seed=4)
+    cfg_r = ref.RunCfg(arch=arch, hidden=64)
+    s = api.TrainSession(g, api.TrainConfig(arch=arch, hidden=64))
+    for w in (0, 1):
+        loss_r, pred_r, grads_r = g_ref.sample_grads(cfg_r, w)
+        loss, pred, grads = s.sample_grads(w)
+        assert abs(loss - loss_r) <= 1e-5 * abs(loss_r), (loss, loss_r)
+        assert nrel(pred, pred_r) < 1e-5
+        assert nrel(grads, grads_r) < 1e-4
+
+
 def test_spmm_column_slices_match_reference(ref):
     """The L2 column-sliced pull SpMMs (forced to 2 and 4 slices) in a fresh
     process, against the reference."""
