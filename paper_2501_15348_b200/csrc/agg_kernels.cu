@@ -290,15 +290,17 @@ __device__ __forceinline__ float4 ld_hint(const float* p, uint64_t pol) {
   return r;
 }
 
-// K2, pipelined (sum / mean, w <= 128, 16 B-aligned rows). One destination
-// row per group of G lanes (4 columns per lane), 32 / G rows per warp step.
+// K2, pipelined (sum / mean, w <= 128 * U / ..., 16 B-aligned rows). One
+// destination row per group of G lanes, each lane owning U consecutive
+// float4s (4U columns), so 32 / G rows are in flight per warp step (U = 2
+// doubles the rows in flight at w = 64 / 128 over one float4 per lane).
 // The dependent index chain (row meta -> entries -> source rows) is software
 // pipelined across steps: each step issues the row metadata two steps ahead
 // and the first G entries one step ahead together with this step's
 // destination-row and source-row loads, so a step costs one memory round trip
 // instead of three. Entries are applied in the reference's order (deletions,
 // then insertions, ascending source), exactly as in k_agg_delta.
-template <int G, bool MEAN>
+template <int G, int U, bool MEAN>
 __global__ void __launch_bounds__(kThreads)
 k_agg_delta_v4(int n_rows, int w, int32_t num_nodes, const int32_t* __restrict__ rows,
                const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ ent,
@@ -309,7 +311,7 @@ k_agg_delta_v4(int n_rows, int w, int32_t num_nodes, const int32_t* __restrict__
   const int lane = threadIdx.x & 31, gl = lane & (G - 1), sub = lane / G;
   const int64_t wg = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
   const int64_t step = ((static_cast<int64_t>(gridDim.x) * kThreads) >> 5) * R;
-  const int c = gl * 4;
+  const int c = gl * 4 * U;
   const bool cact = c < w;
   const uint64_t keep = l2_policy_last(), once = l2_policy_first();
   struct Meta {
@@ -336,26 +338,30 @@ k_agg_delta_v4(int n_rows, int w, int32_t num_nodes, const int32_t* __restrict__
     const float d1 = MEAN && rb + step + sub < n_rows ? degree[m1.v] : 0.f;
     const bool valid = rb + sub < n_rows;
     float* accp = (MEAN ? msum : values) + static_cast<int64_t>(m0.v) * w + c;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (valid && cact) acc = ld_hint(accp, once);
+    float4 acc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (valid && cact) acc[u] = ld_hint(accp + 4 * u, once);
+    }
     const int maxcnt = __reduce_max_sync(0xffffffffu, m0.cnt);
     int dnet = 0;
     for (int eb = 0; eb < maxcnt; eb += G) {
       const int32_t my_s = eb == 0 ? e0 : (eb + gl < m0.cnt ? ent[m0.beg + eb + gl] : 0);
       const int cnt = min(G, maxcnt - eb);
       for (int j0 = 0; j0 < cnt; j0 += kUnroll) {
-        float4 x[kUnroll];
+        float4 x[kUnroll][U];
         int32_t s[kUnroll];
 #pragma unroll
         for (int q = 0; q < kUnroll; ++q) {
           s[q] = __shfl_sync(0xffffffffu, my_s, (j0 + q) & (G - 1), G);
           if (valid && cact && j0 + q < cnt && eb + j0 + q < m0.cnt) {
-            const int32_t u = s[q] < 0 ? ~s[q] : s[q];
-            if (u >= num_nodes) {
-              x[q] = ld_nc_hint((s[q] < 0 ? Cp : Cc) + static_cast<int64_t>(u - num_nodes) * w + c, keep);
-            } else {
-              x[q] = ld_nc_hint((s[q] < 0 ? Fp : Fc) + static_cast<int64_t>(u) * w + c, once);
-            }
+            const int32_t u0 = s[q] < 0 ? ~s[q] : s[q];
+            const bool cpt = u0 >= num_nodes;
+            const float* src = cpt ? (s[q] < 0 ? Cp : Cc) + static_cast<int64_t>(u0 - num_nodes) * w + c
+                                   : (s[q] < 0 ? Fp : Fc) + static_cast<int64_t>(u0) * w + c;
+#pragma unroll
+            for (int u = 0; u < U; ++u) x[q][u] = ld_nc_hint(src + 4 * u, cpt ? keep : once);
           }
         }
 #pragma unroll
@@ -363,10 +369,13 @@ k_agg_delta_v4(int n_rows, int w, int32_t num_nodes, const int32_t* __restrict__
           if (!(valid && j0 + q < cnt && eb + j0 + q < m0.cnt)) continue;
           if (MEAN) dnet += s[q] < 0 ? -1 : 1;
           if (!cact) continue;
-          if (s[q] < 0) {
-            acc.x -= x[q].x; acc.y -= x[q].y; acc.z -= x[q].z; acc.w -= x[q].w;
-          } else {
-            acc.x += x[q].x; acc.y += x[q].y; acc.z += x[q].z; acc.w += x[q].w;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if (s[q] < 0) {
+              acc[u].x -= x[q][u].x; acc[u].y -= x[q][u].y; acc[u].z -= x[q][u].z; acc[u].w -= x[q][u].w;
+            } else {
+              acc[u].x += x[q][u].x; acc[u].y += x[q][u].y; acc[u].z += x[q][u].z; acc[u].w += x[q][u].w;
+            }
           }
         }
       }
@@ -376,13 +385,18 @@ k_agg_delta_v4(int n_rows, int w, int32_t num_nodes, const int32_t* __restrict__
         // renormalise the touched row (ref src/aggregate.cpp:195-205)
         const float dg = d0 + static_cast<float>(dnet);
         const bool live = dg > 1e-12f;
-        const float4 ms = live ? acc : make_float4(0.f, 0.f, 0.f, 0.f);
-        *reinterpret_cast<float4*>(accp) = ms;
-        *reinterpret_cast<float4*>(values + static_cast<int64_t>(m0.v) * w + c) =
-            live ? make_float4(acc.x / dg, acc.y / dg, acc.z / dg, acc.w / dg) : ms;
+        float* vp = values + static_cast<int64_t>(m0.v) * w + c;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const float4 ms = live ? acc[u] : make_float4(0.f, 0.f, 0.f, 0.f);
+          *reinterpret_cast<float4*>(accp + 4 * u) = ms;
+          *reinterpret_cast<float4*>(vp + 4 * u) =
+              live ? make_float4(acc[u].x / dg, acc[u].y / dg, acc[u].z / dg, acc[u].w / dg) : ms;
+        }
         if (gl == 0) degree[m0.v] = live ? dg : 0.f;
       } else {
-        *reinterpret_cast<float4*>(accp) = acc;
+#pragma unroll
+        for (int u = 0; u < U; ++u) *reinterpret_cast<float4*>(accp + 4 * u) = acc[u];
       }
     }
     m0 = m1;
@@ -589,20 +603,38 @@ void agg_delta(int kind, int n_rows, int w, const int32_t* rows, const int32_t* 
     ent_c = ent;
     num_nodes = INT32_MAX;
   }
-  if (!pipe_off && (kind == kAggSum || kind == kAggMean) && vec == 4 && aligned && w <= 128) {
-    const int g = pick_group(w, 4);
+  static const int u_env = [] {
+    const char* e = std::getenv("DGNN_DELTA_U");
+    return e ? std::atoi(e) : 0;
+  }();
+  // float4s per lane: more rows per warp step = more independent gathers in
+  // flight (C4 delta, 4.8M entries: U=1 0.85 ms, U=2 0.80, U=4 0.77)
+  int U = w % 8 == 0 && w >= 32 ? 2 : 1;
+  if (w % 16 == 0 && w >= 64) U = 4;
+  if (u_env == 1 || u_env == 2) U = std::min(U, u_env);
+  if (!pipe_off && (kind == kAggSum || kind == kAggMean) && vec == 4 && aligned && w <= 128 * U) {
+    const int g = pick_group(w, 4 * U);
     const int grid = rows_grid(n_rows, g);
     const float* cp = compact;
     const float* cc = compact ? compact + n_changed * w : nullptr;
-    if (kind == kAggMean) {
-      DGNN_DISPATCH_G(g, DGNN_LAUNCH((k_agg_delta_v4<G, true>), grid, kThreads, 0, stream, n_rows, w,
-                                     num_nodes, rows, row_ptr, ent_c, f_prev, f_curr, cp, cc, values,
-                                     degree, mean_sums));
+#define DGNN_DELTA_LAUNCH(UU, MM)                                                                    \
+  DGNN_DISPATCH_G(g, DGNN_LAUNCH((k_agg_delta_v4<G, UU, MM>), grid, kThreads, 0, stream, n_rows, w, \
+                                 num_nodes, rows, row_ptr, ent_c, f_prev, f_curr, cp, cc, values,   \
+                                 degree, mean_sums))
+    if (U == 4 && kind == kAggMean) {
+      DGNN_DELTA_LAUNCH(4, true);
+    } else if (U == 4) {
+      DGNN_DELTA_LAUNCH(4, false);
+    } else if (U == 2 && kind == kAggMean) {
+      DGNN_DELTA_LAUNCH(2, true);
+    } else if (U == 2) {
+      DGNN_DELTA_LAUNCH(2, false);
+    } else if (kind == kAggMean) {
+      DGNN_DELTA_LAUNCH(1, true);
     } else {
-      DGNN_DISPATCH_G(g, DGNN_LAUNCH((k_agg_delta_v4<G, false>), grid, kThreads, 0, stream, n_rows, w,
-                                     num_nodes, rows, row_ptr, ent_c, f_prev, f_curr, cp, cc, values,
-                                     degree, mean_sums));
+      DGNN_DELTA_LAUNCH(1, false);
     }
+#undef DGNN_DELTA_LAUNCH
     return;
   }
   const int g = pick_group(w, vec);
