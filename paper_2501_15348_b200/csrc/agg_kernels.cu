@@ -406,6 +406,80 @@ k_agg_delta_v4(int n_rows, int w, int32_t num_nodes, const int32_t* __restrict__
   }
 }
 
+// K1 / K3 for sum (the configs' aggregation): out[v] = (addend[v]) + sum over
+// the CSR row of F[u], ascending u. G lanes per row with U float4s each, so
+// 32 / G rows are gathered concurrently per warp (more independent 16 B
+// gathers in flight than one float4 per lane), and the next G indices of a
+// row are loaded before the current batch's gathers are consumed.
+template <int G, int U>
+__global__ void __launch_bounds__(kThreads)
+k_spmm_sum(int n, int w, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+           const float* __restrict__ F, float* out, const float* addend) {
+  constexpr int R = 32 / G;
+  const int lane = threadIdx.x & 31, gl = lane & (G - 1), sub = lane / G;
+  const int64_t warp_global = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+  const int64_t warp_stride = (static_cast<int64_t>(gridDim.x) * kThreads) >> 5;
+  const int c = gl * 4 * U;
+  const bool cin = c < w;
+  for (int64_t vbase = warp_global * R; vbase < n; vbase += warp_stride * R) {
+    const int64_t v = vbase + sub;
+    const bool valid = v < n;
+    const int64_t beg = valid ? ptr[v] : 0;
+    const int deg = valid ? static_cast<int>(ptr[v + 1] - beg) : 0;
+    const int maxdeg = __reduce_max_sync(0xffffffffu, deg);
+    const bool cact = valid && cin;
+    float4 acc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (addend != nullptr && cact) acc[u] = *reinterpret_cast<const float4*>(addend + v * w + c + 4 * u);
+    }
+    int32_t my_u = gl < deg ? idx[beg + gl] : 0;
+    for (int eb = 0; eb < maxdeg; eb += G) {
+      // next batch's indices in flight with this batch's gathers
+      const int32_t nxt_u = eb + G + gl < deg ? idx[beg + eb + G + gl] : 0;
+      const int cnt = min(G, maxdeg - eb);
+      for (int j0 = 0; j0 < cnt; j0 += kUnroll) {
+        float4 x[kUnroll][U];
+#pragma unroll
+        for (int q = 0; q < kUnroll; ++q) {
+          const int32_t uu = __shfl_sync(0xffffffffu, my_u, (j0 + q) & (G - 1), G);
+          if (cact && j0 + q < cnt && eb + j0 + q < deg) {
+            const float* src = F + static_cast<int64_t>(uu) * w + c;
+#pragma unroll
+            for (int u = 0; u < U; ++u) x[q][u] = __ldg(reinterpret_cast<const float4*>(src + 4 * u));
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kUnroll; ++q) {
+          if (!(cact && j0 + q < cnt && eb + j0 + q < deg)) continue;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            acc[u].x += x[q][u].x; acc[u].y += x[q][u].y; acc[u].z += x[q][u].z; acc[u].w += x[q][u].w;
+          }
+        }
+      }
+      my_u = nxt_u;
+    }
+    if (cact) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) *reinterpret_cast<float4*>(out + v * w + c + 4 * u) = acc[u];
+    }
+  }
+}
+
+// U float4s per lane for k_spmm_sum (0: not applicable); DGNN_SPMM_U overrides
+int spmm_u(int w) {
+  static const int env = [] {
+    const char* e = std::getenv("DGNN_SPMM_U");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (env == 0 || w % 4 != 0) return 0;
+  int u = w % 16 == 0 && w >= 64 ? 4 : (w % 8 == 0 && w >= 32 ? 2 : 1);
+  if (env > 0) u = std::min(u, env);
+  return u;
+}
+
 // Deleted-contributor test for max/min (ref src/aggregate.cpp:145-153).
 __global__ void k_deleted_contributor(int64_t n_del, int w, const uint64_t* __restrict__ del_keys,
                                       const int32_t* __restrict__ argext, int32_t* flag) {
@@ -566,6 +640,27 @@ int spmm_slice_width(int n, int w, int vec) {
   return wc;
 }
 
+int rows_grid(int64_t rows, int g);
+
+void launch_spmm_sum(int U, int n, int w, const int64_t* ptr, const int32_t* idx, const float* F,
+                     float* out, const float* addend, cudaStream_t stream) {
+  const int g = pick_group(w, 4 * U);
+  const int grid = rows_grid(n, g);
+  switch (U) {
+    case 4:
+      DGNN_DISPATCH_G(g, DGNN_LAUNCH((k_spmm_sum<G, 4>), grid, kThreads, 0, stream, n, w, ptr, idx, F, out,
+                                     addend));
+      break;
+    case 2:
+      DGNN_DISPATCH_G(g, DGNN_LAUNCH((k_spmm_sum<G, 2>), grid, kThreads, 0, stream, n, w, ptr, idx, F, out,
+                                     addend));
+      break;
+    default:
+      DGNN_DISPATCH_G(g, DGNN_LAUNCH((k_spmm_sum<G, 1>), grid, kThreads, 0, stream, n, w, ptr, idx, F, out,
+                                     addend));
+  }
+}
+
 int rows_grid(int64_t rows, int g) {
   const int64_t rows_per_block = (kThreads / 32) * (32 / g);
   return wave_grid(rows * kThreads / rows_per_block, kThreads, 8);
@@ -578,6 +673,13 @@ void agg_scratch(int kind, int n, int w, const int64_t* in_ptr, const int32_t* i
                  int32_t* argext, cudaStream_t stream) {
   if (n <= 0 || w <= 0) return;
   const int vec = pick_vec(w, feats, values);
+  if (kind == kAggSum && vec == 4 && std::getenv("DGNN_SPMM_L2_MB") == nullptr &&
+      std::getenv("DGNN_SPMM_SLICES") == nullptr) {
+    if (const int U = spmm_u(w)) {
+      launch_spmm_sum(U, n, w, in_ptr, in_src, feats, values, nullptr, stream);
+      return;
+    }
+  }
   const int wc = spmm_slice_width(n, w, vec);
   const int g = pick_group(wc, vec);
   const int grid = rows_grid(n, g);
@@ -668,6 +770,13 @@ void agg_backward(int kind, int n, int w, const int64_t* out_ptr, const int32_t*
     return;
   }
   const int vec = std::min(pick_vec(w, up, grad), pick_vec(w, addend, nullptr));
+  if (kind == kAggSum && vec == 4 && std::getenv("DGNN_SPMM_L2_MB") == nullptr &&
+      std::getenv("DGNN_SPMM_SLICES") == nullptr) {
+    if (const int U = spmm_u(w)) {
+      launch_spmm_sum(U, n, w, out_ptr, out_dst, up, grad, addend, stream);
+      return;
+    }
+  }
   const int wc = spmm_slice_width(n, w, vec);
   const int g = pick_group(wc, vec);
   const int grid = rows_grid(n, g);
