@@ -255,8 +255,9 @@ def main():
     # kernel reported (and the one whose ncu DRAM traffic is in profiles/)
     if dom == "agg_scratch" and prof["agg_backward"]["ms"] >= 0.97 * prof["agg_scratch"]["ms"]:
         dom = "agg_backward"
-    ncu_kernels = {"agg_backward": "k_agg_backward", "agg_scratch": "k_agg_scratch",
-                   "agg_delta": "k_agg_delta"}
+    # kernel names in the committed ncu capture (profiles/r1_ncu_spmm_<workload>.json,
+    # made by scripts/kernel_bench.py at the workload's shapes)
+    ncu_kernels = {"agg_backward": "k_spmm_sum", "agg_delta": "k_agg_delta"}
 
     def ncu_traffic(name):
         """DRAM bytes per launch (dram__bytes_read + write) of this kernel from
@@ -278,6 +279,9 @@ def main():
         peak = peaks["hbm_gbs"]
         return {"kernel": name, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                 "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": ncu_traffic(name),
+                "note": "achieved = algorithmic bytes (SURVEY 8d: every edge gather counted, no reuse) "
+                        "/ device time; peak = measured copy (read+write) bandwidth — a gather-dominated "
+                        "read stream can exceed it; traffic = ncu DRAM read+write bytes per launch",
                 "alg_bytes_per_launch": round(v["bytes"] / v["launches"]),
                 "peak_source": peak_src, "launches": v["launches"],
                 "avg_launch_us": round(per_ms * 1e3, 2),
