@@ -257,7 +257,7 @@ def main():
         dom = "agg_backward"
     # kernel names in the committed ncu capture (profiles/r1_ncu_spmm_<workload>.json,
     # made by scripts/kernel_bench.py at the workload's shapes)
-    ncu_kernels = {"agg_backward": "k_spmm_sum", "agg_delta": "k_agg_delta"}
+    ncu_kernels = {"agg_backward": "k_spmm_sum<4, 4>", "agg_delta": "k_agg_delta"}
 
     def ncu_traffic(name):
         """DRAM bytes per launch (dram__bytes_read + write) of this kernel from

@@ -27,13 +27,35 @@ def timeit(fn, iters):
     return e0.elapsed_time(e1) / iters
 
 
+def prof_time(fn, iters, res):
+    from torch.profiler import ProfilerActivity, profile
+    fn()
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(iters):
+            fn()
+        torch.cuda.synchronize()
+    tot = 0.0
+    for ev in prof.key_averages():
+        if ev.device_type.name == "CUDA" and ev.count > 0:
+            us = ev.device_time_total / ev.count if hasattr(ev, "device_time_total") else ev.cuda_time_total / ev.count
+            res.setdefault("kernels", {})[ev.key[:60]] = {"launches": ev.count, "mean_us": round(us, 1)}
+            tot += us * ev.count
+    return tot / iters / 1e3
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="")
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--d", type=int, default=128)
+    ap.add_argument("--prof", action="store_true", help="per-kernel mean device times (torch.profiler / CUPTI)")
     args = ap.parse_args()
-    n, d, H = args.n, 128, 64
+    n, d, H = args.n, args.d, 64
+    global timeit
+    if args.prof:
+        timeit = lambda fn, iters: prof_time(fn, iters, res)
     res = {}
     torch.manual_seed(0)
     want = lambda k: not args.only or k in args.only.split(",")
@@ -71,7 +93,7 @@ def main():
         res["agg_delta_feat"] = {"ms": ms, "GBps_alg": alg / ms / 1e6, "alg_bytes": alg, **sz}
     for lstm in (True, False):
         name = "cell_fwd_lstm" if lstm else "cell_fwd_gru"
-        if not want(name) and not want("cell_bwd") and not want("wgrad"):
+        if not want(name) and not want("cell_bwd") and not want("wgrad") and not want("cell_bwd_gru"):
             continue
         X = torch.randn(n, d, device="cuda")
         Hm = torch.randn(n, H, device="cuda")
@@ -83,11 +105,13 @@ def main():
             ms = timeit(lambda: api.cell_forward(lstm, X, Hm, hs, cp, flat), args.iters)
             byts = 4 * n * (d + H + 4 * H + H + (2 * H if lstm else H))
             res[name] = {"ms": ms, "GBps_alg": byts / ms / 1e6, "TFLOPs": 2 * n * (d + H) * 4 * H / ms / 1e9}
-        if lstm and (want("cell_bwd") or want("wgrad")):
+        if want("cell_bwd") or want("wgrad") or (not lstm and want("cell_bwd_gru")):
+            if not lstm and not want("cell_bwd_gru"):
+                continue
             fwd = api.cell_forward(lstm, X, Hm, hs, cp, flat)
             dh, dc = torch.randn(n, H, device="cuda"), torch.randn(n, H, device="cuda")
             ms = timeit(lambda: api.cell_backward(lstm, X, Hm, fwd, hs, cp, dh, dc), args.iters)
-            res["cell_bwd_total"] = {"ms": ms, "TFLOPs": 2 * 2 * n * (d + H) * 4 * H / ms / 1e9}
+            res["cell_bwd_total" if lstm else "cell_bwd_gru_total"] = {"ms": ms, "TFLOPs": 2 * 2 * n * (d + H) * 4 * H / ms / 1e9}
     print(json.dumps(res, indent=1))
 
 
