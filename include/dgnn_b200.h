@@ -30,6 +30,7 @@ extern "C" {
 typedef struct dgnn_graph dgnn_graph;
 typedef struct dgnn_synth dgnn_synth;
 typedef struct dgnn_session dgnn_session;
+typedef struct dgnn_dataset dgnn_dataset;
 
 const char* dgnn_last_error(void);
 const char* dgnn_version(void);
@@ -97,6 +98,33 @@ int dgnn_synth_step(const dgnn_synth* s, int32_t t, const int32_t** del_src,
                     const int32_t** changed, const float** changed_feats);
 /* Uploads the compact graph and builds every snapshot + delta on the device. */
 int dgnn_synth_to_graph(const dgnn_synth* s, void* stream, dgnn_graph** out);
+
+/* ---------------------------------------------------------------- dataset
+ * Replaces dgnn::save_dataset / load_dataset (inc/dataset_io.hpp:6-24,
+ * src/dataset_io.cpp:40-165). format 1 = the reference's text layout
+ * (byte-identical writer, same parser rules and messages); format 2 = binary
+ * twin (manifest "format_version":2, "encoding":"b200-le"; *.bin files).
+ * Host-only reader (no GPU needed): open / info / read_base / read_step;
+ * views stay valid until the next read on the same handle. */
+int dgnn_dataset_open(const char* dir, int32_t threads, dgnn_dataset** out);
+void dgnn_dataset_free(dgnn_dataset* d);
+int dgnn_dataset_info(const dgnn_dataset* d, int32_t* num_nodes, int32_t* feature_dim,
+                      int32_t* T, int32_t* format);
+/* snapshot_0: edges in file order, features num_nodes x feature_dim (fp32). */
+int dgnn_dataset_read_base(dgnn_dataset* d, int64_t* num_edges, const int32_t** src,
+                           const int32_t** dst, const float** feats);
+/* delta_t (1 <= t < T): sizes = [n_del, n_ins, n_changed]. */
+int dgnn_dataset_read_step(dgnn_dataset* d, int32_t t, int64_t* sizes, const int32_t** del_src,
+                           const int32_t** del_dst, const int32_t** ins_src,
+                           const int32_t** ins_dst, const int32_t** changed,
+                           const float** changed_feats);
+/* load_dataset into the HBM graph store, streaming (parse t+1 while the
+ * device builds t; host memory bounded by two steps). threads <= 0: auto. */
+int dgnn_dataset_load(const char* dir, int32_t threads, void* stream, dgnn_graph** out);
+/* save_dataset of a device graph (deltas = DynamicGraph::delta(t), expanded). */
+int dgnn_dataset_save_graph(const dgnn_graph* g, const char* dir, int32_t format);
+/* Generator output (structural deltas + redrawn rows; same snapshots on load). */
+int dgnn_synth_save(const dgnn_synth* s, const char* dir, int32_t format);
 
 /* ------------------------------------------------------------ aggregation
  * Kernels K1/K2/K3 over device buffers (src/aggregate.cpp:55-246). */

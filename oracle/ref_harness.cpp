@@ -17,6 +17,7 @@
 #include <string>
 #include <vector>
 
+#include "dgnn/dataset_io.hpp"
 #include "dgnn/distsim.hpp"
 #include "dgnn/synth.hpp"
 #include "dgnn/train.hpp"
@@ -124,6 +125,17 @@ void* ref_graph_from_arrays(int32_t n, int32_t dim, int32_t T, const int64_t* ed
 }
 
 void ref_graph_free(void* g) { delete static_cast<DynamicGraph*>(g); }
+
+// save_dataset / load_dataset (src/dataset_io.cpp:40-165), unmodified.
+int ref_save_dataset(void* g, const char* dir) {
+  return guarded([&] { save_dataset(*static_cast<DynamicGraph*>(g), dir); });
+}
+
+void* ref_load_dataset(const char* dir) {
+  DynamicGraph* out = nullptr;
+  int rc = guarded([&] { out = new DynamicGraph(load_dataset(dir)); });
+  return rc == 0 ? out : nullptr;
+}
 
 int32_t ref_graph_length(void* g) { return static_cast<DynamicGraph*>(g)->length(); }
 int32_t ref_graph_num_nodes(void* g) { return static_cast<DynamicGraph*>(g)->num_nodes(); }

@@ -106,6 +106,8 @@ def lib():
         "ref_synth": (P, [I32, D, I32, I32, D, D, U64]),
         "ref_graph_from_arrays": (P, [I32, I32, I32, P, P, P, P]),
         "ref_graph_free": (None, [P]),
+        "ref_save_dataset": (C.c_int, [P, C.c_char_p]),
+        "ref_load_dataset": (P, [C.c_char_p]),
         "ref_graph_length": (I32, [P]),
         "ref_graph_num_nodes": (I32, [P]),
         "ref_graph_feature_dim": (I32, [P]),
@@ -180,6 +182,15 @@ class RefGraph:
         dst = np.ascontiguousarray(cat[:, 1])
         feats = np.ascontiguousarray(np.stack(feats_per_t).astype(np.float64))
         return cls(lib().ref_graph_from_arrays(n, dim, T, _p(counts), _p(src), _p(dst), _p(feats)))
+
+    @classmethod
+    def load_dataset(cls, path):
+        """load_dataset (src/dataset_io.cpp:98-165)."""
+        return cls(lib().ref_load_dataset(os.fsencode(path)))
+
+    def save_dataset(self, path):
+        """save_dataset (src/dataset_io.cpp:40-95)."""
+        _check(lib().ref_save_dataset(self.h, os.fsencode(path)))
 
     def __del__(self):
         if getattr(self, "h", None) and _lib is not None:

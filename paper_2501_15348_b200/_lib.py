@@ -61,6 +61,14 @@ SIGNATURES = {
     "dgnn_synth_base": (C.c_int, [P, PP, PP, PP]),
     "dgnn_synth_step": (C.c_int, [P, I32, PP, PP, PP, PP, PP, PP]),
     "dgnn_synth_to_graph": (C.c_int, [P, P, PP]),
+    "dgnn_dataset_open": (C.c_int, [C.c_char_p, I32, PP]),
+    "dgnn_dataset_free": (None, [P]),
+    "dgnn_dataset_info": (C.c_int, [P] + [C.POINTER(I32)] * 4),
+    "dgnn_dataset_read_base": (C.c_int, [P, C.POINTER(I64), PP, PP, PP]),
+    "dgnn_dataset_read_step": (C.c_int, [P, I32, P, PP, PP, PP, PP, PP, PP]),
+    "dgnn_dataset_load": (C.c_int, [C.c_char_p, I32, P, PP]),
+    "dgnn_dataset_save_graph": (C.c_int, [P, C.c_char_p, I32]),
+    "dgnn_synth_save": (C.c_int, [P, C.c_char_p, I32]),
     "dgnn_agg_scratch": (C.c_int, [I32, I32, I32, P, P, P, P, P, P, P, P]),
     "dgnn_agg_delta": (C.c_int, [I32, I32, I32, P, P, P, P, P, P, P, P, P, P]),
     "dgnn_graph_apply_delta": (C.c_int, [P, I32, I32, P, P, P, P, P]),

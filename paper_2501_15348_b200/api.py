@@ -10,6 +10,7 @@ std::invalid_argument), IndexError (std::out_of_range) or DgnnError (CUDA).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -149,6 +150,71 @@ class Synth:
         h = C.c_void_p()
         check(lib().dgnn_synth_to_graph(self.h, _stream_handle(stream), C.byref(h)))
         return DynamicGraph._wrap(h, self.n, self.dim)
+
+
+    def save(self, path, binary=True):
+        """Writes the generator output as a dataset (format 2 binary by default;
+        format 1 = the reference's text layout with structural deltas)."""
+        check(lib().dgnn_synth_save(self.h, os.fsencode(path), 2 if binary else 1))
+
+
+# ---------------------------------------------------------------- datasets
+class Dataset:
+    """Host-side reader of an on-disk dataset (ref load_dataset,
+    src/dataset_io.cpp:98-165): the text layout (format 1) or the binary twin
+    (format 2). Needs no GPU."""
+
+    def __init__(self, path, threads=0):
+        h = C.c_void_p()
+        check(lib().dgnn_dataset_open(os.fsencode(path), threads, C.byref(h)))
+        self.h = h
+        n, d, T, fmt = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+        check(lib().dgnn_dataset_info(self.h, C.byref(n), C.byref(d), C.byref(T), C.byref(fmt)))
+        self.num_nodes, self.feature_dim, self.T, self.format = n.value, d.value, T.value, fmt.value
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None and _lib._lib is not None:
+            lib().dgnn_dataset_free(self.h)
+            self.h = None
+
+    @staticmethod
+    def _arr(p, n, ct=C.c_int32):
+        if n == 0:
+            return np.zeros(0, np.int32 if ct is C.c_int32 else np.float32)
+        return np.ctypeslib.as_array(C.cast(p, C.POINTER(ct)), (n,)).copy()
+
+    def base(self):
+        E = C.c_int64()
+        s, d, f = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        check(lib().dgnn_dataset_read_base(self.h, C.byref(E), C.byref(s), C.byref(d), C.byref(f)))
+        n = self.num_nodes * self.feature_dim
+        return (self._arr(s, E.value), self._arr(d, E.value),
+                self._arr(f, n, C.c_float).reshape(self.num_nodes, self.feature_dim))
+
+    def step(self, t):
+        sizes = np.zeros(3, np.int64)
+        ptrs = [C.c_void_p() for _ in range(6)]
+        check(lib().dgnn_dataset_read_step(self.h, t, _np_ptr(sizes), *[C.byref(p) for p in ptrs]))
+        nd, ni, nc = (int(x) for x in sizes)
+        a = self._arr
+        return {"del_src": a(ptrs[0], nd), "del_dst": a(ptrs[1], nd),
+                "ins_src": a(ptrs[2], ni), "ins_dst": a(ptrs[3], ni), "changed": a(ptrs[4], nc),
+                "changed_feats": a(ptrs[5], nc * self.feature_dim, C.c_float).reshape(nc, self.feature_dim)}
+
+
+def load_dataset(path, stream=None, threads=0) -> "DynamicGraph":
+    """load_dataset (src/dataset_io.cpp:98-165) straight into the HBM graph
+    store, one step at a time."""
+    info = Dataset(path)  # manifest only
+    h = C.c_void_p()
+    check(lib().dgnn_dataset_load(os.fsencode(path), threads, _stream_handle(stream), C.byref(h)))
+    return DynamicGraph._wrap(h, info.num_nodes, info.feature_dim)
+
+
+def save_dataset(graph: "DynamicGraph", path, binary=False):
+    """save_dataset (src/dataset_io.cpp:40-95) of a device graph; format 1
+    (reference text, default) or the binary twin."""
+    check(lib().dgnn_dataset_save_graph(graph.h, os.fsencode(path), 2 if binary else 1))
 
 
 def synthesize(num_nodes, avg_degree, feature_dim, num_snapshots, edge_change, feature_change,

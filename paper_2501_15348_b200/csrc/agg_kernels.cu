@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 namespace dgnn {
@@ -300,8 +301,8 @@ __device__ __forceinline__ float4 ld_hint(const float* p, uint64_t pol) {
 // destination-row and source-row loads, so a step costs one memory round trip
 // instead of three. Entries are applied in the reference's order (deletions,
 // then insertions, ascending source), exactly as in k_agg_delta.
-template <int G, int U, bool MEAN>
-__global__ void __launch_bounds__(kThreads)
+template <int G, int U, bool MEAN, int MINB = 1>
+__global__ void __launch_bounds__(kThreads, MINB)
 k_agg_delta_v4(int n_rows, int w, int32_t num_nodes, const int32_t* __restrict__ rows,
                const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ ent,
                const float* __restrict__ Fp, const float* __restrict__ Fc,
@@ -311,8 +312,11 @@ k_agg_delta_v4(int n_rows, int w, int32_t num_nodes, const int32_t* __restrict__
   const int lane = threadIdx.x & 31, gl = lane & (G - 1), sub = lane / G;
   const int64_t wg = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
   const int64_t step = ((static_cast<int64_t>(gridDim.x) * kThreads) >> 5) * R;
-  const int c = gl * 4 * U;
+  // float4 u of a lane covers columns (u * G + gl) * 4: each load instruction
+  // of a G-lane group reads one contiguous 16G-byte segment of the row
+  const int c = gl * 4;
   const bool cact = c < w;
+  auto col_ok = [&](int u) { return c + 4 * G * u < w; };
   const uint64_t keep = l2_policy_last(), once = l2_policy_first();
   struct Meta {
     int32_t v, beg, cnt;
@@ -342,7 +346,7 @@ k_agg_delta_v4(int n_rows, int w, int32_t num_nodes, const int32_t* __restrict__
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (valid && cact) acc[u] = ld_hint(accp + 4 * u, once);
+      if (valid && col_ok(u)) acc[u] = ld_hint(accp + 4 * G * u, once);
     }
     const int maxcnt = __reduce_max_sync(0xffffffffu, m0.cnt);
     int dnet = 0;
@@ -361,7 +365,8 @@ k_agg_delta_v4(int n_rows, int w, int32_t num_nodes, const int32_t* __restrict__
             const float* src = cpt ? (s[q] < 0 ? Cp : Cc) + static_cast<int64_t>(u0 - num_nodes) * w + c
                                    : (s[q] < 0 ? Fp : Fc) + static_cast<int64_t>(u0) * w + c;
 #pragma unroll
-            for (int u = 0; u < U; ++u) x[q][u] = ld_nc_hint(src + 4 * u, cpt ? keep : once);
+            for (int u = 0; u < U; ++u)
+              if (col_ok(u)) x[q][u] = ld_nc_hint(src + 4 * G * u, cpt ? keep : once);
           }
         }
 #pragma unroll
@@ -371,6 +376,7 @@ k_agg_delta_v4(int n_rows, int w, int32_t num_nodes, const int32_t* __restrict__
           if (!cact) continue;
 #pragma unroll
           for (int u = 0; u < U; ++u) {
+            if (!col_ok(u)) continue;
             if (s[q] < 0) {
               acc[u].x -= x[q][u].x; acc[u].y -= x[q][u].y; acc[u].z -= x[q][u].z; acc[u].w -= x[q][u].w;
             } else {
@@ -388,15 +394,17 @@ k_agg_delta_v4(int n_rows, int w, int32_t num_nodes, const int32_t* __restrict__
         float* vp = values + static_cast<int64_t>(m0.v) * w + c;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
+          if (!col_ok(u)) continue;
           const float4 ms = live ? acc[u] : make_float4(0.f, 0.f, 0.f, 0.f);
-          *reinterpret_cast<float4*>(accp + 4 * u) = ms;
-          *reinterpret_cast<float4*>(vp + 4 * u) =
+          *reinterpret_cast<float4*>(accp + 4 * G * u) = ms;
+          *reinterpret_cast<float4*>(vp + 4 * G * u) =
               live ? make_float4(acc[u].x / dg, acc[u].y / dg, acc[u].z / dg, acc[u].w / dg) : ms;
         }
         if (gl == 0) degree[m0.v] = live ? dg : 0.f;
       } else {
 #pragma unroll
-        for (int u = 0; u < U; ++u) *reinterpret_cast<float4*>(accp + 4 * u) = acc[u];
+        for (int u = 0; u < U; ++u)
+          if (col_ok(u)) *reinterpret_cast<float4*>(accp + 4 * G * u) = acc[u];
       }
     }
     m0 = m1;
@@ -419,8 +427,11 @@ k_spmm_sum(int n, int w, const int64_t* __restrict__ ptr, const int32_t* __restr
   const int lane = threadIdx.x & 31, gl = lane & (G - 1), sub = lane / G;
   const int64_t warp_global = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
   const int64_t warp_stride = (static_cast<int64_t>(gridDim.x) * kThreads) >> 5;
-  const int c = gl * 4 * U;
+  // float4 u of a lane covers columns (u * G + gl) * 4 (coalesced 16G-byte
+  // segments per load instruction)
+  const int c = gl * 4;
   const bool cin = c < w;
+  auto col_ok = [&](int u) { return c + 4 * G * u < w; };
   for (int64_t vbase = warp_global * R; vbase < n; vbase += warp_stride * R) {
     const int64_t v = vbase + sub;
     const bool valid = v < n;
@@ -432,7 +443,8 @@ k_spmm_sum(int n, int w, const int64_t* __restrict__ ptr, const int32_t* __restr
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (addend != nullptr && cact) acc[u] = *reinterpret_cast<const float4*>(addend + v * w + c + 4 * u);
+      if (addend != nullptr && cact && col_ok(u))
+        acc[u] = *reinterpret_cast<const float4*>(addend + v * w + c + 4 * G * u);
     }
     int32_t my_u = gl < deg ? idx[beg + gl] : 0;
     for (int eb = 0; eb < maxdeg; eb += G) {
@@ -447,7 +459,8 @@ k_spmm_sum(int n, int w, const int64_t* __restrict__ ptr, const int32_t* __restr
           if (cact && j0 + q < cnt && eb + j0 + q < deg) {
             const float* src = F + static_cast<int64_t>(uu) * w + c;
 #pragma unroll
-            for (int u = 0; u < U; ++u) x[q][u] = __ldg(reinterpret_cast<const float4*>(src + 4 * u));
+            for (int u = 0; u < U; ++u)
+              if (col_ok(u)) x[q][u] = __ldg(reinterpret_cast<const float4*>(src + 4 * G * u));
           }
         }
 #pragma unroll
@@ -455,6 +468,7 @@ k_spmm_sum(int n, int w, const int64_t* __restrict__ ptr, const int32_t* __restr
           if (!(cact && j0 + q < cnt && eb + j0 + q < deg)) continue;
 #pragma unroll
           for (int u = 0; u < U; ++u) {
+            if (!col_ok(u)) continue;
             acc[u].x += x[q][u].x; acc[u].y += x[q][u].y; acc[u].z += x[q][u].z; acc[u].w += x[q][u].w;
           }
         }
@@ -463,7 +477,8 @@ k_spmm_sum(int n, int w, const int64_t* __restrict__ ptr, const int32_t* __restr
     }
     if (cact) {
 #pragma unroll
-      for (int u = 0; u < U; ++u) *reinterpret_cast<float4*>(out + v * w + c + 4 * u) = acc[u];
+      for (int u = 0; u < U; ++u)
+        if (col_ok(u)) *reinterpret_cast<float4*>(out + v * w + c + 4 * G * u) = acc[u];
     }
   }
 }
@@ -701,6 +716,20 @@ void agg_delta(int kind, int n_rows, int w, const int32_t* rows, const int32_t* 
     const char* e = std::getenv("DGNN_DELTA_PIPE");
     return e && e[0] == '0';
   }();
+  // Optional L2 set-aside for evict_last lines (the compact changed-row
+  // block); DGNN_L2_PERSIST_MB, capped at the device maximum.
+  static const bool l2_once = [] {
+    const char* e = std::getenv("DGNN_L2_PERSIST_MB");
+    if (!e) return false;
+    int dev = 0, mx = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    const size_t want = std::min<size_t>(static_cast<size_t>(std::atof(e) * 1048576.0), static_cast<size_t>(mx));
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+    std::fprintf(stderr, "[dgnn] L2 persisting limit %zu bytes (device max %d)\n", want, mx);
+    return true;
+  }();
+  (void)l2_once;
   if (ent_c == nullptr) {  // no compact block: every source is a full-matrix row
     ent_c = ent;
     num_nodes = INT32_MAX;
@@ -723,8 +752,20 @@ void agg_delta(int kind, int n_rows, int w, const int32_t* rows, const int32_t* 
   DGNN_DISPATCH_G(g, DGNN_LAUNCH((k_agg_delta_v4<G, UU, MM>), grid, kThreads, 0, stream, n_rows, w, \
                                  num_nodes, rows, row_ptr, ent_c, f_prev, f_curr, cp, cc, values,   \
                                  degree, mean_sums))
+    static const int minb = [] {
+      const char* e = std::getenv("DGNN_DELTA_MINB");
+      return e ? std::atoi(e) : 0;
+    }();
     if (U == 4 && kind == kAggMean) {
       DGNN_DELTA_LAUNCH(4, true);
+    } else if (U == 4 && minb == 3) {
+      DGNN_DISPATCH_G(g, DGNN_LAUNCH((k_agg_delta_v4<G, 4, false, 3>), grid, kThreads, 0, stream, n_rows,
+                                     w, num_nodes, rows, row_ptr, ent_c, f_prev, f_curr, cp, cc,
+                                     values, degree, mean_sums))
+    } else if (U == 4 && minb == 4) {
+      DGNN_DISPATCH_G(g, DGNN_LAUNCH((k_agg_delta_v4<G, 4, false, 4>), grid, kThreads, 0, stream, n_rows,
+                                     w, num_nodes, rows, row_ptr, ent_c, f_prev, f_curr, cp, cc,
+                                     values, degree, mean_sums))
     } else if (U == 4) {
       DGNN_DELTA_LAUNCH(4, false);
     } else if (U == 2 && kind == kAggMean) {

@@ -7,8 +7,10 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
+#include "host/dataset_io.hpp"
 #include "host/synth.hpp"
 #include "umma_kernels.h"
 #include "host/train.hpp"
@@ -119,6 +121,35 @@ int guarded(F&& f) {
 }
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// Pinned staging buffer reused across the loader's steps (grown on demand).
+struct PinnedStage {
+  void* p = nullptr;
+  size_t cap = 0;
+  ~PinnedStage() {
+    if (p) cudaFreeHost(p);
+  }
+  template <class T>
+  T* put(size_t& off, const std::vector<T>& v) {
+    T* d = reinterpret_cast<T*>(static_cast<char*>(p) + off);
+    if (!v.empty()) std::memcpy(d, v.data(), v.size() * sizeof(T));
+    off += (v.size() * sizeof(T) + 255) / 256 * 256;
+    return d;
+  }
+  void reserve(size_t bytes) {
+    if (bytes <= cap) return;
+    if (p) DGNN_CUDA(cudaFreeHost(p));
+    p = nullptr;
+    DGNN_CUDA(cudaMallocHost(&p, bytes));
+    cap = bytes;
+  }
+};
+
+size_t staged_bytes(const CompactStep& s) {
+  auto r = [](size_t b) { return (b + 255) / 256 * 256; };
+  return r(s.del_src.size() * 4) + r(s.del_dst.size() * 4) + r(s.ins_src.size() * 4) +
+         r(s.ins_dst.size() * 4) + r(s.changed.size() * 4) + r(s.changed_feats.size() * 4);
+}
 
 }  // namespace
 
@@ -351,6 +382,192 @@ int dgnn_synth_to_graph(const dgnn_synth* s, void* stream, dgnn_graph** out) {
     cuda::release_stream_blocks(g->stream);
     *out = guard.release();
   });
+}
+
+// ---------------------------------------------------------------- dataset
+struct dgnn_dataset {
+  std::unique_ptr<DatasetReader> r;
+  std::vector<int32_t> src, dst;
+  std::vector<float> feats;
+  CompactStep step;
+};
+
+int dgnn_dataset_open(const char* dir, int32_t threads, dgnn_dataset** out) {
+  return guarded([&] {
+    auto d = std::make_unique<dgnn_dataset>();
+    d->r = std::make_unique<DatasetReader>(dir, threads);
+    *out = d.release();
+  });
+}
+
+void dgnn_dataset_free(dgnn_dataset* d) { delete d; }
+
+int dgnn_dataset_info(const dgnn_dataset* d, int32_t* num_nodes, int32_t* feature_dim,
+                      int32_t* T, int32_t* format) {
+  return guarded([&] {
+    const DatasetManifest& m = d->r->manifest();
+    if (num_nodes) *num_nodes = m.num_nodes;
+    if (feature_dim) *feature_dim = m.feature_dim;
+    if (T) *T = m.T;
+    if (format) *format = m.format;
+  });
+}
+
+int dgnn_dataset_read_base(dgnn_dataset* d, int64_t* num_edges, const int32_t** src,
+                           const int32_t** dst, const float** feats) {
+  return guarded([&] {
+    d->r->read_base(d->src, d->dst, d->feats);
+    *num_edges = static_cast<int64_t>(d->src.size());
+    *src = d->src.data();
+    *dst = d->dst.data();
+    *feats = d->feats.data();
+  });
+}
+
+int dgnn_dataset_read_step(dgnn_dataset* d, int32_t t, int64_t* sizes, const int32_t** del_src,
+                           const int32_t** del_dst, const int32_t** ins_src,
+                           const int32_t** ins_dst, const int32_t** changed,
+                           const float** changed_feats) {
+  return guarded([&] {
+    d->r->read_step(t, d->step);
+    const CompactStep& st = d->step;
+    sizes[0] = static_cast<int64_t>(st.del_src.size());
+    sizes[1] = static_cast<int64_t>(st.ins_src.size());
+    sizes[2] = static_cast<int64_t>(st.changed.size());
+    *del_src = st.del_src.data();
+    *del_dst = st.del_dst.data();
+    *ins_src = st.ins_src.data();
+    *ins_dst = st.ins_dst.data();
+    *changed = st.changed.data();
+    *changed_feats = st.changed_feats.data();
+  });
+}
+
+// load_dataset (src/dataset_io.cpp:98-165) into the HBM graph store, one step
+// at a time: a parser thread reads step t+1 while the device builds step t
+// (snapshot CSRs, extract_delta), so host memory holds two steps, never the
+// materialised snapshots.
+int dgnn_dataset_load(const char* dir, int32_t threads, void* stream, dgnn_graph** out) {
+  return guarded([&] {
+    DatasetReader r(dir, threads);
+    const DatasetManifest& m = r.manifest();
+    dgnn_graph* g = nullptr;
+    if (dgnn_graph_create(m.num_nodes, m.feature_dim, stream, &g) != 0)
+      throw std::invalid_argument(g_err);
+    std::unique_ptr<dgnn_graph, void (*)(dgnn_graph*)> guard(g, dgnn_graph_free);
+    {
+      std::vector<int32_t> src, dst;
+      std::vector<float> feats;
+      r.read_base(src, dst, feats);
+      g->g->add_snapshot(src.data(), dst.data(), static_cast<int64_t>(src.size()), feats.data());
+    }
+    CompactStep bufs[2];
+    PinnedStage stage[2];
+    std::exception_ptr perr;
+    auto parse = [&](int32_t t, int slot) {
+      try {
+        r.read_step(t, bufs[slot]);
+      } catch (...) {
+        perr = std::current_exception();
+      }
+    };
+    if (m.T > 1) parse(1, 0);
+    for (int32_t t = 1; t < m.T; ++t) {
+      if (perr) std::rethrow_exception(perr);
+      const int cur = (t - 1) & 1;
+      std::thread next;
+      if (t + 1 < m.T) next = std::thread(parse, t + 1, cur ^ 1);
+      try {
+        const CompactStep& st = bufs[cur];
+        // stage into pinned memory once the previous use of this slot is done
+        DGNN_CUDA(cudaStreamSynchronize(g->stream));
+        stage[cur].reserve(staged_bytes(st));
+        size_t off = 0;
+        const int32_t* ds = stage[cur].put(off, st.del_src);
+        const int32_t* dd = stage[cur].put(off, st.del_dst);
+        const int32_t* is = stage[cur].put(off, st.ins_src);
+        const int32_t* id = stage[cur].put(off, st.ins_dst);
+        const int32_t* ch = stage[cur].put(off, st.changed);
+        const float* cf = stage[cur].put(off, st.changed_feats);
+        g->g->add_delta(ds, dd, static_cast<int64_t>(st.del_src.size()), is, id,
+                        static_cast<int64_t>(st.ins_src.size()), ch,
+                        static_cast<int64_t>(st.changed.size()), cf);
+      } catch (...) {
+        if (next.joinable()) next.join();
+        throw;
+      }
+      if (next.joinable()) next.join();
+    }
+    DGNN_CUDA(cudaStreamSynchronize(g->stream));
+    cuda::release_stream_blocks(g->stream);
+    *out = guard.release();
+  });
+}
+
+// save_dataset (src/dataset_io.cpp:40-95) from the HBM graph store: snapshot 0
+// from its out-CSR (ascending (src,dst)) and features, each delta as
+// DynamicGraph::delta(t) (the expanded G- / G+, changed rows at t).
+int dgnn_dataset_save_graph(const dgnn_graph* g, const char* dir, int32_t format) {
+  return guarded([&] {
+    check(format == 1 || format == 2, "unsupported dataset format version");
+    const DeviceGraph& G = *g->g;
+    check(G.length() > 0, "graph has no snapshots");
+    DatasetManifest m{G.num_nodes(), G.feature_dim(), G.length(), format};
+    write_manifest(dir, m);
+    const int64_t N = m.num_nodes, d = m.feature_dim;
+    {
+      const DevSnapshot& s0 = G.snapshot(0);
+      std::vector<int64_t> ptr(N + 1);
+      std::vector<int32_t> dst(s0.num_edges), src(s0.num_edges);
+      copy_to_host(ptr.data(), s0.out_ptr.get(), sizeof(int64_t) * (N + 1), g->stream);
+      copy_to_host(dst.data(), s0.out_dst.get(), sizeof(int32_t) * s0.num_edges, g->stream);
+      for (int64_t u = 0; u < N; ++u)
+        for (int64_t e = ptr[u]; e < ptr[u + 1]; ++e) src[e] = static_cast<int32_t>(u);
+      std::vector<float> feats(N * d);
+      {
+        FeatRef f0 = G.features(0, g->stream);
+        copy_to_host(feats.data(), f0->get(), sizeof(float) * N * d, g->stream);
+      }
+      write_base(dir, m, src.data(), dst.data(), s0.num_edges, feats.data());
+    }
+    for (int32_t t = 1; t < G.length(); ++t) {
+      const DevDelta& dd = G.delta(t);
+      std::vector<uint64_t> del(dd.n_del), ins(dd.n_ins);
+      copy_to_host(del.data(), dd.del.get(), sizeof(uint64_t) * dd.n_del, g->stream);
+      copy_to_host(ins.data(), dd.ins.get(), sizeof(uint64_t) * dd.n_ins, g->stream);
+      std::vector<int32_t> ds(dd.n_del), dt(dd.n_del), is(dd.n_ins), it(dd.n_ins), ch(dd.n_changed);
+      for (int64_t i = 0; i < dd.n_del; ++i) {
+        ds[i] = static_cast<int32_t>(del[i] >> 32);
+        dt[i] = static_cast<int32_t>(del[i] & 0xffffffffu);
+      }
+      for (int64_t i = 0; i < dd.n_ins; ++i) {
+        is[i] = static_cast<int32_t>(ins[i] >> 32);
+        it[i] = static_cast<int32_t>(ins[i] & 0xffffffffu);
+      }
+      std::vector<float> rows(dd.n_changed * d);
+      if (dd.n_changed) {
+        copy_to_host(ch.data(), dd.changed.get(), sizeof(int32_t) * dd.n_changed, g->stream);
+        // second half of the compact block = F_t[changed]
+        copy_to_host(rows.data(), dd.compact.get() + dd.n_changed * d,
+                     sizeof(float) * dd.n_changed * d, g->stream);
+      }
+      StepView v;
+      v.n_del = dd.n_del;
+      v.n_ins = dd.n_ins;
+      v.n_changed = dd.n_changed;
+      v.del_src = ds.data();
+      v.del_dst = dt.data();
+      v.ins_src = is.data();
+      v.ins_dst = it.data();
+      v.changed = ch.data();
+      v.changed_feats = rows.data();
+      write_step(dir, m, t, v);
+    }
+  });
+}
+
+int dgnn_synth_save(const dgnn_synth* s, const char* dir, int32_t format) {
+  return guarded([&] { save_compact(s->cg, dir, format); });
 }
 
 // ------------------------------------------------------------ aggregation
