@@ -31,6 +31,8 @@ typedef struct dgnn_graph dgnn_graph;
 typedef struct dgnn_synth dgnn_synth;
 typedef struct dgnn_session dgnn_session;
 typedef struct dgnn_dataset dgnn_dataset;
+typedef struct dgnn_cg dgnn_cg;
+typedef struct dgnn_cg_update dgnn_cg_update;
 
 const char* dgnn_last_error(void);
 const char* dgnn_version(void);
@@ -125,6 +127,32 @@ int dgnn_dataset_load(const char* dir, int32_t threads, void* stream, dgnn_graph
 int dgnn_dataset_save_graph(const dgnn_graph* g, const char* dir, int32_t format);
 /* Generator output (structural deltas + redrawn rows; same snapshots on load). */
 int dgnn_synth_save(const dgnn_synth* s, const char* dir, int32_t format);
+
+/* ------------------------------------------------------------------ k-hop
+ * Replaces dgnn::khop / ComputationalGraph / khop_delta / apply_cg_update
+ * (inc/khop.hpp:35-88, src/khop.cpp:12-150), sampled on the device from
+ * snapshot t, bit-exact (mt19937_64 per (destination, hop), derive_seed,
+ * partial Fisher-Yates, libstdc++ uniform_int_distribution). Fanout -1 =
+ * full. Hop k: sorted destinations (the (k)-hop closure) and sorted
+ * (src, dst) edges. */
+int dgnn_khop(const dgnn_graph* g, int32_t t, const int32_t* seeds, int64_t n_seeds,
+              const int32_t* fanouts, int32_t n_hops, uint64_t seed, dgnn_cg** out);
+void dgnn_cg_free(dgnn_cg* c);
+int32_t dgnn_cg_num_hops(const dgnn_cg* c);
+int dgnn_cg_hop_sizes(const dgnn_cg* c, int32_t k, int64_t* n_dest, int64_t* n_edges);
+int dgnn_cg_hop_copy(const dgnn_cg* c, int32_t k, int32_t* dests, int32_t* src, int32_t* dst);
+/* ComputationalGraph::to_view (src/khop.cpp:22-33): device in-CSR (+ out-CSR)
+ * over the node universe of the deepest hop's edges; owned by c. */
+int dgnn_cg_view(dgnn_cg* c, const int64_t** in_ptr, const int32_t** in_src,
+                 const int64_t** out_ptr, const int32_t** out_dst, int64_t* num_edges);
+/* khop_delta against snapshot t of g (t >= 1). */
+int dgnn_khop_delta(const dgnn_cg* prev, const dgnn_graph* g, int32_t t, dgnn_cg_update** out);
+void dgnn_cg_update_free(dgnn_cg_update* u);
+int dgnn_cg_update_sizes(const dgnn_cg_update* u, int32_t k, int64_t* n_added, int64_t* n_removed);
+int dgnn_cg_update_copy(const dgnn_cg_update* u, int32_t k, int32_t* add_src, int32_t* add_dst,
+                        int32_t* rem_src, int32_t* rem_dst);
+int32_t dgnn_cg_update_empty(const dgnn_cg_update* u);
+int dgnn_apply_cg_update(const dgnn_cg* prev, const dgnn_cg_update* up, dgnn_cg** out);
 
 /* ------------------------------------------------------------ aggregation
  * Kernels K1/K2/K3 over device buffers (src/aggregate.cpp:55-246). */

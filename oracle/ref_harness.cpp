@@ -19,6 +19,7 @@
 
 #include "dgnn/dataset_io.hpp"
 #include "dgnn/distsim.hpp"
+#include "dgnn/khop.hpp"
 #include "dgnn/synth.hpp"
 #include "dgnn/train.hpp"
 
@@ -125,6 +126,72 @@ void* ref_graph_from_arrays(int32_t n, int32_t dim, int32_t T, const int64_t* ed
 }
 
 void ref_graph_free(void* g) { delete static_cast<DynamicGraph*>(g); }
+
+// khop / khop_delta / apply_cg_update (src/khop.cpp), unmodified.
+void* ref_khop(void* g, int32_t t, const int32_t* seeds, int64_t n_seeds, const int32_t* fanouts,
+               int32_t n_hops, uint64_t seed) {
+  ComputationalGraph* out = nullptr;
+  int rc = guarded([&] {
+    const DynamicGraph& G = *static_cast<DynamicGraph*>(g);
+    out = new ComputationalGraph(khop(G.snapshot(t), std::vector<NodeId>(seeds, seeds + n_seeds),
+                                      std::vector<Fanout>(fanouts, fanouts + n_hops), seed));
+  });
+  return rc == 0 ? out : nullptr;
+}
+void ref_cg_free(void* c) { delete static_cast<ComputationalGraph*>(c); }
+int32_t ref_cg_num_hops(void* c) { return static_cast<int32_t>(static_cast<ComputationalGraph*>(c)->hops.size()); }
+void ref_cg_hop_sizes(void* c, int32_t k, int64_t* nd, int64_t* ne) {
+  const HopBlock& h = static_cast<ComputationalGraph*>(c)->hops.at(k);
+  *nd = static_cast<int64_t>(h.destinations.size());
+  *ne = static_cast<int64_t>(h.edges.size());
+}
+void ref_cg_hop_copy(void* c, int32_t k, int32_t* dests, int32_t* src, int32_t* dst) {
+  const HopBlock& h = static_cast<ComputationalGraph*>(c)->hops.at(k);
+  for (size_t i = 0; i < h.destinations.size(); ++i) dests[i] = h.destinations[i];
+  for (size_t i = 0; i < h.edges.size(); ++i) {
+    src[i] = h.edges[i].src;
+    dst[i] = h.edges[i].dst;
+  }
+}
+void ref_cg_view(void* c, int32_t n, int64_t* in_ptr, int32_t* in_src) {
+  OwnedView v = static_cast<ComputationalGraph*>(c)->to_view(n);
+  std::memcpy(in_ptr, v.in_ptr.data(), sizeof(int64_t) * v.in_ptr.size());
+  if (!v.in_src.empty()) std::memcpy(in_src, v.in_src.data(), sizeof(int32_t) * v.in_src.size());
+}
+void* ref_khop_delta(void* c, void* g, int32_t t) {
+  CgUpdate* out = nullptr;
+  int rc = guarded([&] {
+    const DynamicGraph& G = *static_cast<DynamicGraph*>(g);
+    out = new CgUpdate(khop_delta(*static_cast<ComputationalGraph*>(c), G.snapshot(t), G.delta(t)));
+  });
+  return rc == 0 ? out : nullptr;
+}
+void ref_cg_update_free(void* u) { delete static_cast<CgUpdate*>(u); }
+void ref_cg_update_sizes(void* u, int32_t k, int64_t* na, int64_t* nr) {
+  const auto& h = static_cast<CgUpdate*>(u)->hops.at(k);
+  *na = static_cast<int64_t>(h.added.size());
+  *nr = static_cast<int64_t>(h.removed.size());
+}
+void ref_cg_update_copy(void* u, int32_t k, int32_t* as, int32_t* ad, int32_t* rs, int32_t* rd) {
+  const auto& h = static_cast<CgUpdate*>(u)->hops.at(k);
+  for (size_t i = 0; i < h.added.size(); ++i) {
+    as[i] = h.added[i].src;
+    ad[i] = h.added[i].dst;
+  }
+  for (size_t i = 0; i < h.removed.size(); ++i) {
+    rs[i] = h.removed[i].src;
+    rd[i] = h.removed[i].dst;
+  }
+}
+int32_t ref_cg_update_empty(void* u) { return static_cast<CgUpdate*>(u)->empty() ? 1 : 0; }
+void* ref_apply_cg_update(void* c, void* u) {
+  ComputationalGraph* out = nullptr;
+  int rc = guarded([&] {
+    out = new ComputationalGraph(
+        apply_cg_update(*static_cast<ComputationalGraph*>(c), *static_cast<CgUpdate*>(u)));
+  });
+  return rc == 0 ? out : nullptr;
+}
 
 // save_dataset / load_dataset (src/dataset_io.cpp:40-165), unmodified.
 int ref_save_dataset(void* g, const char* dir) {

@@ -107,6 +107,18 @@ def lib():
         "ref_graph_from_arrays": (P, [I32, I32, I32, P, P, P, P]),
         "ref_graph_free": (None, [P]),
         "ref_save_dataset": (C.c_int, [P, C.c_char_p]),
+        "ref_khop": (P, [P, I32, P, I64, P, I32, U64]),
+        "ref_cg_free": (None, [P]),
+        "ref_cg_num_hops": (I32, [P]),
+        "ref_cg_hop_sizes": (None, [P, I32, P, P]),
+        "ref_cg_hop_copy": (None, [P, I32, P, P, P]),
+        "ref_cg_view": (None, [P, I32, P, P]),
+        "ref_khop_delta": (P, [P, P, I32]),
+        "ref_cg_update_free": (None, [P]),
+        "ref_cg_update_sizes": (None, [P, I32, P, P]),
+        "ref_cg_update_copy": (None, [P, I32, P, P, P, P]),
+        "ref_cg_update_empty": (I32, [P]),
+        "ref_apply_cg_update": (P, [P, P]),
         "ref_load_dataset": (P, [C.c_char_p]),
         "ref_graph_length": (I32, [P]),
         "ref_graph_num_nodes": (I32, [P]),
@@ -296,6 +308,62 @@ class RefGraph:
         pin = None if params is None else np.ascontiguousarray(params, np.float64)
         _check(lib().ref_sample_grads(self.h, C.byref(c), window_index, _p(pin), C.byref(loss), _p(pred0), _p(grads)))
         return loss.value, pred0, grads
+
+
+class RefCompGraph:
+    """Owns a reference dgnn::ComputationalGraph (inc/khop.hpp:42-51)."""
+
+    def __init__(self, handle, n):
+        if not handle:
+            raise ValueError(lib().ref_last_error().decode())
+        self.h, self.n = handle, n
+
+    @classmethod
+    def khop(cls, g: "RefGraph", t, seeds, fanouts, seed):
+        s = np.ascontiguousarray(seeds, np.int32)
+        f = np.ascontiguousarray(fanouts, np.int32)
+        return cls(lib().ref_khop(g.h, t, _p(s), len(s), _p(f), len(f), seed), g.n)
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.ref_cg_free(self.h)
+            self.h = None
+
+    def hops(self):
+        out = []
+        for k in range(lib().ref_cg_num_hops(self.h)):
+            nd, ne = C.c_int64(), C.c_int64()
+            lib().ref_cg_hop_sizes(self.h, k, C.byref(nd), C.byref(ne))
+            d = np.empty(nd.value, np.int32)
+            s, t = np.empty(ne.value, np.int32), np.empty(ne.value, np.int32)
+            lib().ref_cg_hop_copy(self.h, k, _p(d), _p(s), _p(t))
+            out.append({"dests": d, "src": s, "dst": t})
+        return out
+
+    def view(self):
+        ne = len(self.hops()[-1]["src"])
+        ptr, src = np.empty(self.n + 1, np.int64), np.empty(ne, np.int32)
+        lib().ref_cg_view(self.h, self.n, _p(ptr), _p(src))
+        return ptr, src
+
+    def delta(self, g: "RefGraph", t):
+        u = lib().ref_khop_delta(self.h, g.h, t)
+        if not u:
+            raise ValueError(lib().ref_last_error().decode())
+        try:
+            hops = []
+            for k in range(lib().ref_cg_num_hops(self.h)):
+                na, nr = C.c_int64(), C.c_int64()
+                lib().ref_cg_update_sizes(u, k, C.byref(na), C.byref(nr))
+                a = [np.empty(na.value, np.int32) for _ in range(2)]
+                r = [np.empty(nr.value, np.int32) for _ in range(2)]
+                lib().ref_cg_update_copy(u, k, _p(a[0]), _p(a[1]), _p(r[0]), _p(r[1]))
+                hops.append({"add_src": a[0], "add_dst": a[1], "rem_src": r[0], "rem_dst": r[1]})
+            empty = bool(lib().ref_cg_update_empty(u))
+            applied = RefCompGraph(lib().ref_apply_cg_update(self.h, u), self.n)
+        finally:
+            lib().ref_cg_update_free(u)
+        return hops, empty, applied
 
 
 @dataclass

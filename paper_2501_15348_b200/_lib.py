@@ -69,6 +69,18 @@ SIGNATURES = {
     "dgnn_dataset_load": (C.c_int, [C.c_char_p, I32, P, PP]),
     "dgnn_dataset_save_graph": (C.c_int, [P, C.c_char_p, I32]),
     "dgnn_synth_save": (C.c_int, [P, C.c_char_p, I32]),
+    "dgnn_khop": (C.c_int, [P, I32, P, I64, P, I32, U64, PP]),
+    "dgnn_cg_free": (None, [P]),
+    "dgnn_cg_num_hops": (I32, [P]),
+    "dgnn_cg_hop_sizes": (C.c_int, [P, I32, C.POINTER(I64), C.POINTER(I64)]),
+    "dgnn_cg_hop_copy": (C.c_int, [P, I32, P, P, P]),
+    "dgnn_cg_view": (C.c_int, [P, PP, PP, PP, PP, C.POINTER(I64)]),
+    "dgnn_khop_delta": (C.c_int, [P, P, I32, PP]),
+    "dgnn_cg_update_free": (None, [P]),
+    "dgnn_cg_update_sizes": (C.c_int, [P, I32, C.POINTER(I64), C.POINTER(I64)]),
+    "dgnn_cg_update_copy": (C.c_int, [P, I32, P, P, P, P]),
+    "dgnn_cg_update_empty": (I32, [P]),
+    "dgnn_apply_cg_update": (C.c_int, [P, P, PP]),
     "dgnn_agg_scratch": (C.c_int, [I32, I32, I32, P, P, P, P, P, P, P, P]),
     "dgnn_agg_delta": (C.c_int, [I32, I32, I32, P, P, P, P, P, P, P, P, P, P]),
     "dgnn_graph_apply_delta": (C.c_int, [P, I32, I32, P, P, P, P, P]),

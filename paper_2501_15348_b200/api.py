@@ -217,6 +217,71 @@ def save_dataset(graph: "DynamicGraph", path, binary=False):
     check(lib().dgnn_dataset_save_graph(graph.h, os.fsencode(path), 2 if binary else 1))
 
 
+# ------------------------------------------------------------------ k-hop
+class ComputationalGraph:
+    """Sampled k-hop computational graph on the device (ref
+    ComputationalGraph, inc/khop.hpp:42-51; khop, src/khop.cpp:66-96)."""
+
+    def __init__(self, h, n):
+        self.h, self.n = h, n
+
+    @classmethod
+    def khop(cls, graph: "DynamicGraph", t, seeds, fanouts, seed):
+        s = np.ascontiguousarray(seeds, np.int32)
+        f = np.ascontiguousarray(fanouts, np.int32)
+        h = C.c_void_p()
+        check(lib().dgnn_khop(graph.h, t, _np_ptr(s), len(s), _np_ptr(f), len(f), seed, C.byref(h)))
+        return cls(h, graph.n)
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None and _lib._lib is not None:
+            lib().dgnn_cg_free(self.h)
+            self.h = None
+
+    def hops(self):
+        out = []
+        for k in range(lib().dgnn_cg_num_hops(self.h)):
+            nd, ne = C.c_int64(), C.c_int64()
+            check(lib().dgnn_cg_hop_sizes(self.h, k, C.byref(nd), C.byref(ne)))
+            d = np.empty(nd.value, np.int32)
+            s, t = np.empty(ne.value, np.int32), np.empty(ne.value, np.int32)
+            check(lib().dgnn_cg_hop_copy(self.h, k, _np_ptr(d), _np_ptr(s), _np_ptr(t)))
+            out.append({"dests": d, "src": s, "dst": t})
+        return out
+
+    def view(self):
+        """to_view (src/khop.cpp:22-33): host copies of the device in-CSR."""
+        ip, is_, op, od = (C.c_void_p() for _ in range(4))
+        ne = C.c_int64()
+        check(lib().dgnn_cg_view(self.h, C.byref(ip), C.byref(is_), C.byref(op), C.byref(od), C.byref(ne)))
+        lib().dgnn_synchronize(None)
+        ptr = device_view(ip.value, (self.n + 1,), np.int64).cpu().numpy()
+        src = (device_view(is_.value, (ne.value,), np.int32).cpu().numpy() if ne.value
+               else np.zeros(0, np.int32))
+        return ptr, src
+
+    def delta(self, graph: "DynamicGraph", t):
+        """khop_delta (src/khop.cpp:105-121) -> (per-hop diffs, empty, apply_cg_update result)."""
+        u = C.c_void_p()
+        check(lib().dgnn_khop_delta(self.h, graph.h, t, C.byref(u)))
+        try:
+            hops = []
+            for k in range(lib().dgnn_cg_num_hops(self.h)):
+                na, nr = C.c_int64(), C.c_int64()
+                check(lib().dgnn_cg_update_sizes(u, k, C.byref(na), C.byref(nr)))
+                a = [np.empty(na.value, np.int32) for _ in range(2)]
+                r = [np.empty(nr.value, np.int32) for _ in range(2)]
+                check(lib().dgnn_cg_update_copy(u, k, *[_np_ptr(x) for x in a + r]))
+                hops.append({"add_src": a[0], "add_dst": a[1], "rem_src": r[0], "rem_dst": r[1]})
+            empty = bool(lib().dgnn_cg_update_empty(u))
+            h = C.c_void_p()
+            check(lib().dgnn_apply_cg_update(self.h, u, C.byref(h)))
+            applied = ComputationalGraph(h, self.n)
+        finally:
+            lib().dgnn_cg_update_free(u)
+        return hops, empty, applied
+
+
 def synthesize(num_nodes, avg_degree, feature_dim, num_snapshots, edge_change, feature_change,
                seed=1, stream=None) -> "DynamicGraph":
     return Synth(num_nodes, avg_degree, feature_dim, num_snapshots, edge_change,

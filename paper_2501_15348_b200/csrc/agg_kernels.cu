@@ -283,6 +283,11 @@ __device__ __forceinline__ float4 ld_nc_hint(const float* p, uint64_t pol) {
                : "l"(p), "l"(pol));
   return r;
 }
+__device__ __forceinline__ void st_hint(float* p, float4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ float4 ld_hint(const float* p, uint64_t pol) {
   float4 r;
   asm volatile("ld.global.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
@@ -307,7 +312,8 @@ k_agg_delta_v4(int n_rows, int w, int32_t num_nodes, const int32_t* __restrict__
                const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ ent,
                const float* __restrict__ Fp, const float* __restrict__ Fc,
                const float* __restrict__ Cp, const float* __restrict__ Cc,
-               float* __restrict__ values, float* __restrict__ degree, float* __restrict__ msum) {
+               float* __restrict__ values, float* __restrict__ degree, float* __restrict__ msum,
+               int st_evict_first) {
   constexpr int R = 32 / G;
   const int lane = threadIdx.x & 31, gl = lane & (G - 1), sub = lane / G;
   const int64_t wg = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
@@ -403,8 +409,11 @@ k_agg_delta_v4(int n_rows, int w, int32_t num_nodes, const int32_t* __restrict__
         if (gl == 0) degree[m0.v] = live ? dg : 0.f;
       } else {
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (col_ok(u)) *reinterpret_cast<float4*>(accp + 4 * G * u) = acc[u];
+        for (int u = 0; u < U; ++u) {
+          if (!col_ok(u)) continue;
+          if (st_evict_first) st_hint(accp + 4 * G * u, acc[u], once);
+          else *reinterpret_cast<float4*>(accp + 4 * G * u) = acc[u];
+        }
       }
     }
     m0 = m1;
@@ -751,7 +760,13 @@ void agg_delta(int kind, int n_rows, int w, const int32_t* rows, const int32_t* 
 #define DGNN_DELTA_LAUNCH(UU, MM)                                                                    \
   DGNN_DISPATCH_G(g, DGNN_LAUNCH((k_agg_delta_v4<G, UU, MM>), grid, kThreads, 0, stream, n_rows, w, \
                                  num_nodes, rows, row_ptr, ent_c, f_prev, f_curr, cp, cc, values,   \
-                                 degree, mean_sums))
+                                 degree, mean_sums, st_ef))
+    // destination rows are written once per delta: evict_first keeps them
+    // from displacing the compact block (DGNN_DELTA_ST_HINT=0 disables)
+    static const int st_ef = [] {
+      const char* e = std::getenv("DGNN_DELTA_ST_HINT");
+      return e ? std::atoi(e) : 1;
+    }();
     static const int minb = [] {
       const char* e = std::getenv("DGNN_DELTA_MINB");
       return e ? std::atoi(e) : 0;
@@ -761,11 +776,11 @@ void agg_delta(int kind, int n_rows, int w, const int32_t* rows, const int32_t* 
     } else if (U == 4 && minb == 3) {
       DGNN_DISPATCH_G(g, DGNN_LAUNCH((k_agg_delta_v4<G, 4, false, 3>), grid, kThreads, 0, stream, n_rows,
                                      w, num_nodes, rows, row_ptr, ent_c, f_prev, f_curr, cp, cc,
-                                     values, degree, mean_sums))
+                                     values, degree, mean_sums, st_ef))
     } else if (U == 4 && minb == 4) {
       DGNN_DISPATCH_G(g, DGNN_LAUNCH((k_agg_delta_v4<G, 4, false, 4>), grid, kThreads, 0, stream, n_rows,
                                      w, num_nodes, rows, row_ptr, ent_c, f_prev, f_curr, cp, cc,
-                                     values, degree, mean_sums))
+                                     values, degree, mean_sums, st_ef))
     } else if (U == 4) {
       DGNN_DELTA_LAUNCH(4, false);
     } else if (U == 2 && kind == kAggMean) {

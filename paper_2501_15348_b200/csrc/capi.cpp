@@ -570,6 +570,120 @@ int dgnn_synth_save(const dgnn_synth* s, const char* dir, int32_t format) {
   return guarded([&] { save_compact(s->cg, dir, format); });
 }
 
+// ------------------------------------------------------------------ k-hop
+struct dgnn_cg {
+  DevCompGraph cg;
+  int32_t num_nodes = 0;
+  cudaStream_t stream = nullptr;
+  std::unique_ptr<DevSnapshot> view;  // to_view(), built on first request
+};
+
+struct dgnn_cg_update {
+  DevCgUpdate up;
+};
+
+int dgnn_khop(const dgnn_graph* g, int32_t t, const int32_t* seeds, int64_t n_seeds,
+              const int32_t* fanouts, int32_t n_hops, uint64_t seed, dgnn_cg** out) {
+  return guarded([&] {
+    auto c = std::make_unique<dgnn_cg>();
+    c->num_nodes = g->g->num_nodes();
+    c->stream = g->stream;
+    std::vector<int32_t> s(seeds, seeds + (n_seeds > 0 ? n_seeds : 0));
+    std::vector<int32_t> f(fanouts, fanouts + (n_hops > 0 ? n_hops : 0));
+    c->cg = khop(g->g->snapshot(t), c->num_nodes, std::move(s), std::move(f), seed, g->stream);
+    *out = c.release();
+  });
+}
+
+void dgnn_cg_free(dgnn_cg* c) { delete c; }
+
+int32_t dgnn_cg_num_hops(const dgnn_cg* c) { return static_cast<int32_t>(c->cg.hops.size()); }
+
+int dgnn_cg_hop_sizes(const dgnn_cg* c, int32_t k, int64_t* n_dest, int64_t* n_edges) {
+  return guarded([&] {
+    const DevHop& h = c->cg.hops.at(k);
+    *n_dest = h.n_dest;
+    *n_edges = h.n_edges;
+  });
+}
+
+int dgnn_cg_hop_copy(const dgnn_cg* c, int32_t k, int32_t* dests, int32_t* src, int32_t* dst) {
+  return guarded([&] {
+    const DevHop& h = c->cg.hops.at(k);
+    if (dests) copy_to_host(dests, h.dests.get(), sizeof(int32_t) * h.n_dest, c->stream);
+    std::vector<uint64_t> e(h.n_edges);
+    copy_to_host(e.data(), h.edges.get(), sizeof(uint64_t) * h.n_edges, c->stream);
+    for (int64_t i = 0; i < h.n_edges; ++i) {
+      if (src) src[i] = static_cast<int32_t>(e[i] >> 32);
+      if (dst) dst[i] = static_cast<int32_t>(e[i] & 0xffffffffu);
+    }
+  });
+}
+
+int dgnn_cg_view(dgnn_cg* c, const int64_t** in_ptr, const int32_t** in_src,
+                 const int64_t** out_ptr, const int32_t** out_dst, int64_t* num_edges) {
+  return guarded([&] {
+    if (!c->view) {
+      const DevHop& h = c->cg.hops.back();
+      c->view = std::make_unique<DevSnapshot>(csr_from_keys(h.edges.get(), h.n_edges, c->num_nodes, c->stream));
+    }
+    if (in_ptr) *in_ptr = c->view->in_ptr.get();
+    if (in_src) *in_src = c->view->in_src.get();
+    if (out_ptr) *out_ptr = c->view->out_ptr.get();
+    if (out_dst) *out_dst = c->view->out_dst.get();
+    if (num_edges) *num_edges = c->view->num_edges;
+  });
+}
+
+int dgnn_khop_delta(const dgnn_cg* prev, const dgnn_graph* g, int32_t t, dgnn_cg_update** out) {
+  return guarded([&] {
+    check(t >= 1 && t < g->g->length(), "delta index out of range");
+    auto u = std::make_unique<dgnn_cg_update>();
+    u->up = khop_delta(prev->cg, g->g->snapshot(t), g->g->num_nodes(), g->stream);
+    *out = u.release();
+  });
+}
+
+void dgnn_cg_update_free(dgnn_cg_update* u) { delete u; }
+
+int dgnn_cg_update_sizes(const dgnn_cg_update* u, int32_t k, int64_t* n_added, int64_t* n_removed) {
+  return guarded([&] {
+    const auto& h = u->up.hops.at(k);
+    *n_added = h.n_added;
+    *n_removed = h.n_removed;
+  });
+}
+
+int dgnn_cg_update_copy(const dgnn_cg_update* u, int32_t k, int32_t* add_src, int32_t* add_dst,
+                        int32_t* rem_src, int32_t* rem_dst) {
+  return guarded([&] {
+    const auto& h = u->up.hops.at(k);
+    auto split = [](const cuda::DevArray<uint64_t>& keys, int64_t n, int32_t* s, int32_t* d) {
+      std::vector<uint64_t> e(n);
+      copy_to_host(e.data(), keys.get(), sizeof(uint64_t) * n, nullptr);
+      for (int64_t i = 0; i < n; ++i) {
+        if (s) s[i] = static_cast<int32_t>(e[i] >> 32);
+        if (d) d[i] = static_cast<int32_t>(e[i] & 0xffffffffu);
+      }
+    };
+    DGNN_CUDA(cudaDeviceSynchronize());
+    split(h.added, h.n_added, add_src, add_dst);
+    split(h.removed, h.n_removed, rem_src, rem_dst);
+  });
+}
+
+int32_t dgnn_cg_update_empty(const dgnn_cg_update* u) { return u->up.empty() ? 1 : 0; }
+
+int dgnn_apply_cg_update(const dgnn_cg* prev, const dgnn_cg_update* up, dgnn_cg** out) {
+  return guarded([&] {
+    auto c = std::make_unique<dgnn_cg>();
+    c->num_nodes = prev->num_nodes;
+    c->stream = prev->stream;
+    c->cg = apply_cg_update(prev->cg, up->up, prev->stream);
+    *out = c.release();
+  });
+}
+
 // ------------------------------------------------------------ aggregation
 int dgnn_agg_scratch(int32_t kind, int32_t n, int32_t w, const int64_t* in_ptr,
                      const int32_t* in_src, const float* feats, float* values, float* degree,

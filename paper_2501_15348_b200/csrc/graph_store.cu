@@ -4,6 +4,7 @@
 // library primitives); the graph-specific passes are the kernels below.
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <cstdlib>
 #include <stdexcept>
 
@@ -480,36 +481,39 @@ void DeviceGraph::add_delta(const int32_t* del_src, const int32_t* del_dst, int6
   DGNN_CUDA(cudaEventRecord(cur->ready, st));
 }
 
-void DeviceGraph::finish_snapshot(DevArray<uint64_t> keys, const float* prev_feats,
-                                  const float* feats) {
-  cudaStream_t st = stream_;
+DevSnapshot csr_from_keys(const uint64_t* keys, int64_t E, int32_t n, cudaStream_t st) {
   Cub cub(st);
-  const int64_t E = static_cast<int64_t>(keys.size());
   DevSnapshot s;
   s.num_edges = E;
   // out-CSR: keys already sorted by (src, dst)
-  DevArray<unsigned long long> cnt(n_ + 1, st);
+  DevArray<unsigned long long> cnt(n + 1, st);
   cnt.zero(st);
-  s.out_ptr = DevArray<int64_t>(n_ + 1, st);
+  s.out_ptr = DevArray<int64_t>(n + 1, st);
   s.out_dst = DevArray<int32_t>(E, st);
   if (E > 0) {
-    DGNN_LAUNCH(k_hist_hi, grid_for(E), kT, 0, st, E, keys.get(), cnt.get());
-    DGNN_LAUNCH(k_low32, grid_for(E), kT, 0, st, E, keys.get(), s.out_dst.get());
+    DGNN_LAUNCH(k_hist_hi, grid_for(E), kT, 0, st, E, keys, cnt.get());
+    DGNN_LAUNCH(k_low32, grid_for(E), kT, 0, st, E, keys, s.out_dst.get());
   }
-  cub.exclusive_sum(reinterpret_cast<const int64_t*>(cnt.get()), s.out_ptr.get(), n_ + 1);
+  cub.exclusive_sum(reinterpret_cast<const int64_t*>(cnt.get()), s.out_ptr.get(), n + 1);
   // in-CSR: sort by (dst, src)
-  s.in_ptr = DevArray<int64_t>(n_ + 1, st);
+  s.in_ptr = DevArray<int64_t>(n + 1, st);
   s.in_src = DevArray<int32_t>(E, st);
   cnt.zero(st);
   if (E > 0) {
     DevArray<uint64_t> sw(E, st), sw_sorted(E, st);
-    DGNN_LAUNCH(k_swap_halves, grid_for(E), kT, 0, st, E, keys.get(), sw.get());
+    DGNN_LAUNCH(k_swap_halves, grid_for(E), kT, 0, st, E, keys, sw.get());
     cub.sort(sw.get(), sw_sorted.get(), E);
     DGNN_LAUNCH(k_hist_hi, grid_for(E), kT, 0, st, E, sw_sorted.get(), cnt.get());
     DGNN_LAUNCH(k_low32, grid_for(E), kT, 0, st, E, sw_sorted.get(), s.in_src.get());
   }
-  cub.exclusive_sum(reinterpret_cast<const int64_t*>(cnt.get()), s.in_ptr.get(), n_ + 1);
-  snaps_.push_back(std::move(s));
+  cub.exclusive_sum(reinterpret_cast<const int64_t*>(cnt.get()), s.in_ptr.get(), n + 1);
+  return s;
+}
+
+void DeviceGraph::finish_snapshot(DevArray<uint64_t> keys, const float* prev_feats,
+                                  const float* feats) {
+  const int64_t E = static_cast<int64_t>(keys.size());
+  snaps_.push_back(csr_from_keys(keys.get(), E, n_, stream_));
   deltas_.emplace_back();
   prev_keys_ = std::move(curr_keys_);
   curr_keys_ = std::move(keys);
@@ -618,6 +622,259 @@ void DeviceGraph::build_delta(int32_t t, const float* prev_feats, const float* f
                 dd.changed.get(), n_, dd.ent_c.get());
   DGNN_CUDA(cudaStreamSynchronize(st));
   deltas_[t] = std::move(dd);
+}
+
+// ---------------------------------------------------------------- k-hop
+namespace {
+
+// std::mt19937_64 (libstdc++), full state in local memory.
+struct Mt64 {
+  static constexpr int kN = 312, kM = 156;
+  uint64_t mt[kN];
+  int idx;
+  __device__ explicit Mt64(uint64_t s) {
+    mt[0] = s;
+    for (int i = 1; i < kN; ++i) mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + i;
+    idx = kN;
+  }
+  __device__ void twist() {
+    for (int i = 0; i < kN; ++i) {
+      const uint64_t y = (mt[i] & 0xFFFFFFFF80000000ULL) | (mt[i + 1 < kN ? i + 1 : 0] & 0x7FFFFFFFULL);
+      mt[i] = mt[i + kM < kN ? i + kM : i + kM - kN] ^ (y >> 1) ^ ((y & 1ULL) ? 0xB5026F5AA96619E9ULL : 0ULL);
+    }
+    idx = 0;
+  }
+  __device__ uint64_t operator()() {
+    if (idx >= kN) twist();
+    uint64_t z = mt[idx++];
+    z ^= (z >> 29) & 0x5555555555555555ULL;
+    z ^= (z << 17) & 0x71D67FFFEDA60000ULL;
+    z ^= (z << 37) & 0xFFF7EEE000000000ULL;
+    z ^= z >> 43;
+    return z;
+  }
+};
+
+__device__ __forceinline__ uint64_t d_mix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+// derive_seed (ref inc/common.hpp:50-52)
+__device__ __forceinline__ uint64_t d_derive_seed(uint64_t seed, uint64_t a, uint64_t b, uint64_t c) {
+  return d_mix64(d_mix64(d_mix64(seed ^ d_mix64(a)) ^ d_mix64(b)) ^ d_mix64(c));
+}
+
+// uniform_int_distribution<size_t>(a, b) on a 64-bit engine: Lemire's
+// nearly-divisionless reduction (libstdc++ bits/uniform_int_dist.h, _S_nd).
+__device__ __forceinline__ uint64_t d_uniform(Mt64& g, uint64_t a, uint64_t b) {
+  const uint64_t range = b - a + 1;
+  uint64_t x = g();
+  uint64_t hi = __umul64hi(x, range), lo = x * range;
+  if (lo < range) {
+    const uint64_t threshold = (0ULL - range) % range;
+    while (lo < threshold) {
+      x = g();
+      hi = __umul64hi(x, range);
+      lo = x * range;
+    }
+  }
+  return a + hi;
+}
+
+__global__ void k_hop_counts(int64_t nd, const int32_t* __restrict__ dests,
+                             const int64_t* __restrict__ in_ptr, int32_t fanout,
+                             int64_t* __restrict__ cnt, int64_t* __restrict__ pool_cnt) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nd;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t v = dests[i];
+    const int64_t deg = in_ptr[v + 1] - in_ptr[v];
+    const bool all = fanout < 0 || deg <= fanout;
+    cnt[i] = all ? deg : fanout;
+    pool_cnt[i] = all ? 0 : deg;
+  }
+}
+
+// sample_in_edges (ref src/khop.cpp:38-55), one destination per thread.
+__global__ void __launch_bounds__(128)
+k_hop_sample(int64_t nd, const int32_t* __restrict__ dests, const int64_t* __restrict__ in_ptr,
+             const int32_t* __restrict__ in_src, int32_t fanout, uint64_t seed, int hop,
+             const int64_t* __restrict__ off, const int64_t* __restrict__ pool_off,
+             int32_t* __restrict__ pool, uint64_t* __restrict__ keys) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nd;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t v = dests[i];
+    const int64_t b = in_ptr[v], deg = in_ptr[v + 1] - b;
+    uint64_t* out = keys + off[i];
+    if (fanout < 0 || deg <= fanout) {
+      for (int64_t j = 0; j < deg; ++j)
+        out[j] = (static_cast<uint64_t>(static_cast<uint32_t>(in_src[b + j])) << 32) | static_cast<uint32_t>(v);
+      continue;
+    }
+    int32_t* p = pool + pool_off[i];
+    for (int64_t j = 0; j < deg; ++j) p[j] = in_src[b + j];
+    Mt64 g(d_derive_seed(seed, static_cast<uint64_t>(v), static_cast<uint64_t>(hop), 0));
+    for (int32_t j = 0; j < fanout; ++j) {  // partial Fisher-Yates
+      const uint64_t k = d_uniform(g, static_cast<uint64_t>(j), static_cast<uint64_t>(deg - 1));
+      const int32_t t = p[j];
+      p[j] = p[k];
+      p[k] = t;
+      out[j] = (static_cast<uint64_t>(static_cast<uint32_t>(p[j])) << 32) | static_cast<uint32_t>(v);
+    }
+  }
+}
+
+__global__ void k_nodes_to_keys(int64_t n, const int32_t* __restrict__ nodes, uint64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<uint32_t>(nodes[i]);
+}
+
+__global__ void k_src_to_keys(int64_t n, const uint64_t* __restrict__ edges, uint64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = edges[i] >> 32;
+}
+
+DevArray<uint64_t> copy_keys(const uint64_t* src, int64_t n, cudaStream_t st) {
+  DevArray<uint64_t> out(n, st);
+  if (n) DGNN_CUDA(cudaMemcpyAsync(out.get(), src, sizeof(uint64_t) * n, cudaMemcpyDeviceToDevice, st));
+  return out;
+}
+
+// closure: sorted unique (dests U sources of edges) (ref src/khop.cpp:88-93)
+DevArray<int32_t> closure(const DevArray<int32_t>& dests, int64_t nd, const DevArray<uint64_t>& edges,
+                          int64_t ne, int64_t* n_out, Cub& cub) {
+  cudaStream_t st = cub.st;
+  const int64_t m = nd + ne;
+  DevArray<uint64_t> cat(m, st), sorted(m, st), uniq(m, st);
+  if (nd) DGNN_LAUNCH(k_nodes_to_keys, grid_for(nd), kT, 0, st, nd, dests.get(), cat.get());
+  if (ne) DGNN_LAUNCH(k_src_to_keys, grid_for(ne), kT, 0, st, ne, edges.get(), cat.get() + nd);
+  cub.sort(cat.get(), sorted.get(), m, 32);
+  *n_out = cub.unique(sorted.get(), uniq.get(), m);
+  DevArray<int32_t> out(*n_out, st);
+  if (*n_out) DGNN_LAUNCH(k_low32, grid_for(*n_out), kT, 0, st, *n_out, uniq.get(), out.get());
+  return out;
+}
+
+// a \ b over sorted unique keys
+DevArray<uint64_t> set_minus(const DevArray<uint64_t>& a, int64_t na, const DevArray<uint64_t>& b,
+                             int64_t nb, int64_t* n_out, Cub& cub) {
+  cudaStream_t st = cub.st;
+  if (na == 0) {
+    *n_out = 0;
+    return DevArray<uint64_t>(0, st);
+  }
+  DevArray<uint8_t> keep(na, st);
+  DevArray<uint64_t> tmp(na, st);
+  DGNN_LAUNCH(k_mark, grid_for(na), kT, 0, st, na, a.get(), nb, b.get(), 0, keep.get());
+  *n_out = cub.select_flagged(a.get(), keep.get(), tmp.get(), na);
+  return copy_keys(tmp.get(), *n_out, st);
+}
+
+}  // namespace
+
+DevCompGraph khop(const DevSnapshot& snap, int32_t num_nodes, std::vector<int32_t> seeds,
+                  std::vector<int32_t> fanouts, uint64_t seed, cudaStream_t st) {
+  // ref src/khop.cpp:66-80 (checks and messages)
+  if (seeds.empty()) throw std::invalid_argument("khop: seeds must be non-empty");
+  if (fanouts.empty()) throw std::invalid_argument("khop: fanouts must name at least one hop");
+  std::sort(seeds.begin(), seeds.end());
+  seeds.erase(std::unique(seeds.begin(), seeds.end()), seeds.end());
+  for (int32_t s : seeds)
+    if (s < 0 || s >= num_nodes) throw std::invalid_argument("khop: seed node out of range");
+  for (int32_t f : fanouts)
+    if (!(f == -1 || f >= 1)) throw std::invalid_argument("khop: fanout must be positive or full");
+  Cub cub(st);
+  DevCompGraph cg;
+  cg.seeds = seeds;
+  cg.fanouts = fanouts;
+  cg.sample_seed = seed;
+  int64_t nd = static_cast<int64_t>(seeds.size());
+  DevArray<int32_t> dests = upload(seeds.data(), nd, st);
+  for (size_t k = 0; k < fanouts.size(); ++k) {
+    DevHop h;
+    h.n_dest = nd;
+    DevArray<int64_t> cnt(nd + 1, st), off(nd + 1, st), pcnt(nd + 1, st), poff(nd + 1, st);
+    cnt.zero(st);
+    pcnt.zero(st);
+    DGNN_LAUNCH(k_hop_counts, grid_for(nd), kT, 0, st, nd, dests.get(), snap.in_ptr.get(),
+                fanouts[k], cnt.get(), pcnt.get());
+    cub.exclusive_sum(cnt.get(), off.get(), nd + 1);
+    cub.exclusive_sum(pcnt.get(), poff.get(), nd + 1);
+    const int64_t ne = cub.read(off.get() + nd), np = cub.read(poff.get() + nd);
+    DevArray<uint64_t> raw(ne, st);
+    DevArray<int32_t> pool(np, st);
+    DGNN_LAUNCH(k_hop_sample, cuda::wave_grid(nd, 128, 4), 128, 0, st, nd, dests.get(),
+                snap.in_ptr.get(), snap.in_src.get(), fanouts[k], seed, static_cast<int>(k),
+                off.get(), poff.get(), pool.get(), raw.get());
+    h.edges = DevArray<uint64_t>(ne, st);
+    cub.sort(raw.get(), h.edges.get(), ne);
+    h.n_edges = ne;
+    int64_t nn = 0;
+    DevArray<int32_t> next = closure(dests, nd, h.edges, ne, &nn, cub);
+    h.dests = std::move(dests);
+    cg.hops.push_back(std::move(h));
+    dests = std::move(next);
+    nd = nn;
+  }
+  DGNN_CUDA(cudaStreamSynchronize(st));
+  return cg;
+}
+
+DevCgUpdate khop_delta(const DevCompGraph& prev, const DevSnapshot& curr, int32_t num_nodes,
+                       cudaStream_t st) {
+  DevCompGraph fresh = khop(curr, num_nodes, prev.seeds, prev.fanouts, prev.sample_seed, st);
+  if (prev.hops.size() != fresh.hops.size())
+    throw std::invalid_argument("khop_delta: hop count mismatch");
+  Cub cub(st);
+  DevCgUpdate up;
+  up.hops.resize(fresh.hops.size());
+  for (size_t k = 0; k < fresh.hops.size(); ++k) {
+    const DevHop &a = prev.hops[k], &b = fresh.hops[k];
+    up.hops[k].added = set_minus(b.edges, b.n_edges, a.edges, a.n_edges, &up.hops[k].n_added, cub);
+    up.hops[k].removed = set_minus(a.edges, a.n_edges, b.edges, b.n_edges, &up.hops[k].n_removed, cub);
+  }
+  DGNN_CUDA(cudaStreamSynchronize(st));
+  return up;
+}
+
+DevCompGraph apply_cg_update(const DevCompGraph& prev, const DevCgUpdate& update, cudaStream_t st) {
+  if (update.hops.size() != prev.hops.size())
+    throw std::invalid_argument("apply_cg_update: hop count mismatch");
+  Cub cub(st);
+  DevCompGraph out;
+  out.seeds = prev.seeds;
+  out.fanouts = prev.fanouts;
+  out.sample_seed = prev.sample_seed;
+  int64_t nd = static_cast<int64_t>(prev.seeds.size());
+  DevArray<int32_t> dests = upload(prev.seeds.data(), nd, st);
+  for (size_t k = 0; k < prev.hops.size(); ++k) {
+    const DevHop& p = prev.hops[k];
+    const auto& diff = update.hops[k];
+    int64_t nk = 0;
+    DevArray<uint64_t> kept = set_minus(p.edges, p.n_edges, diff.removed, diff.n_removed, &nk, cub);
+    // set_union of two sorted unique ranges = sort + unique of the concatenation
+    const int64_t m = nk + diff.n_added;
+    DevArray<uint64_t> cat(m, st), sorted(m, st), uniq(m, st);
+    if (nk) DGNN_CUDA(cudaMemcpyAsync(cat.get(), kept.get(), 8 * nk, cudaMemcpyDeviceToDevice, st));
+    if (diff.n_added)
+      DGNN_CUDA(cudaMemcpyAsync(cat.get() + nk, diff.added.get(), 8 * diff.n_added, cudaMemcpyDeviceToDevice, st));
+    cub.sort(cat.get(), sorted.get(), m);
+    DevHop h;
+    h.n_edges = cub.unique(sorted.get(), uniq.get(), m);
+    h.edges = copy_keys(uniq.get(), h.n_edges, st);
+    h.n_dest = nd;
+    int64_t nn = 0;
+    DevArray<int32_t> next = closure(dests, nd, h.edges, h.n_edges, &nn, cub);
+    h.dests = std::move(dests);
+    out.hops.push_back(std::move(h));
+    dests = std::move(next);
+    nd = nn;
+  }
+  DGNN_CUDA(cudaStreamSynchronize(st));
+  return out;
 }
 
 }  // namespace dgnn

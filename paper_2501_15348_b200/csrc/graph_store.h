@@ -143,4 +143,54 @@ class DeviceGraph {
 // Host copies (tests / C-ABI getters).
 void copy_to_host(void* dst, const void* src, size_t bytes, cudaStream_t stream);
 
+// In-CSR (sources ascending per destination) + out-CSR over num_nodes from
+// sorted unique (src << 32 | dst) keys (ref Snapshot ctor CSR build,
+// src/snapshot.cpp:46-69, and ComputationalGraph::to_view, src/khop.cpp:22-33).
+DevSnapshot csr_from_keys(const uint64_t* keys, int64_t num_edges, int32_t num_nodes,
+                          cudaStream_t stream);
+
+// ---------------------------------------------------------------- k-hop
+// Sampled k-hop computational graphs (ref inc/khop.hpp:35-88, src/khop.cpp),
+// built on the device from a resident snapshot. Sampling is bit-exact with the
+// reference: per (destination, hop) an mt19937_64 seeded with
+// derive_seed(seed, dst, hop) drives a partial Fisher-Yates over the
+// destination's ascending in-neighbours with libstdc++'s
+// uniform_int_distribution<size_t> (Lemire's nearly-divisionless method).
+struct DevHop {
+  int64_t n_dest = 0, n_edges = 0;
+  cuda::DevArray<int32_t> dests;   // sorted
+  cuda::DevArray<uint64_t> edges;  // sorted (src << 32 | dst), dst in dests
+};
+
+struct DevCompGraph {
+  std::vector<int32_t> seeds;    // sorted unique (host)
+  std::vector<int32_t> fanouts;  // -1 = full
+  uint64_t sample_seed = 0;
+  std::vector<DevHop> hops;
+};
+
+struct DevCgUpdate {
+  struct Diff {
+    int64_t n_added = 0, n_removed = 0;
+    cuda::DevArray<uint64_t> added, removed;  // sorted keys
+  };
+  std::vector<Diff> hops;
+  bool empty() const {
+    for (const auto& h : hops)
+      if (h.n_added || h.n_removed) return false;
+    return true;
+  }
+};
+
+// khop (src/khop.cpp:66-96): reference checks and messages.
+DevCompGraph khop(const DevSnapshot& snap, int32_t num_nodes, std::vector<int32_t> seeds,
+                  std::vector<int32_t> fanouts, uint64_t seed, cudaStream_t stream);
+// khop_delta (src/khop.cpp:105-121): fresh k-hop graph of `curr`, per-hop set
+// differences against prev.
+DevCgUpdate khop_delta(const DevCompGraph& prev, const DevSnapshot& curr, int32_t num_nodes,
+                       cudaStream_t stream);
+// apply_cg_update (src/khop.cpp:123-150).
+DevCompGraph apply_cg_update(const DevCompGraph& prev, const DevCgUpdate& update,
+                             cudaStream_t stream);
+
 }  // namespace dgnn

@@ -531,12 +531,15 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
 // ------------------------------------------------------------- weight gradient
 // Partial D'_cta (Mg x Npad) = sum over this CTA's rows of G^T(:, rows) *
 // [X | Hm | 1](rows, :), with Mg = 4H in {128, 256} and Npad >= in + H + 1.
-// Warps 0-7 copy raw 16-row chunks (cp.async, two chunks ahead) and write
-// the transposed, 3xTF32-split operands; warp 8 issues the MMAs. Hand-offs
+// Warps 0-15 copy raw 16-row chunks (cp.async, two chunks ahead) and write
+// the transposed, 3xTF32-split operands; warp 16 issues the MMAs; warps 0-7
+// drain the TMEM partial. Hand-offs
 // are mbarriers only (no block-wide barrier per chunk): raw chunk landed
 // (cp.async.mbarrier.arrive.noinc from every copier), raw slot consumed,
 // operand stage full (every converter), stage free (tcgen05.commit).
-constexpr int kWgConv = 256;               // copy + convert threads
+// copy + convert threads: the conversion is issue-latency bound (ncu: "wait"
+// and long-scoreboard stalls with 2 warps per scheduler at 256 threads)
+constexpr int kWgConv = 512;
 constexpr int kThreads = kWgConv + 32;     // + the MMA warp
 constexpr int kKW = 16;  // rows (the MMA K) per staged chunk
 
@@ -597,7 +600,7 @@ k_wgrad(int M, int in, int H, const float* __restrict__ G, const float* __restri
   const int64_t re = rb + per < M ? rb + per : M;
   const int nchunks = re > rb ? static_cast<int>((re - rb + kKW - 1) / kKW) : 0;
 
-  if (warp < 8) {
+  if (warp < kWgConv / 32) {
     // ---------------- copy + convert
     // raw slot layout: G [kKW][MG] | X [kKW][in] | Hm [kKW][H]
     const uint32_t raw0 = sbase + S::kRawOff;
@@ -668,7 +671,7 @@ k_wgrad(int M, int in, int H, const float* __restrict__ G, const float* __restri
       mbar_arrive(&rawempty[r]);
     }
   } else if (lane == 0) {
-    // ---------------- MMA issuer (warp 8)
+    // ---------------- MMA issuer (warp kWgConv / 32)
     constexpr uint32_t idesc = idesc_tf32(128, NPAD);
     constexpr uint32_t lboA = tile_lbo(MG), lboB = tile_lbo(NPAD);
     for (int c = 0; c < nchunks; ++c) {

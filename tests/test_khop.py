@@ -1,0 +1,76 @@
+"""Sampled k-hop computational graphs on the device against
+the compiled reference's khop / to_view / khop_delta / apply_cg_update
+(src/khop.cpp:12-150): destinations, sampled edges, views and per-hop
+updates must be bitwise identical (the sampler replays the reference's
+mt19937_64 / uniform_int_distribution draws)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GRAPH = dict(n=600, avg_degree=12, dim=4, T=4, edge=0.05, feat=0.05)
+CASES = [
+    ([0, 5, 17, 599], [5, 3], 7),
+    (list(range(0, 600, 7)), [25, 10], 1),
+    ([3, 3, 1, 2], [1, -1], 11),
+    (list(range(40)), [-1, -1], 2),
+    ([10, 20, 30], [2, 3, 4], 123456789),
+]
+
+
+@pytest.fixture(scope="module")
+def graphs(ref):
+    import torch
+    assert torch.cuda.is_available()
+    from paper_2501_15348_b200 import api
+    g = GRAPH
+    args = (g["n"], g["avg_degree"], g["dim"], g["T"], g["edge"], g["feat"])
+    return api, ref.RefGraph.synth(*args, seed=3), api.Synth(*args, seed=3).to_graph()
+
+
+def _same_hops(a, b):
+    assert len(a) == len(b)
+    for k, (x, y) in enumerate(zip(a, b)):
+        for key in ("dests", "src", "dst"):
+            assert np.array_equal(x[key], y[key]), (k, key)
+
+
+@pytest.mark.parametrize("case", range(len(CASES)))
+@pytest.mark.parametrize("t", [0, 2])
+def test_khop_bitwise(ref, graphs, case, t):
+    api, gr, g = graphs
+    seeds, fanouts, seed = CASES[case]
+    cr = ref.RefCompGraph.khop(gr, t, seeds, fanouts, seed)
+    c = api.ComputationalGraph.khop(g, t, seeds, fanouts, seed)
+    _same_hops(c.hops(), cr.hops())
+    for a, b in zip(c.view(), cr.view()):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_khop_delta_and_apply_bitwise(ref, graphs, case):
+    api, gr, g = graphs
+    seeds, fanouts, seed = CASES[case]
+    for t in range(1, GRAPH["T"]):
+        cr = ref.RefCompGraph.khop(gr, t - 1, seeds, fanouts, seed)
+        c = api.ComputationalGraph.khop(g, t - 1, seeds, fanouts, seed)
+        hr, er, ar = cr.delta(gr, t)
+        h, e, a = c.delta(g, t)
+        assert e == er
+        for x, y in zip(h, hr):
+            for key in x:
+                assert np.array_equal(x[key], y[key]), (t, key)
+        _same_hops(a.hops(), ar.hops())
+        # applying the update yields the fresh sample of snapshot t
+        _same_hops(a.hops(), api.ComputationalGraph.khop(g, t, seeds, fanouts, seed).hops())
+
+
+@pytest.mark.parametrize("seeds,fanouts", [([], [2]), ([1], []), ([1, 600], [2]), ([1], [0]),
+                                           ([-1], [2]), ([1], [-2])])
+def test_khop_rejects_like_reference(ref, graphs, seeds, fanouts):
+    api, gr, g = graphs
+    with pytest.raises(ValueError) as er:
+        ref.RefCompGraph.khop(gr, 0, seeds, fanouts, 1)
+    with pytest.raises(ValueError) as eo:
+        api.ComputationalGraph.khop(g, 0, seeds, fanouts, 1)
+    assert str(er.value) == "invalid_argument: " + str(eo.value)
