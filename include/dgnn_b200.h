@@ -227,6 +227,10 @@ typedef struct dgnn_run_cfg {
   int32_t window_total; /* sliding_windows total T' (0 -> T-1) */
   int32_t record_events;
   int64_t hbm_cache_budget_bytes; /* 0 = no second cache level */
+  /* ModelConfig::fanouts (inc/model.hpp:37): 0 hops or all -1 = whole-snapshot
+   * views; otherwise sampled k-hop views per sample (src/train.cpp:86-98). */
+  int32_t n_fanouts;
+  int32_t fanouts[8];
 } dgnn_run_cfg;
 
 typedef struct dgnn_epoch_report {

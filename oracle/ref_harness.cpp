@@ -83,6 +83,8 @@ struct RefRunCfg {
   int32_t epochs;
   int32_t window_total;    // T' passed to sliding_windows (T-1)
   int32_t record_events;
+  int32_t n_fanouts;       // ModelConfig::fanouts (inc/model.hpp:37)
+  int32_t fanouts[8];
 };
 
 const char* ref_last_error() { return g_err.c_str(); }
@@ -431,6 +433,7 @@ ModelConfig model_cfg(const RefRunCfg& c, Eigen::Index feature_dim) {
   m.aggr = AggrFn{static_cast<AggrKind>(c.aggr)};
   m.fanouts = {kFullFanout, kFullFanout};
   m.seed = c.seed;
+  m.fanouts.assign(c.fanouts, c.fanouts + c.n_fanouts);
   return m;
 }
 

@@ -31,7 +31,7 @@ class RefRunCfg(C.Structure):
         ("fallback_threshold", C.c_double), ("rescratch_period", C.c_int32),
         ("incremental", C.c_int32), ("cache_policy", C.c_int32), ("cache_frac", C.c_double),
         ("workers", C.c_int32), ("epochs", C.c_int32), ("window_total", C.c_int32),
-        ("record_events", C.c_int32),
+        ("record_events", C.c_int32), ("n_fanouts", C.c_int32), ("fanouts", C.c_int32 * 8),
     ]
 
 
@@ -59,6 +59,7 @@ class RunCfg:
     epochs: int = 1
     window_total: int = 0  # 0 -> T-1
     record_events: bool = True
+    fanouts: tuple = ()
 
     def to_c(self, T: int) -> RefRunCfg:
         c = RefRunCfg()
@@ -83,6 +84,9 @@ class RunCfg:
         c.epochs = self.epochs
         c.window_total = self.window_total if self.window_total > 0 else T - 1
         c.record_events = int(self.record_events)
+        c.n_fanouts = len(self.fanouts)
+        for i, f in enumerate(self.fanouts):
+            c.fanouts[i] = f
         return c
 
 

@@ -562,6 +562,7 @@ class TrainConfig:
     window_total: int = 0
     record_events: bool = False
     hbm_cache_budget_bytes: int = 0
+    fanouts: tuple = ()  # () or all -1: whole-snapshot views; else sampled k-hop views
 
     def to_c(self) -> _lib.RunCfg:
         c = _lib.RunCfg()
@@ -573,6 +574,11 @@ class TrainConfig:
         c.incremental, c.cache_policy, c.cache_frac = int(self.incremental), POLICY[self.cache], self.cache_frac
         c.workers, c.epochs, c.window_total = self.workers, self.epochs, self.window_total
         c.record_events, c.hbm_cache_budget_bytes = int(self.record_events), self.hbm_cache_budget_bytes
+        if len(self.fanouts) > 8:
+            raise ValueError("at most 8 fanout hops")
+        c.n_fanouts = len(self.fanouts)
+        for i, f in enumerate(self.fanouts):
+            c.fanouts[i] = f
         return c
 
 

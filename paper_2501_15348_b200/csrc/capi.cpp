@@ -790,7 +790,7 @@ int dgnn_cell_forward(int32_t lstm, int32_t n, int32_t in, int32_t H, const floa
     cudaStream_t st = as_stream(stream);
     if (cuda::umma_cell_supported(in, H)) {
       cuda::DevArray<float> img(cuda::umma_bimage_floats(4 * H, in + H), st);
-      cuda::umma_pack_b(W, 4 * H, true, 0, 4 * H, in + H, img.get(), st);
+      cuda::umma_pack_cell_image(lstm != 0, W, in, H, img.get(), st);
       cuda::umma_cell_forward(lstm != 0, n, in, H, X, Hm, h_skip, c_prev, img.get(), bias, gates,
                               c, h, st);
       DGNN_CUDA(cudaStreamSynchronize(st));
@@ -861,6 +861,8 @@ void fill_configs(dgnn_session* s) {
   check(c.aggr >= 0 && c.aggr <= 3, "unknown aggregation kind");
   m.aggr = AggrFn{static_cast<AggrKind>(c.aggr)};
   m.seed = c.seed;
+  check(c.n_fanouts >= 0 && c.n_fanouts <= 8, "at most 8 fanout hops");
+  m.fanouts.assign(c.fanouts, c.fanouts + c.n_fanouts);
   TrainConfig& t = s->tcfg;
   t.batch_size = c.batch_size;
   t.epochs = c.epochs;
@@ -1047,7 +1049,7 @@ int dgnn_session_sample_grads(dgnn_session* s, int32_t window_index, double* los
     auto batches = make_batches(G.num_nodes(), s->tcfg.batch_size, s->tcfg.seed, 0);
     SeqSample sample = build_sample(G, s->mcfg, windows[window_index],
                                     static_cast<Timestep>(windows.size() - 1 - window_index), 0,
-                                    batches[0], st);
+                                    batches[0], s->tcfg.seed, st);
     ForwardArtifacts fwd = model_forward(model, sample, fresh.provider());
     cuda::DevArray<double> slot(1, st), ws(512, st);
     slot.zero(st);

@@ -286,7 +286,7 @@ void DgnnModel::refresh_packed() {
     cuda::transpose(c.in + c.H, 4 * c.H, c.W.get(), c.WT.get(), stream_);
     if (c.umma) {
       const int K = c.in + c.H, NC = 4 * c.H;
-      cuda::umma_pack_b(c.W.get(), NC, true, 0, NC, K, c.Bf.get(), stream_);       // W^T
+      cuda::umma_pack_cell_image(c.lstm, c.W.get(), c.in, c.H, c.Bf.get(), stream_);  // W^T
       cuda::umma_pack_b(c.W.get(), NC, false, 0, K, NC, c.Bb.get(), stream_);      // W
       cuda::umma_pack_b(c.W.get(), NC, false, c.in, c.H, NC, c.Bbh.get(), stream_);  // W[in:]
     }
@@ -305,8 +305,7 @@ void DgnnModel::refresh_packed() {
 
 SeqSample build_sample(const DeviceGraph& graph, const ModelConfig& mcfg,
                        const SequenceWindow& window, Timestep windows_remaining, int64_t batch_id,
-                       std::pair<NodeId, NodeId> node_range, cudaStream_t stream) {
-  (void)mcfg;
+                       std::pair<NodeId, NodeId> node_range, uint64_t seed, cudaStream_t stream) {
   SeqSample s;
   s.window = window;
   s.batch_id = batch_id;
@@ -314,7 +313,37 @@ SeqSample build_sample(const DeviceGraph& graph, const ModelConfig& mcfg,
   s.seed_begin = node_range.first;
   s.seed_end = node_range.second;
   const Timestep span = window.length + window.horizon;
-  for (Timestep i = 0; i < span; ++i) s.views.push_back(GraphView::of(graph, window.start + i));
+  bool whole = true;  // full_fanouts (src/train.cpp:68-73)
+  for (int32_t f : mcfg.fanouts)
+    if (f != -1) whole = false;
+  std::vector<int32_t> seeds;
+  if (!whole)
+    for (NodeId v = node_range.first; v < node_range.second; ++v) seeds.push_back(v);
+  for (Timestep i = 0; i < span; ++i) {
+    const Timestep t = window.start + i;
+    if (whole) {
+      s.views.push_back(GraphView::of(graph, t));
+      continue;
+    }
+    // sampled k-hop view of snapshot t (src/train.cpp:93-97), built on the
+    // device on the graph's stream, ordered before `stream`
+    const DevSnapshot& snap = graph.snapshot(t);
+    DevCompGraph cg = khop(snap, graph.num_nodes(), seeds, mcfg.fanouts,
+                           derive_seed(seed, static_cast<uint64_t>(t)), stream);
+    const DevHop& deep = cg.hops.back();
+    s.owned.push_back(std::make_shared<DevSnapshot>(
+        csr_from_keys(deep.edges.get(), deep.n_edges, graph.num_nodes(), stream)));
+    const DevSnapshot& o = *s.owned.back();
+    GraphView v;
+    v.num_nodes = graph.num_nodes();
+    v.num_edges = o.num_edges;
+    v.in_ptr = o.in_ptr.get();
+    v.in_src = o.in_src.get();
+    v.out_ptr = o.out_ptr.get();
+    v.out_dst = o.out_dst.get();
+    v.t = t;
+    s.views.push_back(v);
+  }
   // snapshot(t) bound check reproduces the reference's .at()
   for (Timestep i = 0; i <= span; ++i) {
     s.feat_refs.push_back(graph.features(window.start + i, stream));

@@ -50,6 +50,7 @@ struct ModelConfig {
   bool teacher_forcing = true;
   AggrFn aggr;
   uint64_t seed = 1;
+  std::vector<int32_t> fanouts;  // empty or all -1: whole-snapshot views (inc/model.hpp:37)
 };
 
 // Parameter names in visit_params order (src/model.cpp:72-89) and the fp64
@@ -142,6 +143,7 @@ class DgnnModel {
 struct SeqSample {
   SequenceWindow window;
   std::vector<GraphView> views;       // L+H views
+  std::vector<std::shared_ptr<DevSnapshot>> owned;  // sampled k-hop views (to_view)
   std::vector<const float*> feats;    // L+H+1 feature matrices (device)
   std::vector<FeatRef> feat_refs;     // their version leases (resident while the sample lives)
   NodeId seed_begin = 0, seed_end = 0;  // loss rows (contiguous node range)
@@ -151,7 +153,7 @@ struct SeqSample {
 
 SeqSample build_sample(const DeviceGraph& graph, const ModelConfig& mcfg,
                        const SequenceWindow& window, Timestep windows_remaining, int64_t batch_id,
-                       std::pair<NodeId, NodeId> node_range, cudaStream_t stream);
+                       std::pair<NodeId, NodeId> node_range, uint64_t seed, cudaStream_t stream);
 
 struct CellTape {
   Buf gates;      // n x 4H (LSTM i,f,g,o; GRU r,z,n,hn)

@@ -106,7 +106,8 @@ void Worker::run_sample(const SequenceWindow& window, Timestep windows_remaining
   {
     ProfScope whole(kProfSample, stream_, 0.0);
     SeqSample sample =
-        build_sample(graph_, model_.cfg_, window, windows_remaining, batch_id, node_range, stream_);
+        build_sample(graph_, model_.cfg_, window, windows_remaining, batch_id, node_range,
+                     cfg_.seed, stream_);
     prof_add_host(kProfHostBuild, since(h0));
     const auto h1 = clk::now();
     Lanes lanes(stream_, aux_);

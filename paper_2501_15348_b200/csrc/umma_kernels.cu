@@ -56,8 +56,10 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, float a, float b, fl
 // ------------------------------------------------------------- B images
 // out: per K chunk c: [hi tile (Npad x KC)][lo tile], canonical layout.
 // B(n, k) = trans ? M[k * ld + (n0 + n)] : M[(n0 + n) * ld + k]; zero padded.
+// perm_h > 0: GRU column blocks stored as [n | r | z | hn] (source blocks
+// r, z, n, hn = 0..3 of width perm_h), see RowGemmArgs::gru_split.
 __global__ void k_pack_b(const float* __restrict__ M, int ld, int trans, int n0, int N, int K,
-                         int Npad, int nchunks, float* __restrict__ out) {
+                         int Npad, int nchunks, float* __restrict__ out, int perm_h) {
   const int64_t per_tile = tile_bytes(Npad, kKC) / 4;
   const int64_t total = static_cast<int64_t>(nchunks) * Npad * kKC;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -66,8 +68,13 @@ __global__ void k_pack_b(const float* __restrict__ M, int ld, int trans, int n0,
     const int rem = static_cast<int>(i - static_cast<int64_t>(c) * Npad * kKC);
     const int n = rem / kKC, kk = rem % kKC;
     const int k = c * kKC + kk;
+    int ns = n;
+    if (perm_h > 0 && n < N) {
+      const int blk = n / perm_h;
+      ns = (blk == 0 ? 2 : (blk == 3 ? 3 : blk - 1)) * perm_h + n % perm_h;
+    }
     float v = 0.f;
-    if (n < N && k < K) v = trans ? M[static_cast<int64_t>(k) * ld + n0 + n] : M[static_cast<int64_t>(n0 + n) * ld + k];
+    if (n < N && k < K) v = trans ? M[static_cast<int64_t>(k) * ld + n0 + ns] : M[static_cast<int64_t>(n0 + ns) * ld + k];
     float hi, lo;
     split_tf32(v, hi, lo);
     float* base = out + static_cast<int64_t>(c) * 2 * per_tile;
@@ -114,6 +121,12 @@ struct RowGemmArgs {
   float* C1;
   float* C2;
   int store_accumulate;
+  // GRU block-sparse contraction (0 = off, else H): the B image holds the
+  // gate columns as [n | r | z | hn]; X-only K chunks skip the hn block
+  // (X has no h-part of the candidate gate) and Hm-only chunks skip the
+  // x-part n block, i.e. N = 3H instead of 4H after a full-N first chunk
+  // that initialises every accumulator column.
+  int gru_split;
   // profiling switches (env DGNN_UMMA_DEBUG): 1 skip epilogue math/stores,
   // 2 skip the B copy, 4 skip the A split/stores
   int debug;
@@ -289,6 +302,9 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
     // ---------------- MMA issuer
     constexpr uint32_t idesc = idesc_tf32(kTileM, NPAD);
     constexpr uint32_t lboA = tile_lbo(kTileM), lboB = tile_lbo(NPAD);
+    const int gs = (EPI == kEpiGru || EPI == kEpiGruBwd) ? p.gru_split : 0;
+    const uint32_t idesc3 = gs ? idesc_tf32(kTileM, 3 * gs) : idesc;
+    const uint32_t boffH = static_cast<uint32_t>(gs / 8) * 128u;  // B rows [H, 4H)
     uint32_t g = 0, it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const uint32_t b = it & 1u;
@@ -301,15 +317,25 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
         fence_after_sync();
         const uint32_t st = sbase + s * S::kStage;
         if (lane == 0) {
+          // GRU split: chunk 0 full N; X chunks N = 3H at column 0 ([n r z]);
+          // Hm chunks N = 3H at column H ([r z hn])
+          uint32_t id = idesc, dd = d, bo = 0;
+          if (gs && c > 0) {
+            id = idesc3;
+            if (c * kKC >= p.k1) {
+              dd = d + static_cast<uint32_t>(gs);
+              bo = boffH;
+            }
+          }
 #pragma unroll
           for (int ks = 0; ks < kKC / 8; ++ks) {
             const uint64_t ahi = make_desc(st + 2 * ks * lboA, lboA, 128);
             const uint64_t alo = make_desc(st + S::kA + 2 * ks * lboA, lboA, 128);
-            const uint64_t bhi = make_desc(st + 2 * S::kA + 2 * ks * lboB, lboB, 128);
-            const uint64_t blo = make_desc(st + 2 * S::kA + S::kB + 2 * ks * lboB, lboB, 128);
-            mma_tf32(d, ahi, bhi, idesc, (c > 0 || ks > 0) ? 1u : 0u);
-            mma_tf32(d, ahi, blo, idesc, 1u);
-            mma_tf32(d, alo, bhi, idesc, 1u);
+            const uint64_t bhi = make_desc(st + 2 * S::kA + 2 * ks * lboB + bo, lboB, 128);
+            const uint64_t blo = make_desc(st + 2 * S::kA + S::kB + 2 * ks * lboB + bo, lboB, 128);
+            mma_tf32(dd, ahi, bhi, id, (c > 0 || ks > 0) ? 1u : 0u);
+            mma_tf32(dd, ahi, blo, id, 1u);
+            mma_tf32(dd, alo, bhi, id, 1u);
           }
           commit(&empty[s]);
           if (c == p.nchunks - 1) commit(&tfull[b]);
@@ -364,15 +390,18 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
           for (int u = 0; u < 16; ++u) v[u] = 0.f;
         }
       };
+      // accumulator column block of each gate (GRU split: [n | r | z | hn])
+      const bool gsplit = (EPI == kEpiGru || EPI == kEpiGruBwd) && p.gru_split;
+      const int cb0 = gsplit ? p.H : 0, cb1 = gsplit ? 2 * p.H : p.H, cb2 = gsplit ? 0 : 2 * p.H;
       if (EPI == kEpiLstmBwd || EPI == kEpiGruBwd) {
         const int H = p.H;
         const int U = H / 2;
         for (int j0 = half * U; j0 < (half + 1) * U; j0 += 16) {
           float a0[16], a1[16], a2[16], a3[16];
           float cv[16];  // out: dc_prev (LSTM) / dh_skip (GRU)
-          tmem_ld16(trow + 0 * H + j0, a0);
-          tmem_ld16(trow + 1 * H + j0, a1);
-          tmem_ld16(trow + 2 * H + j0, a2);
+          tmem_ld16(trow + cb0 + j0, a0);
+          tmem_ld16(trow + cb1 + j0, a1);
+          tmem_ld16(trow + cb2 + j0, a2);
           tmem_ld16(trow + 3 * H + j0, a3);
           tmem_wait_ld();
           // per-row operands 4 columns at a time (register budget of 152)
@@ -433,9 +462,9 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
           // state row prefetch overlaps the TMEM reads
           float sv[16];
           load16(EPI == kEpiLstm ? p.c_prev : p.h_skip, j0, sv);
-          tmem_ld16(trow + 0 * H + j0, a0);
-          tmem_ld16(trow + 1 * H + j0, a1);
-          tmem_ld16(trow + 2 * H + j0, a2);
+          tmem_ld16(trow + cb0 + j0, a0);
+          tmem_ld16(trow + cb1 + j0, a1);
+          tmem_ld16(trow + cb2 + j0, a2);
           tmem_ld16(trow + 3 * H + j0, a3);
           tmem_wait_ld();
           if (!(p.debug & 1)) {
@@ -806,7 +835,24 @@ void umma_pack_b(const float* M, int ld, bool trans, int n0, int N, int K, float
   const int nchunks = (K + kKC - 1) / kKC;
   const int64_t total = static_cast<int64_t>(nchunks) * npad * kKC;
   DGNN_LAUNCH(k_pack_b, wave_grid(total, 256, 4), 256, 0, stream, M, ld, trans ? 1 : 0, n0, N, K,
-              npad, nchunks, out);
+              npad, nchunks, out, 0);
+}
+
+bool umma_gru_split(bool lstm, int in, int H) {
+  static const bool on = [] {
+    const char* e = std::getenv("DGNN_GRU_SPLIT");
+    return !(e && e[0] == '0');
+  }();
+  return on && !lstm && in % kKC == 0 && H % 16 == 0 && umma_npad(4 * H) == 4 * H;
+}
+
+void umma_pack_cell_image(bool lstm, const float* W, int in, int H, float* out, cudaStream_t stream) {
+  const int N = 4 * H, K = in + H;
+  const int npad = umma_npad(N);
+  const int nchunks = (K + kKC - 1) / kKC;
+  const int64_t total = static_cast<int64_t>(nchunks) * npad * kKC;
+  DGNN_LAUNCH(k_pack_b, wave_grid(total, 256, 4), 256, 0, stream, W, N, 1, 0, N, K, npad, nchunks,
+              out, umma_gru_split(lstm, in, H) ? H : 0);
 }
 
 void umma_cell_forward(bool lstm, int n, int in, int H, const float* X, const float* Hm,
@@ -828,6 +874,7 @@ void umma_cell_forward(bool lstm, int n, int in, int H, const float* X, const fl
   a.gates = gates;
   a.c_out = c;
   a.h_out = h;
+  a.gru_split = umma_gru_split(lstm, in, H) ? H : 0;
   a.debug = umma_debug_flags();
   const int npad = umma_npad(4 * H);
   if (lstm) dispatch_row_gemm<kEpiLstm>(npad, a, stream);
@@ -855,6 +902,7 @@ void umma_cell_backward_recompute(bool lstm, int n, int in, int H, const float* 
   a.dc = dc;
   a.G = G;
   a.dstate = dstate;
+  a.gru_split = umma_gru_split(lstm, in, H) ? H : 0;
   a.debug = umma_debug_flags();
   const int npad = umma_npad(4 * H);
   if (lstm) dispatch_row_gemm<kEpiLstmBwd>(npad, a, stream);

@@ -18,6 +18,11 @@ int umma_npad(int N);
 int64_t umma_bimage_floats(int N, int K);
 // Packed B image: B(n, k) = trans ? M[k*ld + n0+n] : M[(n0+n)*ld + k], split
 // into TF32 hi/lo tiles in the canonical UMMA layout, K chunked by 32.
+// Forward-contraction B image of a packed cell weight W ((in+H) x 4H): W^T,
+// GRU gate columns permuted when umma_gru_split (used by umma_cell_forward /
+// umma_cell_backward_recompute, which must be given this image).
+bool umma_gru_split(bool lstm, int in, int H);
+void umma_pack_cell_image(bool lstm, const float* W, int in, int H, float* out, cudaStream_t stream);
 void umma_pack_b(const float* M, int ld, bool trans, int n0, int N, int K, float* out,
                  cudaStream_t stream);
 
