@@ -231,6 +231,7 @@ typedef struct dgnn_run_cfg {
    * views; otherwise sampled k-hop views per sample (src/train.cpp:86-98). */
   int32_t n_fanouts;
   int32_t fanouts[8];
+  int32_t iteration; /* IterationOrder (inc/train.hpp:17): 0 seq-first, 1 node-first */
 } dgnn_run_cfg;
 
 typedef struct dgnn_epoch_report {

@@ -85,6 +85,7 @@ struct RefRunCfg {
   int32_t record_events;
   int32_t n_fanouts;       // ModelConfig::fanouts (inc/model.hpp:37)
   int32_t fanouts[8];
+  int32_t iteration;       // 0 seq-first, 1 node-first
 };
 
 const char* ref_last_error() { return g_err.c_str(); }
@@ -589,7 +590,9 @@ void* ref_run(void* g, const RefRunCfg* cfg) {
     const auto t0 = std::chrono::steady_clock::now();
     for (int e = 0; e < c.epochs; ++e) {
       if (c.workers <= 0) {
-        EpochReport r = seq_first_epoch(model, G, windows, tcfg, *provs[0], opt, e);
+        EpochReport r = c.iteration == 0
+                            ? seq_first_epoch(model, G, windows, tcfg, *provs[0], opt, e)
+                            : node_first_epoch(model, G, windows, tcfg, *provs[0], opt, e);
         res->losses.insert(res->losses.end(), r.sample_losses.begin(), r.sample_losses.end());
         for (auto [b, w] : r.visitation) {
           int64_t row[3] = {0, b, w};

@@ -32,6 +32,7 @@ class RefRunCfg(C.Structure):
         ("incremental", C.c_int32), ("cache_policy", C.c_int32), ("cache_frac", C.c_double),
         ("workers", C.c_int32), ("epochs", C.c_int32), ("window_total", C.c_int32),
         ("record_events", C.c_int32), ("n_fanouts", C.c_int32), ("fanouts", C.c_int32 * 8),
+        ("iteration", C.c_int32),
     ]
 
 
@@ -60,6 +61,7 @@ class RunCfg:
     window_total: int = 0  # 0 -> T-1
     record_events: bool = True
     fanouts: tuple = ()
+    iteration: str = "seq_first"
 
     def to_c(self, T: int) -> RefRunCfg:
         c = RefRunCfg()
@@ -87,6 +89,7 @@ class RunCfg:
         c.n_fanouts = len(self.fanouts)
         for i, f in enumerate(self.fanouts):
             c.fanouts[i] = f
+        c.iteration = {"seq_first": 0, "node_first": 1}[self.iteration]
         return c
 
 

@@ -25,7 +25,7 @@ class RunCfg(C.Structure):
         ("rescratch_period", I32), ("incremental", I32), ("cache_policy", I32),
         ("cache_frac", D), ("workers", I32), ("epochs", I32), ("window_total", I32),
         ("record_events", I32), ("hbm_cache_budget_bytes", I64),
-        ("n_fanouts", I32), ("fanouts", I32 * 8),
+        ("n_fanouts", I32), ("fanouts", I32 * 8), ("iteration", I32),
     ]
 
 

@@ -563,6 +563,7 @@ class TrainConfig:
     record_events: bool = False
     hbm_cache_budget_bytes: int = 0
     fanouts: tuple = ()  # () or all -1: whole-snapshot views; else sampled k-hop views
+    iteration: str = "seq_first"  # or "node_first" (ref IterationOrder)
 
     def to_c(self) -> _lib.RunCfg:
         c = _lib.RunCfg()
@@ -579,6 +580,7 @@ class TrainConfig:
         c.n_fanouts = len(self.fanouts)
         for i, f in enumerate(self.fanouts):
             c.fanouts[i] = f
+        c.iteration = {"seq_first": 0, "node_first": 1}[self.iteration]
         return c
 
 

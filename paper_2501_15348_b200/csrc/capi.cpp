@@ -822,10 +822,12 @@ int dgnn_cell_backward(int32_t lstm, int32_t n, int32_t in, int32_t H, const flo
       cuda::DevArray<float> img(cuda::umma_bimage_floats(K, 4 * H), st);
       if (dX) {
         cuda::umma_pack_b(W, 4 * H, false, 0, K, 4 * H, img.get(), st);
-        cuda::umma_gemm_store2(n, 4 * H, G.get(), img.get(), in, H, dX, dHm, st);
+        cuda::umma_gemm_store2(n, 4 * H, G.get(), img.get(), in, H, dX, dHm, st, nullptr, false,
+                               lstm ? 0 : H);
       } else {
         cuda::umma_pack_b(W, 4 * H, false, in, H, 4 * H, img.get(), st);
-        cuda::umma_gemm_store2(n, 4 * H, G.get(), img.get(), H, 0, dHm, nullptr, st);
+        cuda::umma_gemm_store2(n, 4 * H, G.get(), img.get(), H, 0, dHm, nullptr, st, nullptr, false,
+                               lstm ? 0 : H);
       }
       cuda::unpack_cell_grad(lstm != 0, in, H, dW.get(), db.get(), dflat, st);
       DGNN_CUDA(cudaStreamSynchronize(st));
@@ -881,6 +883,8 @@ void fill_configs(dgnn_session* s) {
   }
   t.cache_capacity_frac = c.cache_frac;
   t.hbm_cache_budget_bytes = c.hbm_cache_budget_bytes;
+  check(c.iteration == 0 || c.iteration == 1, "unknown iteration order");
+  t.iteration = c.iteration == 0 ? IterationOrder::kSeqFirst : IterationOrder::kNodeFirst;
 }
 
 void attach_observer(dgnn_session* s) {

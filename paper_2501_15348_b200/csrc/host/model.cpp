@@ -655,9 +655,11 @@ StepGrads cell_step_backward(CellSlot& c, const CellTape& tape, const float* X, 
                  2.0 * n * 4 * H * ((need_dx ? in : 0) + H));
     if (c.umma) {
       if (need_dx) {
-        cuda::umma_gemm_store2(n, 4 * H, G->get(), c.Bb.get(), in, H, dX->get(), dHm->get(), st);
+        cuda::umma_gemm_store2(n, 4 * H, G->get(), c.Bb.get(), in, H, dX->get(), dHm->get(), st,
+                               nullptr, false, c.lstm ? 0 : H);
       } else {
-        cuda::umma_gemm_store2(n, 4 * H, G->get(), c.Bbh.get(), H, 0, dHm->get(), nullptr, st);
+        cuda::umma_gemm_store2(n, 4 * H, G->get(), c.Bbh.get(), H, 0, dHm->get(), nullptr, st,
+                               nullptr, false, c.lstm ? 0 : H);
       }
     } else if (need_dx) {
       cuda::gemm_nn(n, 4 * H, 0, in, H, G->get(), nullptr, c.WT.get(), in + H, nullptr, false,

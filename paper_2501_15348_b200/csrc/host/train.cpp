@@ -123,9 +123,14 @@ void Worker::run_sample(const SequenceWindow& window, Timestep windows_remaining
 }
 
 // ---------------------------------------------------------------- seq-first
-EpochReport seq_first_epoch(DgnnModel& model, const DeviceGraph& graph,
-                            const std::vector<SequenceWindow>& windows, const TrainConfig& cfg,
-                            Worker& worker, OptimizerState& opt, int64_t epoch_index) {
+namespace {
+
+// run_epoch_impl (ref src/train.cpp:146-206): seq-first visits (batch outer,
+// window inner), node-first (window outer, batch inner).
+EpochReport run_epoch_impl(DgnnModel& model, const DeviceGraph& graph,
+                           const std::vector<SequenceWindow>& windows, const TrainConfig& cfg,
+                           Worker& worker, OptimizerState& opt, int64_t epoch_index,
+                           bool seq_first) {
   check(!windows.empty(), "epoch needs at least one window");
   cudaStream_t st = worker.stream();
   AggProvider& provider = worker.provider();
@@ -143,15 +148,21 @@ EpochReport seq_first_epoch(DgnnModel& model, const DeviceGraph& graph,
   losses.zero(st);
   cuda::DevArray<float> grad(model.num_params(), st);
   int64_t k = 0;
-  for (int64_t b = 0; b < static_cast<int64_t>(batches.size()); ++b) {
-    for (int64_t w = 0; w < static_cast<int64_t>(windows.size()); ++w) {
-      grad.zero(st);
-      worker.run_sample(windows[w], static_cast<Timestep>(windows.size() - 1 - w), b, batches[b],
-                        grad.get(), losses.get() + k);
-      if (!optimizer_step(model, grad.get(), 1.f, opt, cfg, provider.store(), st)) ++report.skipped_steps;
-      report.visitation.push_back({b, w});
-      ++k;
-    }
+  auto run = [&](int64_t b, int64_t w) {
+    grad.zero(st);
+    worker.run_sample(windows[w], static_cast<Timestep>(windows.size() - 1 - w), b, batches[b],
+                      grad.get(), losses.get() + k);
+    if (!optimizer_step(model, grad.get(), 1.f, opt, cfg, provider.store(), st)) ++report.skipped_steps;
+    report.visitation.push_back({b, w});
+    ++k;
+  };
+  const int64_t nb = static_cast<int64_t>(batches.size()), nw = static_cast<int64_t>(windows.size());
+  if (seq_first) {
+    for (int64_t b = 0; b < nb; ++b)
+      for (int64_t w = 0; w < nw; ++w) run(b, w);
+  } else {
+    for (int64_t w = 0; w < nw; ++w)
+      for (int64_t b = 0; b < nb; ++b) run(b, w);
   }
   DGNN_CUDA(cudaEventRecord(e1, st));
   report.sample_losses.resize(nsamples);
@@ -183,6 +194,20 @@ EpochReport seq_first_epoch(DgnnModel& model, const DeviceGraph& graph,
   return report;
 }
 
+}  // namespace
+
+EpochReport seq_first_epoch(DgnnModel& model, const DeviceGraph& graph,
+                            const std::vector<SequenceWindow>& windows, const TrainConfig& cfg,
+                            Worker& worker, OptimizerState& opt, int64_t epoch_index) {
+  return run_epoch_impl(model, graph, windows, cfg, worker, opt, epoch_index, true);
+}
+
+EpochReport node_first_epoch(DgnnModel& model, const DeviceGraph& graph,
+                             const std::vector<SequenceWindow>& windows, const TrainConfig& cfg,
+                             Worker& worker, OptimizerState& opt, int64_t epoch_index) {
+  return run_epoch_impl(model, graph, windows, cfg, worker, opt, epoch_index, false);
+}
+
 TrainSession::TrainSession(const DeviceGraph& graph, const ModelConfig& mcfg,
                            const TrainConfig& tcfg, cudaStream_t stream, Timestep window_total)
     : graph_(graph), tcfg_(tcfg) {
@@ -194,7 +219,10 @@ TrainSession::TrainSession(const DeviceGraph& graph, const ModelConfig& mcfg,
 }
 
 EpochReport TrainSession::run_epoch() {
-  EpochReport r = seq_first_epoch(*model_, graph_, windows_, tcfg_, *worker_, opt_, epoch_index_);
+  EpochReport r =
+      tcfg_.iteration == IterationOrder::kSeqFirst
+          ? seq_first_epoch(*model_, graph_, windows_, tcfg_, *worker_, opt_, epoch_index_)
+          : node_first_epoch(*model_, graph_, windows_, tcfg_, *worker_, opt_, epoch_index_);
   ++epoch_index_;
   return r;
 }

@@ -92,6 +92,10 @@ class Worker {
 EpochReport seq_first_epoch(DgnnModel& model, const DeviceGraph& graph,
                             const std::vector<SequenceWindow>& windows, const TrainConfig& cfg,
                             Worker& worker, OptimizerState& opt, int64_t epoch_index);
+// node-first order (ref src/train.cpp:216-220): window outer, batch inner.
+EpochReport node_first_epoch(DgnnModel& model, const DeviceGraph& graph,
+                             const std::vector<SequenceWindow>& windows, const TrainConfig& cfg,
+                             Worker& worker, OptimizerState& opt, int64_t epoch_index);
 
 class TrainSession {
  public:

@@ -127,6 +127,10 @@ struct RowGemmArgs {
   // x-part n block, i.e. N = 3H instead of 4H after a full-N first chunk
   // that initialises every accumulator column.
   int gru_split;
+  // GRU block sparsity of the store2 contraction G . W^T (0 = off, else H):
+  // K chunks of the n block feed only the x columns [0, s2_nx), chunks of
+  // the hn block only the h columns [s2_h0, s2_h0 + H); r / z chunks all.
+  int s2_gru, s2_nx, s2_h0;
   // profiling switches (env DGNN_UMMA_DEBUG): 1 skip epilogue math/stores,
   // 2 skip the B copy, 4 skip the A split/stores
   int debug;
@@ -320,6 +324,7 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
           // GRU split: chunk 0 full N; X chunks N = 3H at column 0 ([n r z]);
           // Hm chunks N = 3H at column H ([r z hn])
           uint32_t id = idesc, dd = d, bo = 0;
+          bool skip = false;
           if (gs && c > 0) {
             id = idesc3;
             if (c * kKC >= p.k1) {
@@ -327,8 +332,20 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
               bo = boffH;
             }
           }
+          if (EPI == kEpiStore2 && p.s2_gru && c * kKC >= 2 * p.s2_gru) {
+            if (c * kKC >= 3 * p.s2_gru) {  // hn block -> h columns
+              id = idesc_tf32(kTileM, p.s2_gru);
+              dd = d + static_cast<uint32_t>(p.s2_h0);
+              bo = static_cast<uint32_t>(p.s2_h0 / 8) * 128u;
+            } else if (p.s2_nx > 0) {  // n block -> x columns
+              id = idesc_tf32(kTileM, p.s2_nx);
+            } else {
+              skip = true;
+            }
+          }
 #pragma unroll
           for (int ks = 0; ks < kKC / 8; ++ks) {
+            if (skip) break;
             const uint64_t ahi = make_desc(st + 2 * ks * lboA, lboA, 128);
             const uint64_t alo = make_desc(st + S::kA + 2 * ks * lboA, lboA, 128);
             const uint64_t bhi = make_desc(st + 2 * S::kA + 2 * ks * lboB + bo, lboB, 128);
@@ -910,7 +927,7 @@ void umma_cell_backward_recompute(bool lstm, int n, int in, int H, const float* 
 }
 
 void umma_gemm_store2(int n, int K, const float* A, const float* Bimg, int n1, int n2, float* C1,
-                      float* C2, cudaStream_t stream, const float* bias, bool accumulate) {
+                      float* C2, cudaStream_t stream, const float* bias, bool accumulate, int gru_h) {
   if ((bias || accumulate) && !(n1 % 16 == 0 && n2 % 16 == 0 && n1 <= 256))
     throw std::invalid_argument("umma_gemm_store2: bias / accumulate need 16-column blocks");
   RowGemmArgs a{};
@@ -928,6 +945,13 @@ void umma_gemm_store2(int n, int K, const float* A, const float* Bimg, int n1, i
   a.n2 = n2;
   a.C1 = C1;
   a.C2 = C2;
+  // GRU: K = 4H gate columns [r z n hn]; C1 | C2 = [dX | dHm] (n1 = in,
+  // n2 = H) or dHm alone (n1 = H, n2 = 0)
+  if (gru_h > 0 && K == 4 * gru_h && umma_gru_split(false, kKC, gru_h) && n1 % 16 == 0) {
+    a.s2_gru = gru_h;
+    a.s2_nx = n2 > 0 ? n1 : 0;
+    a.s2_h0 = n2 > 0 ? n1 : 0;
+  }
   a.debug = umma_debug_flags();
   dispatch_row_gemm<kEpiStore2>(umma_npad(n1 + n2), a, stream);
 }

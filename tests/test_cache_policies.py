@@ -1,0 +1,61 @@
+"""Cache-policy baselines and iteration orders: REINC, LRU and
+LFU (src/cache.cpp:104-114) under seq-first and node-first epochs
+(src/train.cpp:209-220), several node batches and a capacity small enough to
+evict — same losses, aggregation invocation log, cache event trace and
+statistics as the compiled reference."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GRAPH = dict(n=300, avg_degree=4, dim=8, T=12, edge=0.05, feat=0.02)
+
+
+@pytest.fixture(scope="module")
+def pair(ref):
+    import torch
+    assert torch.cuda.is_available()
+    from paper_2501_15348_b200 import api
+    g = GRAPH
+    args = (g["n"], g["avg_degree"], g["dim"], g["T"], g["edge"], g["feat"])
+    return api, ref.RefGraph.synth(*args, seed=5), api.Synth(*args, seed=5).to_graph()
+
+
+def nrel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def _events_match(ev, ev_ref):
+    ev_ref = ev_ref[:, 1:]
+    assert ev.shape == ev_ref.shape
+    i = 0
+    while i < len(ev):
+        if ev[i, 0] == 4:  # invalidation burst: hash-map order in the reference
+            j = i
+            while j < len(ev) and ev[j, 0] == 4:
+                j += 1
+            assert sorted(map(tuple, ev[i:j].tolist())) == sorted(map(tuple, ev_ref[i:j].tolist()))
+            i = j
+        else:
+            assert np.array_equal(ev[i], ev_ref[i]), (i, ev[i], ev_ref[i])
+            i += 1
+
+
+@pytest.mark.parametrize("cache", ["reinc", "lru", "lfu"])
+@pytest.mark.parametrize("iteration", ["seq_first", "node_first"])
+def test_policy_and_order_match_reference(pair, ref, cache, iteration):
+    api, gr, g = pair
+    kw = dict(arch="gcrn_m2", hidden=16, seq_len=3, batch_size=120, cache=cache, cache_frac=0.3,
+              iteration=iteration)
+    r = gr.run(ref.RunCfg(epochs=2, **kw))
+    s = api.TrainSession(g, api.TrainConfig(record_events=True, **kw))
+    losses = np.concatenate([s.run_epoch()["sample_losses"] for _ in range(2)])
+    assert losses.shape == r.losses.shape
+    assert nrel(losses, r.losses) < 1e-4
+    assert np.array_equal(s.invocations(), r.invocations[:, 1:])
+    _events_match(s.cache_events(), r.events)
+    st = s.stats()
+    keys = ["hits", "misses", "evictions", "expirations", "invalidations", "rejected",
+            "scratch_calls", "incremental_calls", "fallbacks"]
+    assert [st[k] for k in keys] == r.stats[0, :9].tolist()
