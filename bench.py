@@ -277,8 +277,14 @@ def main():
         per_ms = v["ms"] / v["launches"]
         achieved = (v["bytes"] / v["launches"]) / (per_ms / 1e3) / 1e9
         peak = peaks["hbm_gbs"]
+        traffic = ncu_traffic(name)
+        dram = {} if traffic is None else {
+            # measured DRAM bytes (ncu) over the live launch time: the HBM
+            # utilisation behind the algorithmic figure
+            "dram_achieved": round(traffic / (per_ms / 1e3) / 1e9, 1),
+            "dram_frac": round(traffic / (per_ms / 1e3) / 1e9 / peak, 4)}
         return {"kernel": name, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": ncu_traffic(name),
+                "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic, **dram,
                 "note": "achieved = algorithmic bytes (SURVEY 8d: every edge gather counted, no reuse) "
                         "/ device time; peak = measured copy (read+write) bandwidth — a gather-dominated "
                         "read stream can exceed it; traffic = ncu DRAM read+write bytes per launch",

@@ -285,6 +285,17 @@ int64_t dgnn_sliding_windows(int32_t total, int32_t L, int32_t S, int32_t H, int
 /* plan, consecutive_block (src/distsim.cpp:35-81): out[4m..4m+3] =
  * block_begin, block_end, window_begin, window_end. */
 int dgnn_plan(int32_t total, int32_t workers, int32_t L, int32_t S, int32_t H, int64_t* out);
+/* Communication ledger of one distributed epoch (CommLedger, inc/distsim.hpp:58-80;
+ * accounting of src/distsim.cpp:101-182 and the per-step ring all-reduce,
+ * :262-268), placements compared the way the paper's Table 1 does: scheme 0
+ * consecutive_block, 1 node_partition, 2 sequence_partition; overlap 0
+ * replicate_overlap, 1 remote_fetch. Windows = sliding_windows(T, L, S, H) as in
+ * the reference's distributed epoch. out: (workers + 1) x 4 uint64 rows
+ * [remote_features, intermediate_redistribution, gradient_sync, snapshot_fetch],
+ * per worker then the total; bytes at the reference's 8 B per value. */
+int dgnn_comm_ledger(const dgnn_graph* g, int32_t scheme, int32_t overlap, int32_t workers,
+                     int32_t seq_len, int32_t stride, int32_t horizon, int32_t hidden,
+                     int64_t num_params, int64_t num_batches, uint64_t* out);
 /* future_access_count / imminence (src/cache.cpp:27-62); ctx = num_layers,
  * gates, gate, L, S, idx, part, layer, teacher_forcing, H, windows_remaining, kind. */
 int dgnn_cache_scores(const int32_t* ctx, int32_t* f, int32_t* imm);

@@ -790,4 +790,30 @@ uint64_t ref_key_hash(int32_t level, int32_t layer, int32_t t, int32_t kind, int
   return static_cast<uint64_t>(AggKeyHash{}(k));
 }
 
+// run_distributed_epoch under plan(scheme, overlap) (src/distsim.cpp:35-81,
+// 186-344), unmodified; returns its CommLedger as (M+1) x 4 rows.
+int ref_comm_ledger(void* g, const RefRunCfg* cfg, int32_t scheme, int32_t overlap,
+                    uint64_t* out, int64_t* num_params, int64_t* num_batches) {
+  return guarded([&] {
+    const DynamicGraph& G = *static_cast<DynamicGraph*>(g);
+    ModelConfig m = model_cfg(*cfg, G.feature_dim());
+    TrainConfig t = train_cfg(*cfg);
+    WorkerPlan p = plan(static_cast<PlacementScheme>(scheme), G.length(), cfg->workers, m.seq_len,
+                        t.stride, m.horizon, static_cast<OverlapMode>(overlap));
+    DgnnModel model = DgnnModel::create(m);
+    OptimizerState opt;
+    DistributedResult r = run_distributed_epoch(model, G, p, m, t, opt, 0);
+    auto put = [&](int row, const CommVolume& v) {
+      out[4 * row + 0] = v.remote_features;
+      out[4 * row + 1] = v.intermediate_redistribution;
+      out[4 * row + 2] = v.gradient_sync;
+      out[4 * row + 3] = v.snapshot_fetch;
+    };
+    for (int i = 0; i < cfg->workers; ++i) put(i, r.ledger.per_worker[i]);
+    put(cfg->workers, r.ledger.total);
+    *num_params = static_cast<int64_t>(model.flatten_params().size());
+    *num_batches = static_cast<int64_t>(make_batches(G.num_nodes(), t.batch_size, t.seed, 0).size());
+  });
+}
+
 }  // extern "C"

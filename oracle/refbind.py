@@ -115,6 +115,7 @@ def lib():
         "ref_graph_free": (None, [P]),
         "ref_save_dataset": (C.c_int, [P, C.c_char_p]),
         "ref_khop": (P, [P, I32, P, I64, P, I32, U64]),
+        "ref_comm_ledger": (C.c_int, [P, C.POINTER(RefRunCfg), I32, I32, P, P, P]),
         "ref_cg_free": (None, [P]),
         "ref_cg_num_hops": (I32, [P]),
         "ref_cg_hop_sizes": (None, [P, I32, P, P]),
@@ -201,6 +202,14 @@ class RefGraph:
         dst = np.ascontiguousarray(cat[:, 1])
         feats = np.ascontiguousarray(np.stack(feats_per_t).astype(np.float64))
         return cls(lib().ref_graph_from_arrays(n, dim, T, _p(counts), _p(src), _p(dst), _p(feats)))
+
+    def comm_ledger(self, cfg: "RunCfg", scheme: int, overlap: int):
+        """run_distributed_epoch's CommLedger -> ((M+1) x 4, num_params, num_batches)."""
+        c = cfg.to_c(self.T)
+        out = np.zeros((cfg.workers + 1, 4), np.uint64)
+        npar, nb = np.zeros(1, np.int64), np.zeros(1, np.int64)
+        _check(lib().ref_comm_ledger(self.h, C.byref(c), scheme, overlap, _p(out), _p(npar), _p(nb)))
+        return out, int(npar[0]), int(nb[0])
 
     @classmethod
     def load_dataset(cls, path):

@@ -71,6 +71,7 @@ SIGNATURES = {
     "dgnn_dataset_save_graph": (C.c_int, [P, C.c_char_p, I32]),
     "dgnn_synth_save": (C.c_int, [P, C.c_char_p, I32]),
     "dgnn_khop": (C.c_int, [P, I32, P, I64, P, I32, U64, PP]),
+    "dgnn_comm_ledger": (C.c_int, [P, I32, I32, I32, I32, I32, I32, I32, I64, I64, P]),
     "dgnn_cg_free": (None, [P]),
     "dgnn_cg_num_hops": (I32, [P]),
     "dgnn_cg_hop_sizes": (C.c_int, [P, I32, C.POINTER(I64), C.POINTER(I64)]),

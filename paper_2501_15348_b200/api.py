@@ -217,6 +217,22 @@ def save_dataset(graph: "DynamicGraph", path, binary=False):
     check(lib().dgnn_dataset_save_graph(graph.h, os.fsencode(path), 2 if binary else 1))
 
 
+# ------------------------------------------------------------------ ledgers
+LEDGER_FIELDS = ("remote_features", "intermediate_redistribution", "gradient_sync", "snapshot_fetch")
+
+
+def comm_ledger(graph: "DynamicGraph", scheme="consecutive_block", overlap="replicate_overlap",
+                workers=1, seq_len=8, stride=1, horizon=1, hidden=16, num_params=0, num_batches=1):
+    """CommLedger of one distributed epoch (ref inc/distsim.hpp:58-80,
+    src/distsim.cpp:101-182): per-worker rows then the total, in bytes."""
+    sch = {"consecutive_block": 0, "node_partition": 1, "sequence_partition": 2}[scheme]
+    ov = {"replicate_overlap": 0, "remote_fetch": 1}[overlap]
+    out = np.zeros((workers + 1, 4), np.uint64)
+    check(lib().dgnn_comm_ledger(graph.h, sch, ov, workers, seq_len, stride, horizon, hidden,
+                                 num_params, num_batches, _np_ptr(out)))
+    return out
+
+
 # ------------------------------------------------------------------ k-hop
 class ComputationalGraph:
     """Sampled k-hop computational graph on the device (ref

@@ -384,6 +384,26 @@ int dgnn_synth_to_graph(const dgnn_synth* s, void* stream, dgnn_graph** out) {
   });
 }
 
+int dgnn_comm_ledger(const dgnn_graph* g, int32_t scheme, int32_t overlap, int32_t workers,
+                     int32_t seq_len, int32_t stride, int32_t horizon, int32_t hidden,
+                     int64_t num_params, int64_t num_batches, uint64_t* out) {
+  return guarded([&] {
+    check(scheme >= 0 && scheme <= 2, "unknown placement scheme");
+    check(overlap == 0 || overlap == 1, "unknown overlap mode");
+    CommLedger L = comm_ledger(*g->g, static_cast<PlacementScheme>(scheme),
+                               static_cast<OverlapMode>(overlap), workers, seq_len, stride, horizon,
+                               hidden, num_params, num_batches, g->stream);
+    auto put = [&](int row, const CommVolume& v) {
+      out[4 * row + 0] = v.remote_features;
+      out[4 * row + 1] = v.intermediate_redistribution;
+      out[4 * row + 2] = v.gradient_sync;
+      out[4 * row + 3] = v.snapshot_fetch;
+    };
+    for (int m = 0; m < workers; ++m) put(m, L.per_worker[m]);
+    put(workers, L.total);
+  });
+}
+
 // ---------------------------------------------------------------- dataset
 struct dgnn_dataset {
   std::unique_ptr<DatasetReader> r;

@@ -877,4 +877,43 @@ DevCompGraph apply_cg_update(const DevCompGraph& prev, const DevCgUpdate& update
   return out;
 }
 
+// ---------------------------------------------------------------- ledgers
+namespace {
+
+__global__ void k_mark_remote_sources(int32_t nb, int32_t ne, const int64_t* __restrict__ in_ptr,
+                                      const int32_t* __restrict__ in_src, uint8_t* __restrict__ flag) {
+  const int64_t b = in_ptr[nb], e = in_ptr[ne];
+  for (int64_t i = b + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < e;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t u = in_src[i];
+    if (u < nb || u >= ne) flag[u] = 1;
+  }
+}
+
+__global__ void k_count_flags(int32_t n, const uint8_t* __restrict__ flag, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    c += flag[i];
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+}  // namespace
+
+uint64_t remote_source_count(const DevSnapshot& snap, int32_t num_nodes, int32_t nb, int32_t ne,
+                             cudaStream_t st) {
+  DevArray<uint8_t> flag(num_nodes, st);
+  DevArray<unsigned long long> cnt(1, st);
+  DGNN_CUDA(cudaMemsetAsync(flag.get(), 0, num_nodes, st));
+  cnt.zero(st);
+  // the in-CSR rows of [nb, ne) are one contiguous edge range
+  DGNN_LAUNCH(k_mark_remote_sources, cuda::wave_grid(snap.num_edges + 1, kT, 4), kT, 0, st, nb, ne,
+              snap.in_ptr.get(), snap.in_src.get(), flag.get());
+  DGNN_LAUNCH(k_count_flags, grid_for(num_nodes), kT, 0, st, num_nodes, flag.get(), cnt.get());
+  unsigned long long h = 0;
+  copy_to_host(&h, cnt.get(), sizeof(h), st);
+  return h;
+}
+
 }  // namespace dgnn

@@ -149,6 +149,11 @@ void copy_to_host(void* dst, const void* src, size_t bytes, cudaStream_t stream)
 DevSnapshot csr_from_keys(const uint64_t* keys, int64_t num_edges, int32_t num_nodes,
                           cudaStream_t stream);
 
+// Distinct sources outside [nb, ne) with an in-edge into [nb, ne) in one
+// snapshot (the node-partition remote-feature count, src/distsim.cpp:121-139).
+uint64_t remote_source_count(const DevSnapshot& snap, int32_t num_nodes, int32_t nb, int32_t ne,
+                             cudaStream_t stream);
+
 // ---------------------------------------------------------------- k-hop
 // Sampled k-hop computational graphs (ref inc/khop.hpp:35-88, src/khop.cpp),
 // built on the device from a resident snapshot. Sampling is bit-exact with the

@@ -251,6 +251,74 @@ std::vector<WorkerAssignment> plan_consecutive_block(Timestep total, int num_wor
   return out;
 }
 
+CommLedger comm_ledger(const DeviceGraph& graph, PlacementScheme scheme, OverlapMode overlap,
+                       int M, Timestep seq_len, Timestep stride, Timestep horizon, int hidden_dim,
+                       int64_t num_params, int64_t num_batches, cudaStream_t stream) {
+  const Timestep T = graph.length();
+  // the reference's distributed epoch windows the full length (src/distsim.cpp:190)
+  const auto windows = sliding_windows(T, seq_len, stride, horizon);
+  check(!windows.empty(), "distributed epoch needs at least one window");
+  check(M >= 1, "plan needs at least one worker");
+  check(T >= M, "fewer snapshots than workers");
+  CommLedger L;
+  L.per_worker.resize(M);
+  auto add = [&](int m, uint64_t CommVolume::*f, uint64_t b) {
+    L.per_worker[m].*f += b;
+    L.total.*f += b;
+  };
+  // ring all-reduce per optimizer step (src/distsim.cpp:262-268)
+  const uint64_t param_bytes = static_cast<uint64_t>(num_params) * 8;
+  const auto sync = static_cast<uint64_t>(
+      std::llround(2.0 * (M - 1) / std::max(M, 1) * static_cast<double>(param_bytes)));
+  for (int64_t b = 0; b < num_batches; ++b)
+    for (int m = 0; m < M; ++m) add(m, &CommVolume::gradient_sync, sync);
+  const NodeId N = graph.num_nodes();
+  std::vector<std::pair<NodeId, NodeId>> ranges;  // node_ranges (src/distsim.cpp:108-117)
+  {
+    NodeId base = N / M, extra = N % M, cur = 0;
+    for (int m = 0; m < M; ++m) {
+      const NodeId len = base + (m < extra ? 1 : 0);
+      ranges.push_back({cur, cur + len});
+      cur += len;
+    }
+  }
+  const uint64_t d = static_cast<uint64_t>(graph.feature_dim());
+  if (scheme == PlacementScheme::kConsecutiveBlock && overlap == OverlapMode::kRemoteFetch) {
+    // account_snapshot_fetch (src/distsim.cpp:163-178)
+    const auto plan = plan_consecutive_block(T, M, seq_len, stride, horizon);
+    for (int m = 0; m < M; ++m) {
+      const WorkerAssignment& a = plan[m];
+      if (a.window_begin == a.window_end) continue;
+      const Timestep end = std::min<Timestep>(a.block_end + seq_len + horizon - 1, T);
+      for (Timestep t = a.block_end; t < end; ++t)
+        add(m, &CommVolume::snapshot_fetch,
+            static_cast<uint64_t>(graph.snapshot(t).num_edges) * 8 + static_cast<uint64_t>(N) * d * 8);
+    }
+  } else if (scheme == PlacementScheme::kNodePartition) {
+    // account_node_partition (src/distsim.cpp:121-147), counts on the device
+    std::vector<uint64_t> cover(T, 0);
+    for (const auto& w : windows)
+      for (Timestep t = w.start; t < w.start + w.length + w.horizon; ++t) ++cover[t];
+    for (Timestep t = 0; t < T; ++t) {
+      if (!cover[t]) continue;
+      for (int m = 0; m < M; ++m) {
+        const uint64_t uniq = remote_source_count(graph.snapshot(t), N, ranges[m].first, ranges[m].second, stream);
+        add(m, &CommVolume::remote_features, uniq * d * 8 * cover[t]);
+      }
+    }
+  } else if (scheme == PlacementScheme::kSequencePartition) {
+    // account_sequence_partition (src/distsim.cpp:149-161)
+    const uint64_t row = static_cast<uint64_t>(hidden_dim) * 8;
+    for (const auto& w : windows)
+      for (Timestep idx = 0; idx < w.length; ++idx) {
+        const int owner = static_cast<int>(idx % M);
+        const uint64_t resident = static_cast<uint64_t>(ranges[owner].second - ranges[owner].first);
+        add(owner, &CommVolume::intermediate_redistribution, (static_cast<uint64_t>(N) - resident) * row);
+      }
+  }
+  return L;
+}
+
 DistWorker::DistWorker(const DeviceGraph& graph, const ModelConfig& mcfg, const TrainConfig& tcfg,
                        cudaStream_t stream, int rank, int world, Timestep window_total)
     : graph_(graph), tcfg_(tcfg) {

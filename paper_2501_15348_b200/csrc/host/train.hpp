@@ -128,6 +128,24 @@ std::vector<WorkerAssignment> plan_consecutive_block(Timestep total, int num_wor
                                                      Timestep seq_len, Timestep stride,
                                                      Timestep horizon);
 
+// Communication ledger of one distributed epoch (ref CommVolume / CommLedger,
+// inc/distsim.hpp:58-80; accounting src/distsim.cpp:101-182 and the per-step
+// ring all-reduce volume, :262-268). Byte counts follow the reference's fp64
+// storage (8 B per value), so they compare placements the way Table 1 does.
+enum class PlacementScheme { kConsecutiveBlock, kNodePartition, kSequencePartition };
+enum class OverlapMode { kReplicateOverlap, kRemoteFetch };
+struct CommVolume {
+  uint64_t remote_features = 0, intermediate_redistribution = 0, gradient_sync = 0,
+           snapshot_fetch = 0;
+};
+struct CommLedger {
+  CommVolume total;
+  std::vector<CommVolume> per_worker;
+};
+CommLedger comm_ledger(const DeviceGraph& graph, PlacementScheme scheme, OverlapMode overlap,
+                       int num_workers, Timestep seq_len, Timestep stride, Timestep horizon,
+                       int hidden_dim, int64_t num_params, int64_t num_batches, cudaStream_t stream);
+
 // One rank of the snapshot-window-sharded trainer (distsim semantics, ref
 // src/distsim.cpp:197-272): per batch every rank sums the gradients of its
 // own window block in window order; the caller all-reduces the flat buffer

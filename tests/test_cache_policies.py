@@ -46,8 +46,10 @@ def _events_match(ev, ev_ref):
 @pytest.mark.parametrize("iteration", ["seq_first", "node_first"])
 def test_policy_and_order_match_reference(pair, ref, cache, iteration):
     api, gr, g = pair
+    # SGD: 48 optimizer steps of Adam turn fp32-vs-fp64 noise into ~1e-3 loss
+    # drift (DESIGN §3 tolerances); the cache decisions are the point here
     kw = dict(arch="gcrn_m2", hidden=16, seq_len=3, batch_size=120, cache=cache, cache_frac=0.3,
-              iteration=iteration)
+              iteration=iteration, optimizer="sgd")
     r = gr.run(ref.RunCfg(epochs=2, **kw))
     s = api.TrainSession(g, api.TrainConfig(record_events=True, **kw))
     losses = np.concatenate([s.run_epoch()["sample_losses"] for _ in range(2)])
