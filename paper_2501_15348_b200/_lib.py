@@ -10,7 +10,8 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_dgnn_b200.so")
+# DGNN_LIB_PATH: an alternative build of the same library (kernel A/B experiments)
+LIB_PATH = os.environ.get("DGNN_LIB_PATH") or os.path.join(_HERE, "_dgnn_b200.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "dgnn_b200.h")
 
 P, I32, I64, U64, D, F = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_double, C.c_float

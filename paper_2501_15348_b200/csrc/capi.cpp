@@ -646,6 +646,8 @@ int dgnn_cg_view(dgnn_cg* c, const int64_t** in_ptr, const int32_t** in_src,
     if (!c->view) {
       const DevHop& h = c->cg.hops.back();
       c->view = std::make_unique<DevSnapshot>(csr_from_keys(h.edges.get(), h.n_edges, c->num_nodes, c->stream));
+      // callers read the view on other streams
+      DGNN_CUDA(cudaStreamSynchronize(c->stream));
     }
     if (in_ptr) *in_ptr = c->view->in_ptr.get();
     if (in_src) *in_src = c->view->in_src.get();

@@ -144,7 +144,12 @@ int umma_debug_flags() {
   return f;
 }
 
-constexpr int kRgThreads = 416;  // 13 warps: 4 producers, 1 MMA, 8 epilogue
+#ifndef DGNN_RG_PRODUCER_WARPS
+#define DGNN_RG_PRODUCER_WARPS 4
+#endif
+// warps: producers, 1 MMA, 8 epilogue
+constexpr int kProducerWarps = DGNN_RG_PRODUCER_WARPS;
+constexpr int kRgThreads = 32 * (kProducerWarps + 1 + 8);
 // MMA operand stages (A hi/lo + B hi/lo): the producer -> tcgen05 -> commit
 // round trip is latency-bound (ncu: producers wait on `empty`, the MMA thread
 // on `full`, the tensor pipe < 20% busy), so small-N contractions get more
@@ -156,9 +161,11 @@ constexpr int kRgStagesFor = NPAD <= 64 ? 6 : (NPAD <= 128 ? 5 : (NPAD <= 192 ? 
 // per chunk; small-N contractions have little MMA work to hide it behind)
 template <int NPAD>
 constexpr int kRawSlotsFor = NPAD <= 64 ? 7 : (NPAD <= 192 ? 5 : 6);
-constexpr int kProducerThreads = 128;
-constexpr int kMmaWarp = 4;
-constexpr int kEpiWarp0 = 5;  // warps 5..12: lane quadrant = warp % 4 covers 0..3 twice
+constexpr int kProducerThreads = 32 * kProducerWarps;
+constexpr int kProducerRows = kProducerThreads / 4;  // rows per producer pass (4 K quads per row)
+constexpr int kMmaWarp = kProducerWarps;
+// 8 epilogue warps: lane quadrant = warp % 4 covers 0..3 twice
+constexpr int kEpiWarp0 = kProducerWarps + 1;
 constexpr int kEpiWarps = 8;
 constexpr int kRawPerThread = (kTileM * kKC / 4) / kProducerThreads;  // float4 per thread per chunk
 
@@ -219,7 +226,7 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
   const uint32_t sbase = smem_u32(smem);
   const int ntiles = (p.M + kTileM - 1) / kTileM;
 
-  if (warp < 4) {
+  if (warp < kProducerWarps) {
     // ---------------- producers
     // Flat sequence of (tile, chunk) items; raw fp32 A chunks are prefetched
     // kRawSlots - 1 items ahead with cp.async (each thread later re-reads only
@@ -243,7 +250,7 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
         const uint32_t slot = raw0 + is_slot * S::kRaw + tid * 16;
 #pragma unroll
         for (int it = 0; it < kRawPerThread; ++it) {
-          const int64_t grow = r0 + 32 * it;
+          const int64_t grow = r0 + kProducerRows * it;
           const bool valid = kin && grow < p.M;
           cp_async16_zfill(slot + it * kProducerThreads * 16, valid ? base + grow * ld : p.A1, valid);
         }
@@ -278,7 +285,7 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
           split_tf32(v[it].y, h1, l1);
           split_tf32(v[it].z, h2, l2);
           split_tf32(v[it].w, h3, l3);
-          const uint32_t off = tile_offset(kTileM, prow + 32 * it, kq * 4);
+          const uint32_t off = tile_offset(kTileM, prow + kProducerRows * it, kq * 4);
           st_shared_v4(st + off, h0, h1, h2, h3);
           st_shared_v4(st + S::kA + off, l0, l1, l2, l3);
         }

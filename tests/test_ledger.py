@@ -37,4 +37,5 @@ def test_ledger_matches_reference(pair, ref, scheme, overlap, workers, batch):
     got = api.comm_ledger(g, SCHEMES[scheme], OVERLAPS[overlap], workers=workers, seq_len=3,
                           stride=3, horizon=1, hidden=16, num_params=npar, num_batches=nb)
     assert np.array_equal(got, want), (got, want)
-    assert got[-1].sum() > 0
+    if workers > 1:  # one worker communicates nothing
+        assert got[-1].sum() > 0
