@@ -378,8 +378,9 @@ int dgnn_synth_to_graph(const dgnn_synth* s, void* stream, dgnn_graph** out) {
                       static_cast<int64_t>(st.changed.size()), ps.changed_feats);
     }
     DGNN_CUDA(cudaStreamSynchronize(g->stream));
-    // build temporaries (sort buffers, CUB scratch) go back to the pool
-    cuda::release_stream_blocks(g->stream);
+    // build temporaries (sort buffers, CUB scratch, the last snapshot's key
+    // arrays) go back to the pool
+    g->g->release_build_state();
     *out = guard.release();
   });
 }
@@ -519,7 +520,7 @@ int dgnn_dataset_load(const char* dir, int32_t threads, void* stream, dgnn_graph
       if (next.joinable()) next.join();
     }
     DGNN_CUDA(cudaStreamSynchronize(g->stream));
-    cuda::release_stream_blocks(g->stream);
+    g->g->release_build_state();
     *out = guard.release();
   });
 }

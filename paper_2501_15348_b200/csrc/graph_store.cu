@@ -3,6 +3,7 @@
 // (src/snapshot.cpp:20-154). Sorting/selection/scans use CUB (CUDA toolkit
 // library primitives); the graph-specific passes are the kernels below.
 #include <cub/cub.cuh>
+#include <cub/device/device_merge.cuh>
 
 #include <algorithm>
 #include <cstdlib>
@@ -51,6 +52,23 @@ __global__ void k_mark(int64_t na, const uint64_t* __restrict__ a, int64_t nb,
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < na;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
     keep[i] = bsearch_u64(b, nb, a[i]) == (want_found != 0);
+}
+
+// keep[pos] = 0 for every key of `d` present in the sorted array `a`
+// (binary search per key of the small array, not per key of the big one)
+__global__ void k_unmark_present(int64_t nd, const uint64_t* __restrict__ d, int64_t na,
+                                 const uint64_t* __restrict__ a, int swap, uint8_t* __restrict__ keep) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nd;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t k = swap ? (d[i] << 32) | (d[i] >> 32) : d[i];
+    int64_t lo = 0, hi = na;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (a[mid] < k) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo < na && a[lo] == k) keep[lo] = 0;
+  }
 }
 
 __global__ void k_hist_hi(int64_t n, const uint64_t* __restrict__ keys,
@@ -220,6 +238,18 @@ struct Cub {
     size_t b = 0;
     DGNN_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b, in, out, n, st));
     DGNN_CUDA(cub::DeviceScan::ExclusiveSum(get(b), b, in, out, n, st));
+  }
+  void merge(const uint64_t* a, int64_t na, const uint64_t* b, int64_t nb, uint64_t* out) {
+    if (na + nb == 0) return;
+    if (na == 0 || nb == 0) {
+      DGNN_CUDA(cudaMemcpyAsync(out, na ? a : b, sizeof(uint64_t) * (na + nb), cudaMemcpyDeviceToDevice, st));
+      return;
+    }
+    size_t bytes = 0;
+    DGNN_CUDA(cub::DeviceMerge::MergeKeys(nullptr, bytes, a, static_cast<int>(na), b,
+                                          static_cast<int>(nb), out, ::cuda::std::less<>{}, st));
+    DGNN_CUDA(cub::DeviceMerge::MergeKeys(get(bytes), bytes, a, static_cast<int>(na), b,
+                                          static_cast<int>(nb), out, ::cuda::std::less<>{}, st));
   }
   int64_t rle(const int32_t* in, int32_t* uniq, int32_t* counts, int64_t n) {
     if (n == 0) return 0;
@@ -403,6 +433,7 @@ int64_t DeviceGraph::device_bytes() const {
 void DeviceGraph::add_snapshot(const int32_t* src, const int32_t* dst, int64_t num_edges,
                                const float* feats) {
   cuda::release_stream_blocks(stream_);
+  ensure_build_keys();  // previous snapshot's keys for extract_delta
   Cub cub(stream_);
   DevArray<uint64_t> keys = sorted_edge_keys(src, dst, num_edges, n_, cub, true);
   const int64_t nf = static_cast<int64_t>(n_) * d_;
@@ -439,29 +470,75 @@ void DeviceGraph::add_delta(const int32_t* del_src, const int32_t* del_dst, int6
   // the previous build step's temporaries (sizes drift per snapshot) go back
   // to the pool instead of accumulating in the per-size free lists
   cuda::release_stream_blocks(st);
+  ensure_build_keys();
   Cub cub(st);
   DevArray<uint64_t> del = sorted_edge_keys(del_src, del_dst, n_del, n_, cub, false);
   DevArray<uint64_t> ins = sorted_edge_keys(ins_src, ins_dst, n_ins, n_, cub, true);
   const int64_t E0 = static_cast<int64_t>(curr_keys_.size());
-  // prev \ deletions
+  // Incremental snapshot build: the work scales with |D| + |I| plus two
+  // linear select / merge passes, not with sorts or searches over E.
+  // kept = prev \ D: one binary search per deletion into prev
   DevArray<uint8_t> keep(E0, st);
-  DevArray<uint64_t> cat(E0 + n_ins, st);
-  int64_t kept = E0;
+  DevArray<uint64_t> kept(E0, st);
+  int64_t nk = E0;
   if (E0 > 0) {
-    DGNN_LAUNCH(k_mark, grid_for(E0), kT, 0, st, E0, curr_keys_.get(), n_del, del.get(), 0, keep.get());
-    kept = cub.select_flagged(curr_keys_.get(), keep.get(), cat.get(), E0);
+    DGNN_CUDA(cudaMemsetAsync(keep.get(), 1, E0, st));
+    if (n_del) DGNN_LAUNCH(k_unmark_present, grid_for(n_del), kT, 0, st, n_del, del.get(), E0, curr_keys_.get(), 0, keep.get());
+    nk = cub.select_flagged(curr_keys_.get(), keep.get(), kept.get(), E0);
   }
-  // U insertions (set_union: common elements once)
-  if (n_ins > 0)
-    DGNN_CUDA(cudaMemcpyAsync(cat.get() + kept, ins.get(), sizeof(uint64_t) * n_ins,
-                              cudaMemcpyDeviceToDevice, st));
-  const int64_t m = kept + n_ins;
-  DevArray<uint64_t> sorted(m, st), keys(m, st);
-  cub.sort(cat.get(), sorted.get(), m);
-  const int64_t E1 = cub.unique(sorted.get(), keys.get(), m);
+  // I' = I \ kept, so that merge(kept, I') is the set union (src/snapshot.cpp:145-148)
+  DevArray<uint64_t> ins_new(n_ins, st);
+  int64_t ni = 0;
+  if (n_ins) {
+    DevArray<uint8_t> f(n_ins, st);
+    DGNN_LAUNCH(k_mark, grid_for(n_ins), kT, 0, st, n_ins, ins.get(), nk, kept.get(), 0, f.get());
+    ni = cub.select_flagged(ins.get(), f.get(), ins_new.get(), n_ins);
+  }
+  const int64_t E1 = nk + ni;
   DevArray<uint64_t> exact(E1, st);
-  if (E1 > 0)
-    DGNN_CUDA(cudaMemcpyAsync(exact.get(), keys.get(), sizeof(uint64_t) * E1, cudaMemcpyDeviceToDevice, st));
+  cub.merge(kept.get(), nk, ins_new.get(), ni, exact.get());
+  kept.reset();
+  // (dst, src) order: prev's swapped keys minus D, merged with sorted swap(I')
+  DevArray<uint64_t> sw_new(E1, st);
+  {
+    DevArray<uint64_t> sw_kept(E0, st);
+    int64_t nsk = E0;
+    if (E0 > 0) {
+      DGNN_CUDA(cudaMemsetAsync(keep.get(), 1, E0, st));
+      if (n_del) DGNN_LAUNCH(k_unmark_present, grid_for(n_del), kT, 0, st, n_del, del.get(), E0, curr_swapped_.get(), 1, keep.get());
+      nsk = cub.select_flagged(curr_swapped_.get(), keep.get(), sw_kept.get(), E0);
+    }
+    DevArray<uint64_t> swi(ni, st), swi_sorted(ni, st);
+    if (ni) {
+      DGNN_LAUNCH(k_swap_halves, grid_for(ni), kT, 0, st, ni, ins_new.get(), swi.get());
+      cub.sort(swi.get(), swi_sorted.get(), ni);
+    }
+    if (nsk + ni != E1) throw std::runtime_error("graph store: inconsistent incremental build");
+    cub.merge(sw_kept.get(), nsk, swi_sorted.get(), ni, sw_new.get());
+  }
+  keep.reset();
+  // exact structural change for extract_delta: removed = (prev ∩ D) \ I, added = I \ prev
+  StructDiff diff;
+  {
+    diff.removed = DevArray<uint64_t>(n_del, st);
+    if (n_del) {
+      DevArray<uint8_t> in_prev(n_del, st), not_ins(n_del, st);
+      DevArray<uint64_t> tmp(n_del, st), tmp2(n_del, st);
+      DGNN_LAUNCH(k_mark, grid_for(n_del), kT, 0, st, n_del, del.get(), E0, curr_keys_.get(), 1, in_prev.get());
+      const int64_t np = cub.select_flagged(del.get(), in_prev.get(), tmp.get(), n_del);
+      if (np) {
+        DGNN_LAUNCH(k_mark, grid_for(np), kT, 0, st, np, tmp.get(), n_ins, ins.get(), 0, not_ins.get());
+        const int64_t nr = cub.select_flagged(tmp.get(), not_ins.get(), tmp2.get(), np);
+        diff.n_removed = cub.unique(tmp2.get(), diff.removed.get(), nr);  // D may repeat keys
+      }
+    }
+    diff.added = DevArray<uint64_t>(n_ins, st);
+    if (n_ins) {
+      DevArray<uint8_t> f(n_ins, st);
+      DGNN_LAUNCH(k_mark, grid_for(n_ins), kT, 0, st, n_ins, ins.get(), E0, curr_keys_.get(), 0, f.get());
+      diff.n_added = cub.select_flagged(ins.get(), f.get(), diff.added.get(), n_ins);
+    }
+  }
   // features: prev rows with the changed rows replaced
   const int64_t nf = static_cast<int64_t>(n_) * d_;
   const int32_t t = length();
@@ -474,14 +551,51 @@ void DeviceGraph::add_delta(const int32_t* del_src, const int32_t* del_dst, int6
     DGNN_LAUNCH(k_scatter_rows, grid_for(n_changed * d_), kT, 0, st, n_changed, d_, nodes.get(),
                 rows.get(), cur->buf.get());
   }
-  finish_snapshot(std::move(exact), prev->get(), cur->buf.get());
+  finish_snapshot(std::move(exact), prev->get(), cur->buf.get(), std::move(sw_new), &diff);
   cur->t = t;
   cur->writer = st;
   cur->stamp = ++clock_;
   DGNN_CUDA(cudaEventRecord(cur->ready, st));
 }
 
-DevSnapshot csr_from_keys(const uint64_t* keys, int64_t E, int32_t n, cudaStream_t st) {
+namespace {
+// (src,dst) keys of a snapshot from its out-CSR, (dst,src) keys from its in-CSR
+__global__ void k_csr_keys(int32_t n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                           uint64_t* __restrict__ out) {
+  const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int64_t u = warp; u < n; u += nw)
+    for (int64_t e = ptr[u] + lane; e < ptr[u + 1]; e += 32)
+      out[e] = (static_cast<uint64_t>(u) << 32) | static_cast<uint32_t>(idx[e]);
+}
+}  // namespace
+
+void DeviceGraph::ensure_build_keys() {
+  if (snaps_.empty()) return;
+  const DevSnapshot& s = snaps_.back();
+  const int64_t E = s.num_edges;
+  if (static_cast<int64_t>(curr_keys_.size()) == E && static_cast<int64_t>(curr_swapped_.size()) == E) return;
+  curr_keys_ = DevArray<uint64_t>(E, stream_);
+  curr_swapped_ = DevArray<uint64_t>(E, stream_);
+  if (E > 0) {
+    DGNN_LAUNCH(k_csr_keys, cuda::wave_grid(static_cast<int64_t>(n_) * 32, kT, 8), kT, 0, stream_, n_,
+                s.out_ptr.get(), s.out_dst.get(), curr_keys_.get());
+    DGNN_LAUNCH(k_csr_keys, cuda::wave_grid(static_cast<int64_t>(n_) * 32, kT, 8), kT, 0, stream_, n_,
+                s.in_ptr.get(), s.in_src.get(), curr_swapped_.get());
+  }
+}
+
+void DeviceGraph::release_build_state() {
+  DGNN_CUDA(cudaStreamSynchronize(stream_));
+  curr_keys_.reset();
+  curr_swapped_.reset();
+  prev_keys_.reset();
+  cuda::release_stream_blocks(stream_);
+}
+
+DevSnapshot csr_from_keys(const uint64_t* keys, int64_t E, int32_t n, cudaStream_t st,
+                          const uint64_t* swapped_sorted, DevArray<uint64_t>* swapped_out) {
   Cub cub(st);
   DevSnapshot s;
   s.num_edges = E;
@@ -500,28 +614,43 @@ DevSnapshot csr_from_keys(const uint64_t* keys, int64_t E, int32_t n, cudaStream
   s.in_src = DevArray<int32_t>(E, st);
   cnt.zero(st);
   if (E > 0) {
-    DevArray<uint64_t> sw(E, st), sw_sorted(E, st);
-    DGNN_LAUNCH(k_swap_halves, grid_for(E), kT, 0, st, E, keys, sw.get());
-    cub.sort(sw.get(), sw_sorted.get(), E);
-    DGNN_LAUNCH(k_hist_hi, grid_for(E), kT, 0, st, E, sw_sorted.get(), cnt.get());
-    DGNN_LAUNCH(k_low32, grid_for(E), kT, 0, st, E, sw_sorted.get(), s.in_src.get());
+    DevArray<uint64_t> sw_sorted;
+    const uint64_t* swk = swapped_sorted;
+    if (swk == nullptr) {
+      DevArray<uint64_t> sw(E, st);
+      sw_sorted = DevArray<uint64_t>(E, st);
+      DGNN_LAUNCH(k_swap_halves, grid_for(E), kT, 0, st, E, keys, sw.get());
+      cub.sort(sw.get(), sw_sorted.get(), E);
+      swk = sw_sorted.get();
+    }
+    DGNN_LAUNCH(k_hist_hi, grid_for(E), kT, 0, st, E, swk, cnt.get());
+    DGNN_LAUNCH(k_low32, grid_for(E), kT, 0, st, E, swk, s.in_src.get());
+    if (swapped_out && swapped_sorted == nullptr) *swapped_out = std::move(sw_sorted);
   }
   cub.exclusive_sum(reinterpret_cast<const int64_t*>(cnt.get()), s.in_ptr.get(), n + 1);
   return s;
 }
 
 void DeviceGraph::finish_snapshot(DevArray<uint64_t> keys, const float* prev_feats,
-                                  const float* feats) {
+                                  const float* feats, DevArray<uint64_t> swapped,
+                                  const StructDiff* diff) {
   const int64_t E = static_cast<int64_t>(keys.size());
-  snaps_.push_back(csr_from_keys(keys.get(), E, n_, stream_));
+  if (static_cast<int64_t>(swapped.size()) == E && E > 0) {
+    snaps_.push_back(csr_from_keys(keys.get(), E, n_, stream_, swapped.get()));
+  } else {
+    swapped.reset();
+    snaps_.push_back(csr_from_keys(keys.get(), E, n_, stream_, nullptr, &swapped));
+  }
   deltas_.emplace_back();
   prev_keys_ = std::move(curr_keys_);
   curr_keys_ = std::move(keys);
-  if (snaps_.size() >= 2) build_delta(static_cast<int32_t>(snaps_.size()) - 1, prev_feats, feats);
+  curr_swapped_ = std::move(swapped);
+  if (snaps_.size() >= 2) build_delta(static_cast<int32_t>(snaps_.size()) - 1, prev_feats, feats, diff);
   prev_keys_.reset();
 }
 
-void DeviceGraph::build_delta(int32_t t, const float* prev_feats, const float* feats) {
+void DeviceGraph::build_delta(int32_t t, const float* prev_feats, const float* feats,
+                              const StructDiff* diff) {
   cudaStream_t st = stream_;
   Cub cub(st);
   const DevSnapshot& P = snaps_[t - 1];
@@ -558,14 +687,20 @@ void DeviceGraph::build_delta(int32_t t, const float* prev_feats, const float* f
     *total = cub.read(off.get() + dd.n_changed);
     return off;
   };
+  // a \ b (or, from an incremental build, the given exact difference) plus
+  // the out-edges of the changed nodes in S
   auto side = [&](const uint64_t* a, int64_t na, const uint64_t* b, int64_t nb,
-                  const DevSnapshot& S, int64_t* out_n) {
+                  const DevSnapshot& S, int64_t* out_n, const uint64_t* exact_diff, int64_t n_exact) {
     int64_t nexp = 0;
     DevArray<int64_t> off = expansion(S, &nexp);
-    DevArray<uint8_t> keep(na, st);
-    DevArray<uint64_t> cat(na + nexp, st);
+    const int64_t cap = exact_diff ? n_exact : na;
+    DevArray<uint64_t> cat(cap + nexp, st);
     int64_t nd = 0;
-    if (na > 0) {
+    if (exact_diff) {
+      nd = n_exact;
+      if (nd) DGNN_CUDA(cudaMemcpyAsync(cat.get(), exact_diff, 8 * nd, cudaMemcpyDeviceToDevice, st));
+    } else if (na > 0) {
+      DevArray<uint8_t> keep(na, st);
       DGNN_LAUNCH(k_mark, grid_for(na), kT, 0, st, na, a, nb, b, 0, keep.get());
       nd = cub.select_flagged(a, keep.get(), cat.get(), na);
     }
@@ -582,8 +717,10 @@ void DeviceGraph::build_delta(int32_t t, const float* prev_feats, const float* f
                                 cudaMemcpyDeviceToDevice, st));
     return out;
   };
-  dd.del = side(prev_keys_.get(), Ep, curr_keys_.get(), Ec, P, &dd.n_del);
-  dd.ins = side(curr_keys_.get(), Ec, prev_keys_.get(), Ep, Cs, &dd.n_ins);
+  dd.del = side(prev_keys_.get(), Ep, curr_keys_.get(), Ec, P, &dd.n_del,
+                diff ? diff->removed.get() : nullptr, diff ? diff->n_removed : 0);
+  dd.ins = side(curr_keys_.get(), Ec, prev_keys_.get(), Ep, Cs, &dd.n_ins,
+                diff ? diff->added.get() : nullptr, diff ? diff->n_added : 0);
   // distinct sources per side
   DevArray<unsigned long long> heads(2, st);
   heads.zero(st);

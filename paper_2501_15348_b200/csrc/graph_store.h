@@ -121,10 +121,21 @@ class DeviceGraph {
   int64_t feature_materialisations() const { return materialisations_; }
 
   int64_t device_bytes() const;
+  // Frees the build-time key arrays of the last snapshot (2 x 8 B per edge);
+  // a later add_delta rebuilds them from the snapshot's CSRs.
+  void release_build_state();
 
  private:
-  void finish_snapshot(cuda::DevArray<uint64_t> keys, const float* prev_feats, const float* feats);
-  void build_delta(int32_t t, const float* prev_feats, const float* feats);
+  // Structural edge change of an apply_delta step, known exactly from its
+  // inputs: removed = (prev ∩ D) \ I, added = I \ prev (sorted unique).
+  struct StructDiff {
+    cuda::DevArray<uint64_t> removed, added;
+    int64_t n_removed = 0, n_added = 0;
+  };
+  void finish_snapshot(cuda::DevArray<uint64_t> keys, const float* prev_feats, const float* feats,
+                       cuda::DevArray<uint64_t> swapped = {}, const StructDiff* diff = nullptr);
+  void build_delta(int32_t t, const float* prev_feats, const float* feats, const StructDiff* diff);
+  void ensure_build_keys();
   std::shared_ptr<FeatSlot> free_slot(cudaStream_t stream) const;
   void order_after_write(const FeatSlot& s, cudaStream_t stream) const;
 
@@ -133,6 +144,7 @@ class DeviceGraph {
   std::vector<DevSnapshot> snaps_;
   std::vector<DevDelta> deltas_;  // deltas_[t], t >= 1; deltas_[0] unused
   cuda::DevArray<uint64_t> prev_keys_, curr_keys_;  // sorted (src,dst) of the last two snapshots
+  cuda::DevArray<uint64_t> curr_swapped_;           // last snapshot's (dst,src) keys, sorted
   // feature versions (the per-t patch is the second half of delta(t).compact)
   mutable std::vector<std::shared_ptr<FeatSlot>> slots_;  // slots_[0] = snapshot 0
   mutable uint64_t clock_ = 0;
@@ -147,7 +159,8 @@ void copy_to_host(void* dst, const void* src, size_t bytes, cudaStream_t stream)
 // sorted unique (src << 32 | dst) keys (ref Snapshot ctor CSR build,
 // src/snapshot.cpp:46-69, and ComputationalGraph::to_view, src/khop.cpp:22-33).
 DevSnapshot csr_from_keys(const uint64_t* keys, int64_t num_edges, int32_t num_nodes,
-                          cudaStream_t stream);
+                          cudaStream_t stream, const uint64_t* swapped_sorted = nullptr,
+                          cuda::DevArray<uint64_t>* swapped_out = nullptr);
 
 // Distinct sources outside [nb, ne) with an in-edge into [nb, ne) in one
 // snapshot (the node-partition remote-feature count, src/distsim.cpp:121-139).
