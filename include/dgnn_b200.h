@@ -312,7 +312,8 @@ int64_t dgnn_init_params(const dgnn_run_cfg* cfg, int32_t feature_dim, double* o
 /* ---------------------------------------------------------------- profiling
  * Device timing per kernel class (0 agg_scratch, 1 agg_delta, 2 agg_backward,
  * 3 cell_fwd, 4 cell_bwd (pointwise), 5 weight_grad, 6 other, 7 cell_bwd_gemm
- * (the dX | dHm contraction), 8 sample = one whole (window, batch) sample)
+ * (the dX | dHm contraction), 8 agg_rebase (a hidden aggregation carried
+ * across a structural delta), 9 sample = one whole (window, batch) sample)
  * with algorithmic bytes; dgnn_prof_get_max = the longest single scope. */
 /* Device memory pool (stream-ordered allocations of every buffer above):
  * reserved / used bytes, current and high-water. */

@@ -711,7 +711,7 @@ class TrainSession:
 
 # ------------------------------------------------------------------ profiling
 PROF_CLASSES = ["agg_scratch", "agg_delta", "agg_backward", "cell_fwd", "cell_bwd",
-                "weight_grad", "other", "cell_bwd_gemm"]
+                "weight_grad", "other", "cell_bwd_gemm", "agg_rebase"]
 # non-kernel scopes (not part of kernel-time sums)
 PROF_SCOPES = ["sample", "sample_host", "host_build", "host_fwd", "host_bwd", "host_alloc"]
 

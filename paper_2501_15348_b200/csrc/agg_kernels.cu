@@ -305,15 +305,19 @@ __device__ __forceinline__ float4 ld_hint(const float* p, uint64_t pol) {
 // and the first G entries one step ahead together with this step's
 // destination-row and source-row loads, so a step costs one memory round trip
 // instead of three. Entries are applied in the reference's order (deletions,
-// then insertions, ascending source), exactly as in k_agg_delta.
-template <int G, int U, bool MEAN, int MINB = 1>
+// then insertions, ascending source); with the compact block a persisting
+// changed-source pair is one entry (its difference row) at the deletion's place.
+template <int G, int U, bool MEAN, int MINB = 1, bool STRUCT = false>
 __global__ void __launch_bounds__(kThreads, MINB)
 k_agg_delta_v4(int n_rows, int w, int32_t num_nodes, const int32_t* __restrict__ rows,
                const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ ent,
                const float* __restrict__ Fp, const float* __restrict__ Fc,
                const float* __restrict__ Cp, const float* __restrict__ Cc,
                float* __restrict__ values, float* __restrict__ degree, float* __restrict__ msum,
-               int st_evict_first) {
+               int st_evict_first, const int32_t* __restrict__ changed) {
+  // STRUCT: structural mode (Fp == Fc = one matrix H, no compact
+  // block): folded pairs ~(N + p) cancel and are skipped, insertions N + p
+  // read H[changed[p]] — Agg_{G_t}(H) from Agg_{G_{t-1}}(H)
   constexpr int R = 32 / G;
   const int lane = threadIdx.x & 31, gl = lane & (G - 1), sub = lane / G;
   const int64_t wg = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
@@ -365,20 +369,25 @@ k_agg_delta_v4(int n_rows, int w, int32_t num_nodes, const int32_t* __restrict__
 #pragma unroll
         for (int q = 0; q < kUnroll; ++q) {
           s[q] = __shfl_sync(0xffffffffu, my_s, (j0 + q) & (G - 1), G);
-          if (valid && cact && j0 + q < cnt && eb + j0 + q < m0.cnt) {
+          if (valid && cact && j0 + q < cnt && eb + j0 + q < m0.cnt &&
+              !(STRUCT && s[q] < 0 && ~s[q] >= num_nodes)) {
             const int32_t u0 = s[q] < 0 ? ~s[q] : s[q];
             const bool cpt = u0 >= num_nodes;
-            const float* src = cpt ? (s[q] < 0 ? Cp : Cc) + static_cast<int64_t>(u0 - num_nodes) * w + c
-                                   : (s[q] < 0 ? Fp : Fc) + static_cast<int64_t>(u0) * w + c;
+            const float* src;
+            if (STRUCT && cpt) src = Fc + static_cast<int64_t>(changed[u0 - num_nodes]) * w + c;
+            else if (cpt) src = (s[q] < 0 ? Cp : Cc) + static_cast<int64_t>(u0 - num_nodes) * w + c;
+            else src = (s[q] < 0 ? Fp : Fc) + static_cast<int64_t>(u0) * w + c;
 #pragma unroll
             for (int u = 0; u < U; ++u)
-              if (col_ok(u)) x[q][u] = ld_nc_hint(src + 4 * G * u, cpt ? keep : once);
+              if (col_ok(u)) x[q][u] = ld_nc_hint(src + 4 * G * u, cpt && !STRUCT ? keep : once);
           }
         }
 #pragma unroll
         for (int q = 0; q < kUnroll; ++q) {
           if (!(valid && j0 + q < cnt && eb + j0 + q < m0.cnt)) continue;
-          if (MEAN) dnet += s[q] < 0 ? -1 : 1;
+          if (STRUCT && s[q] < 0 && ~s[q] >= num_nodes) continue;  // persisting pair: cancels
+          // a compact-block deletion is a folded (deletion, insertion) pair
+          if (MEAN) dnet += s[q] >= 0 ? 1 : (~s[q] >= num_nodes ? 0 : -1);
           if (!cact) continue;
 #pragma unroll
           for (int u = 0; u < U; ++u) {
@@ -717,7 +726,8 @@ void agg_scratch(int kind, int n, int w, const int64_t* in_ptr, const int32_t* i
 void agg_delta(int kind, int n_rows, int w, const int32_t* rows, const int32_t* row_ptr,
                const int32_t* ent, const float* f_prev, const float* f_curr, float* values,
                float* degree, float* mean_sums, int32_t* argext, cudaStream_t stream,
-               const int32_t* ent_c, int32_t num_nodes, int64_t n_changed, const float* compact) {
+               const int32_t* ent_c, int32_t num_nodes, int64_t n_changed, const float* compact,
+               const int32_t* row_ptr_c) {
   if (n_rows <= 0 || w <= 0) return;
   const int vec = pick_vec(w, f_prev, values);
   const bool aligned = pick_vec(w, f_curr, mean_sums) == 4 && pick_vec(w, compact, nullptr) == 4;
@@ -741,6 +751,7 @@ void agg_delta(int kind, int n_rows, int w, const int32_t* rows, const int32_t* 
   (void)l2_once;
   if (ent_c == nullptr) {  // no compact block: every source is a full-matrix row
     ent_c = ent;
+    row_ptr_c = row_ptr;
     num_nodes = INT32_MAX;
   }
   static const int u_env = [] {
@@ -759,8 +770,8 @@ void agg_delta(int kind, int n_rows, int w, const int32_t* rows, const int32_t* 
     const float* cc = compact ? compact + n_changed * w : nullptr;
 #define DGNN_DELTA_LAUNCH(UU, MM)                                                                    \
   DGNN_DISPATCH_G(g, DGNN_LAUNCH((k_agg_delta_v4<G, UU, MM>), grid, kThreads, 0, stream, n_rows, w, \
-                                 num_nodes, rows, row_ptr, ent_c, f_prev, f_curr, cp, cc, values,   \
-                                 degree, mean_sums, st_ef))
+                                 num_nodes, rows, row_ptr_c, ent_c, f_prev, f_curr, cp, cc, values, \
+                                 degree, mean_sums, st_ef, nullptr))
     // destination rows are written once per delta: evict_first keeps them
     // from displacing the compact block (DGNN_DELTA_ST_HINT=0 disables)
     static const int st_ef = [] {
@@ -775,12 +786,12 @@ void agg_delta(int kind, int n_rows, int w, const int32_t* rows, const int32_t* 
       DGNN_DELTA_LAUNCH(4, true);
     } else if (U == 4 && minb == 3) {
       DGNN_DISPATCH_G(g, DGNN_LAUNCH((k_agg_delta_v4<G, 4, false, 3>), grid, kThreads, 0, stream, n_rows,
-                                     w, num_nodes, rows, row_ptr, ent_c, f_prev, f_curr, cp, cc,
-                                     values, degree, mean_sums, st_ef))
+                                     w, num_nodes, rows, row_ptr_c, ent_c, f_prev, f_curr, cp, cc,
+                                     values, degree, mean_sums, st_ef, nullptr))
     } else if (U == 4 && minb == 4) {
       DGNN_DISPATCH_G(g, DGNN_LAUNCH((k_agg_delta_v4<G, 4, false, 4>), grid, kThreads, 0, stream, n_rows,
-                                     w, num_nodes, rows, row_ptr, ent_c, f_prev, f_curr, cp, cc,
-                                     values, degree, mean_sums, st_ef))
+                                     w, num_nodes, rows, row_ptr_c, ent_c, f_prev, f_curr, cp, cc,
+                                     values, degree, mean_sums, st_ef, nullptr))
     } else if (U == 4) {
       DGNN_DELTA_LAUNCH(4, false);
     } else if (U == 2 && kind == kAggMean) {
@@ -800,6 +811,35 @@ void agg_delta(int kind, int n_rows, int w, const int32_t* rows, const int32_t* 
   DGNN_DISPATCH_KIND(kind, DGNN_DISPATCH_V(vec, DGNN_DISPATCH_G(g,
       DGNN_LAUNCH((k_agg_delta<V, G, KIND>), grid, kThreads, 0, stream, n_rows, w, rows, row_ptr,
                   ent, f_prev, f_curr, values, degree, mean_sums, argext))));
+}
+
+bool agg_delta_struct(int kind, int n_rows, int w, const int32_t* rows, const int32_t* row_ptr_c,
+                      const int32_t* ent_c, int32_t num_nodes, const int32_t* changed,
+                      const float* h, float* values, float* degree, float* mean_sums,
+                      cudaStream_t stream) {
+  if (kind != kAggSum && kind != kAggMean) return false;
+  if (pick_vec(w, h, values) != 4 || pick_vec(w, mean_sums, nullptr) != 4) return false;
+  int U = w % 8 == 0 && w >= 32 ? 2 : 1;
+  if (w % 16 == 0 && w >= 64) U = 4;
+  if (w > 128 * U) return false;
+  if (n_rows <= 0) return true;
+  const int g = pick_group(w, 4 * U);
+  const int grid = rows_grid(n_rows, g);
+#define DGNN_STRUCT_LAUNCH(UU, MM)                                                                    \
+  DGNN_DISPATCH_G(g, DGNN_LAUNCH((k_agg_delta_v4<G, UU, MM, 1, true>), grid, kThreads, 0, stream,  \
+                                 n_rows, w, num_nodes, rows, row_ptr_c, ent_c, h, h, nullptr,       \
+                                 nullptr, values,                                                   \
+                                 degree, mean_sums, 1, changed))
+  const bool mean = kind == kAggMean;
+  if (U == 4) {
+    if (mean) DGNN_STRUCT_LAUNCH(4, true) else DGNN_STRUCT_LAUNCH(4, false)
+  } else if (U == 2) {
+    if (mean) DGNN_STRUCT_LAUNCH(2, true) else DGNN_STRUCT_LAUNCH(2, false)
+  } else {
+    if (mean) DGNN_STRUCT_LAUNCH(1, true) else DGNN_STRUCT_LAUNCH(1, false)
+  }
+#undef DGNN_STRUCT_LAUNCH
+  return true;
 }
 
 void agg_deleted_contributor(int64_t n_del, int w, const uint64_t* del_keys,

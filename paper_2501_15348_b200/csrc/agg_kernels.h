@@ -23,15 +23,27 @@ void agg_scratch(int kind, int n, int w, const int64_t* in_ptr, const int32_t* i
 // are deletions (~src, gathered from f_prev) then insertions (src, from f_curr).
 // sum: values +=/-=; mean: mean_sums and degree updated, values renormalised;
 // max/min: insertions only (deleted contributors must have been ruled out).
-// With ent_c (sum / mean, 128-bit aligned rows, w <= 128) the pipelined
-// kernel reads sources >= num_nodes from the compact changed-row block:
-// deletions from compact[(s - N) * w], insertions from compact[(n_changed +
-// s - N) * w] — the same values, so the same results.
+// With ent_c / row_ptr_c (sum / mean, 128-bit aligned rows, w <= 512) the
+// pipelined kernel reads sources >= num_nodes from the compact changed-row
+// block (DevDelta::compact): deletions ~(N + p) subtract the negated
+// difference row compact[p * w] (a folded deletion + insertion pair: degree
+// unchanged), insertions N + p add F_t[changed[p]] = compact[(n_changed + p) * w].
 void agg_delta(int kind, int n_rows, int w, const int32_t* rows, const int32_t* row_ptr,
                const int32_t* ent, const float* f_prev, const float* f_curr, float* values,
                float* degree, float* mean_sums, int32_t* argext, cudaStream_t stream,
                const int32_t* ent_c = nullptr, int32_t num_nodes = 0, int64_t n_changed = 0,
-               const float* compact = nullptr);
+               const float* compact = nullptr, const int32_t* row_ptr_c = nullptr);
+
+// Structural update of one matrix's aggregation, in place: values (=
+// Agg_{G_{t-1}}(H), sum / mean) becomes Agg_{G_t}(H) using delta t's folded
+// layout (rows, row_ptr_c, ent_c; `changed` = DevDelta::changed): removed
+// edges subtract H[src], added edges add it, persisting edges of
+// feature-changed nodes are skipped. Returns false (nothing launched) when
+// the shape / kind is not supported; the caller then aggregates from scratch.
+bool agg_delta_struct(int kind, int n_rows, int w, const int32_t* rows, const int32_t* row_ptr_c,
+                      const int32_t* ent_c, int32_t num_nodes, const int32_t* changed,
+                      const float* h, float* values, float* degree, float* mean_sums,
+                      cudaStream_t stream);
 
 // flag |= 1 if any deleted edge (sorted src << 32 | dst keys) is a recorded
 // max/min contributor.

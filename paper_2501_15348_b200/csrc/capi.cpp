@@ -739,7 +739,7 @@ int dgnn_graph_apply_delta(const dgnn_graph* g, int32_t t, int32_t kind, float* 
     FeatRef fp = G.features(t - 1, st), fc = G.features(t, st);
     cuda::agg_delta(kind, dd.n_rows, G.feature_dim(), dd.rows.get(), dd.row_ptr.get(), dd.ent.get(),
                     fp->get(), fc->get(), values, degree, mean_sums, argext, st, dd.ent_c.get(),
-                    G.num_nodes(), dd.n_changed, dd.compact.get());
+                    G.num_nodes(), dd.n_changed, dd.compact.get(), dd.row_ptr_c.get());
   });
 }
 

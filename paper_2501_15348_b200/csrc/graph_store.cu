@@ -178,24 +178,93 @@ __global__ void k_gather_rows(int64_t m, int32_t d, const int32_t* __restrict__ 
   }
 }
 
-// ent_c[i] = ent[i] with a source found in `changed` (ascending) replaced by
-// N + its position, keeping the deletion (~) / insertion encoding
-__global__ void k_remap_compact(int64_t m, const int32_t* __restrict__ ent, int64_t n_changed,
-                                const int32_t* __restrict__ changed, int32_t num_nodes,
-                                int32_t* __restrict__ ent_c) {
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int32_t e = ent[i];
-    const int32_t s = e < 0 ? ~e : e;
-    int64_t lo = 0, hi = n_changed;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (changed[mid] < s) lo = mid + 1; else hi = mid;
-    }
-    int32_t r = s;
-    if (lo < n_changed && changed[lo] == s) r = num_nodes + static_cast<int32_t>(lo);
-    ent_c[i] = e < 0 ? ~r : r;
+__device__ __forceinline__ int64_t find_sorted(const int32_t* a, int64_t n, int32_t x) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1; else hi = mid;
   }
+  return lo < n && a[lo] == x ? lo : -1;
+}
+
+// Per delta-SpMM entry (one thread; a hub destination can hold 10^4+
+// entries, so rows are not serialised): ent_c = ent re-indexed for the
+// compact block [F_{t-1}[changed] - F_t[changed] | F_t[changed]]. A
+// feature-changed source u present as a deletion AND an insertion of the same
+// destination (a persisting out-edge of a changed node — most of a feature
+// delta's entries) becomes ONE deletion of its negated difference row
+// (~(N + pos)): the row gains F_t[u] - F_{t-1}[u] from one gather instead of
+// two, and the insertion entry is dropped (keep = 0). An unpaired changed
+// insertion reads F_t[u] from the compact block (N + pos); an unpaired
+// changed deletion keeps its plain index (F_{t-1} matrix). Row order is
+// unchanged: deletions, then insertions, each ascending by source.
+__global__ void k_remap_compact_ent(int64_t ne, int32_t n_rows, const int32_t* __restrict__ row_ptr,
+                                    const int32_t* __restrict__ ent, int64_t n_changed,
+                                    const int32_t* __restrict__ changed, int32_t num_nodes,
+                                    int32_t* __restrict__ ent_c, int32_t* __restrict__ keep) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < ne;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t x = ent[i];
+    const bool del = x < 0;
+    const int32_t s = del ? ~x : x;
+    const int64_t pos = find_sorted(changed, n_changed, s);
+    int32_t out = x, k1 = 1;
+    if (pos >= 0) {
+      // row of entry i: last r with row_ptr[r] <= i
+      int32_t lo = 0, hi = n_rows;
+      while (hi - lo > 1) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (row_ptr[mid] <= i) lo = mid; else hi = mid;
+      }
+      const int32_t b = row_ptr[lo], e = row_ptr[lo + 1];
+      // first insertion of the row (deletions < 0 come first)
+      int32_t kl = b, kh = e;
+      while (kl < kh) {
+        const int32_t mid = (kl + kh) >> 1;
+        if (ent[mid] < 0) kl = mid + 1; else kh = mid;
+      }
+      // the opposite side, ascending by source
+      int32_t l2 = del ? kl : b, h2 = del ? e : kl;
+      const int32_t end = h2;
+      while (l2 < h2) {
+        const int32_t mid = (l2 + h2) >> 1;
+        const int32_t v = del ? ent[mid] : ~ent[mid];
+        if (v < s) l2 = mid + 1; else h2 = mid;
+      }
+      const bool paired = l2 < end && (del ? ent[l2] : ~ent[l2]) == s;
+      const int32_t ci = num_nodes + static_cast<int32_t>(pos);
+      if (del) {
+        if (paired) out = ~ci;  // negated difference row
+      } else if (paired) {
+        k1 = 0;  // folded into the deletion entry
+      } else {
+        out = ci;
+      }
+    }
+    ent_c[i] = out;
+    keep[i] = k1;
+  }
+}
+
+// row_ptr_c[r] = kept entries before row r (scan of keep at the row start)
+__global__ void k_row_ptr_c(int32_t n_rows, const int32_t* __restrict__ row_ptr,
+                            const int32_t* __restrict__ scan, int32_t* __restrict__ row_ptr_c) {
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r <= n_rows;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    row_ptr_c[r] = scan[row_ptr[r]];
+}
+
+__global__ void k_nonzero_u8(int64_t n, const int32_t* __restrict__ x, uint8_t* __restrict__ f) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    f[i] = x[i] != 0;
+}
+
+// dst[i] -= src[i]
+__global__ void k_sub_inplace(int64_t n, float* __restrict__ dst, const float* __restrict__ src) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[i] -= src[i];
 }
 
 int grid_for(int64_t n) { return cuda::wave_grid(n, kT, 8); }
@@ -425,7 +494,7 @@ int64_t DeviceGraph::device_bytes() const {
     b += s.in_ptr.bytes() + s.out_ptr.bytes() + s.in_src.bytes() + s.out_dst.bytes();
   for (const auto& d : deltas_)
     b += d.del.bytes() + d.ins.bytes() + d.changed.bytes() + d.rows.bytes() + d.row_ptr.bytes() +
-         d.ent.bytes() + d.ent_c.bytes() + d.compact.bytes();
+         d.ent.bytes() + d.ent_c.bytes() + d.row_ptr_c.bytes() + d.compact.bytes();
   for (const auto& s : slots_) b += s->buf.bytes();
   return b;
 }
@@ -669,12 +738,15 @@ void DeviceGraph::build_delta(int32_t t, const float* prev_feats, const float* f
   if (dd.n_changed) {
     DGNN_CUDA(cudaMemcpyAsync(dd.changed.get(), changed.get(), sizeof(int32_t) * dd.n_changed,
                               cudaMemcpyDeviceToDevice, st));
-    // [F_{t-1}[changed] | F_t[changed]]; the second half is the version patch of t
+    // [F_{t-1}[changed] - F_t[changed] | F_t[changed]]; the second half is the
+    // version patch of t
     dd.compact = DevArray<float>(2 * dd.n_changed * d_, st);
     DGNN_LAUNCH(k_gather_rows, grid_for(dd.n_changed * d_), kT, 0, st, dd.n_changed, d_,
                 dd.changed.get(), prev_feats, dd.compact.get());
     DGNN_LAUNCH(k_gather_rows, grid_for(dd.n_changed * d_), kT, 0, st, dd.n_changed, d_,
                 dd.changed.get(), feats, dd.compact.get() + dd.n_changed * d_);
+    DGNN_LAUNCH(k_sub_inplace, grid_for(dd.n_changed * d_), kT, 0, st, dd.n_changed * d_,
+                dd.compact.get(), dd.compact.get() + dd.n_changed * d_);
   }
   // expansion sizes
   auto expansion = [&](const DevSnapshot& S, int64_t* total) {
@@ -752,11 +824,28 @@ void DeviceGraph::build_delta(int32_t t, const float* prev_feats, const float* f
     DGNN_CUDA(cudaMemsetAsync(counts.get() + nr, 0, sizeof(int32_t), st));
   }
   cub.exclusive_sum(counts.get(), dd.row_ptr.get(), nr + 1);
-  // sources re-indexed into the compact changed-row block
-  dd.ent_c = DevArray<int32_t>(ne, st);
-  if (ne)
-    DGNN_LAUNCH(k_remap_compact, grid_for(ne), kT, 0, st, ne, dd.ent.get(), dd.n_changed,
-                dd.changed.get(), n_, dd.ent_c.get());
+  // sources re-indexed into the compact changed-row block, persisting
+  // changed-source pairs folded into one difference-row entry
+  {
+    DevArray<int32_t> ent_all(ne, st), keep(ne + 1, st), scan(ne + 1, st);
+    DGNN_CUDA(cudaMemsetAsync(keep.get() + ne, 0, sizeof(int32_t), st));
+    if (ne)
+      DGNN_LAUNCH(k_remap_compact_ent, grid_for(ne), kT, 0, st, ne, static_cast<int32_t>(nr),
+                  dd.row_ptr.get(), dd.ent.get(), dd.n_changed, dd.changed.get(), n_,
+                  ent_all.get(), keep.get());
+    cub.exclusive_sum(keep.get(), scan.get(), ne + 1);
+    dd.row_ptr_c = DevArray<int32_t>(nr + 1, st);
+    DGNN_LAUNCH(k_row_ptr_c, grid_for(nr + 1), kT, 0, st, static_cast<int32_t>(nr),
+                dd.row_ptr.get(), scan.get(), dd.row_ptr_c.get());
+    DevArray<uint8_t> flag(ne, st);
+    if (ne) DGNN_LAUNCH(k_nonzero_u8, grid_for(ne), kT, 0, st, ne, keep.get(), flag.get());
+    DevArray<int32_t> tmp(ne, st);
+    dd.n_ent_c = cub.select_flagged(ent_all.get(), flag.get(), tmp.get(), ne);
+    dd.ent_c = DevArray<int32_t>(dd.n_ent_c, st);
+    if (dd.n_ent_c)
+      DGNN_CUDA(cudaMemcpyAsync(dd.ent_c.get(), tmp.get(), sizeof(int32_t) * dd.n_ent_c,
+                                cudaMemcpyDeviceToDevice, st));
+  }
   DGNN_CUDA(cudaStreamSynchronize(st));
   deltas_[t] = std::move(dd);
 }

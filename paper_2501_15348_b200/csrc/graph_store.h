@@ -75,13 +75,17 @@ struct DevDelta {
   int32_t n_rows = 0;
   int64_t n_ent = 0;
   cuda::DevArray<int32_t> rows, row_ptr, ent;
-  // Feature-changed sources, compacted: compact = [F_{t-1}[changed] |
-  // F_t[changed]] (2 x n_changed x d; the second half is also the version
-  // patch of t), and ent_c = ent with every source in `changed` re-indexed to
-  // N + (its position in changed). A changed node contributes all its
-  // out-edges to both G- and G+, so ~2/3 of the delta's gathers at C4 hit this
-  // small L2-resident block instead of random rows of two 2 GB matrices.
-  cuda::DevArray<int32_t> ent_c;
+  // Feature-changed sources, compacted: compact = [F_{t-1}[changed] -
+  // F_t[changed] | F_t[changed]] (2 x n_changed x d; the second half is also
+  // the version patch of t). A changed node contributes all its out-edges to
+  // both G- and G+ (~2/3 of the delta's entries at C4); ent_c / row_ptr_c fold
+  // each such persisting pair into ONE entry ~(N + pos) that subtracts the
+  // negated difference row, so those gathers halve and hit a 41 MB
+  // L2-resident block instead of random rows of two 2 GB matrices. Unpaired
+  // changed insertions read N + pos (F_t half); unpaired deletions keep
+  // their plain index.
+  int64_t n_ent_c = 0;
+  cuda::DevArray<int32_t> ent_c, row_ptr_c;
   cuda::DevArray<float> compact;
   // distinct deletion / insertion sources (algorithmic-byte accounting)
   int64_t u_minus = 0, u_plus = 0;

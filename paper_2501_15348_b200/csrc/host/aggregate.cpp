@@ -337,6 +337,32 @@ std::shared_ptr<AggResult> aggregate_scratch(const GraphView& graph, const float
   return r;
 }
 
+std::shared_ptr<AggResult> aggregate_rebase(const AggResult& base, const GraphView& graph,
+                                            const float* feats, int32_t dim, const DevDelta& delta,
+                                            const AggrFn& fn, cudaStream_t stream) {
+  check(fn.kind == AggrKind::kSum || fn.kind == AggrKind::kMean, "rebase: sum / mean only");
+  check(base.rows == graph.num_nodes, "rebase: base rows differ from the view");
+  auto r = alloc_result(fn.kind, graph.num_nodes, dim, stream);
+  r->num_edges = graph.num_edges;
+  r->t = graph.t;
+  const size_t nw = static_cast<size_t>(graph.num_nodes) * dim;
+  // copy of the base + the structural delta's gathers and row read-modify-writes
+  const double bytes = 8.0 * nw + 8.0 * delta.n_ent_c + 4.0 * dim * delta.n_ent_c +
+                       8.0 * dim * delta.n_rows;
+  ProfScope ps(kProfAggRebase, stream, bytes);
+  copy_dev(r->values.get(), base.values.get(), nw * sizeof(float), stream);
+  if (fn.kind == AggrKind::kMean) {
+    copy_dev(r->degree.get(), base.degree.get(), graph.num_nodes * sizeof(float), stream);
+    copy_dev(r->mean_sums.get(), base.mean_sums.get(), nw * sizeof(float), stream);
+  }
+  const bool ok = cuda::agg_delta_struct(kind_i(fn.kind), delta.n_rows, dim, delta.rows.get(),
+                                         delta.row_ptr_c.get(), delta.ent_c.get(), graph.num_nodes,
+                                         delta.changed.get(), feats, r->values.get(),
+                                         r->degree.get(), r->mean_sums.get(), stream);
+  check(ok, "rebase: unsupported aggregation shape");
+  return r;
+}
+
 IncrementalResult aggregate_incremental(const AggResult& prev, const GraphView& prev_graph,
                                         const GraphView& curr_graph, const float* prev_feats,
                                         const float* curr_feats, const DevDelta& delta,
@@ -393,7 +419,8 @@ IncrementalResult aggregate_incremental(const AggResult& prev, const GraphView& 
     cuda::agg_delta(kind_i(fn.kind), delta.n_rows, dim, delta.rows.get(), delta.row_ptr.get(),
                     delta.ent.get(), prev_feats, curr_feats, r->values.get(), r->degree.get(),
                     r->mean_sums.get(), r->argext.get(), stream, delta.ent_c.get(),
-                    curr_graph.num_nodes, delta.n_changed, delta.compact.get());
+                    curr_graph.num_nodes, delta.n_changed, delta.compact.get(),
+                    delta.row_ptr_c.get());
   }
   refresh_dense(*r, stream);
   return {std::move(r), false, FallbackReason::kNone};

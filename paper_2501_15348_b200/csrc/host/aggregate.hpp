@@ -100,6 +100,14 @@ std::shared_ptr<AggResult> aggregate_scratch(const GraphView& graph, const float
 
 // Eq. 2 incremental update from prev (ref src/aggregate.cpp:117-207): the
 // new result is out of place (prev stays valid for its co-owners).
+// Agg_{G_t}(H) from base = Agg_{G_{t-1}}(H) of the SAME matrix H: a copy
+// plus the structural part of delta t (removed edges subtract H[src], added
+// edges add it). Same values as aggregate_scratch(graph, H) up to fp32
+// summation order. Sum / mean only; graph must be the full snapshot t.
+std::shared_ptr<AggResult> aggregate_rebase(const AggResult& base, const GraphView& graph,
+                                            const float* feats, int32_t dim, const DevDelta& delta,
+                                            const AggrFn& fn, cudaStream_t stream);
+
 IncrementalResult aggregate_incremental(const AggResult& prev, const GraphView& prev_graph,
                                         const GraphView& curr_graph, const float* prev_feats,
                                         const float* curr_feats, const DevDelta& delta,
@@ -117,11 +125,12 @@ void aggregate_backward(const GraphView& graph, const float* upstream, int32_t d
 // algorithmic bytes per class.
 enum ProfClass { kProfAggScratch = 0, kProfAggDelta = 1, kProfAggBackward = 2, kProfCellFwd = 3,
                  kProfCellBwd = 4, kProfWeightGrad = 5, kProfOther = 6, kProfCellBwdGemm = 7,
-                 kProfSample = 8,      // one whole (window, batch) sample, first to last op
-                 kProfSampleHost = 9,  // host time to issue one sample (no events)
-                 kProfHostBuild = 10, kProfHostFwd = 11, kProfHostBwd = 12,  // its phases
-                 kProfHostAlloc = 13,  // host time inside device allocations
-                 kProfCount = 14 };
+                 kProfAggRebase = 8,   // hidden aggregation rebased across a structural delta
+                 kProfSample = 9,      // one whole (window, batch) sample, first to last op
+                 kProfSampleHost = 10, // host time to issue one sample (no events)
+                 kProfHostBuild = 11, kProfHostFwd = 12, kProfHostBwd = 13,  // its phases
+                 kProfHostAlloc = 14,  // host time inside device allocations
+                 kProfCount = 15 };
 struct ProfStat {
   int64_t launches = 0;
   double ms = 0.0;

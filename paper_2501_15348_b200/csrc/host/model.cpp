@@ -835,7 +835,9 @@ ForwardArtifacts model_forward(DgnnModel& model, const SeqSample& sample, AggPro
   if (is_stacked(model.cfg_.arch)) return stacked_forward(model, sample, provider);
   cudaStream_t prev = provider.stream();
   provider.set_stream(lanes.main());
+  provider.clear_hidden_bases();
   ForwardArtifacts out = seq2seq_forward(model, sample, provider, lanes);
+  provider.clear_hidden_bases();
   provider.set_stream(prev);
   return out;
 }

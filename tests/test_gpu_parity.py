@@ -149,8 +149,9 @@ def test_agg_delta_kernel_inplace(pair, api):
 @pytest.mark.parametrize("kind", ["sum", "mean"])
 def test_graph_delta_compact_block(ref, api, kind):
     """K2 on the graph's own delta with the compact changed-row block (heavy
-    feature churn): equals scratch at t, and is bitwise the plain-index
-    kernel's result (same values gathered in the same order)."""
+    feature churn; persisting changed-source pairs folded into one
+    difference-row entry): equals scratch at t and the plain-index kernel's
+    result within fp32 rounding; mean degrees exact."""
     import torch
     g_ref, g = make_pair(ref, api, n=500, avg_degree=6, dim=16, T=5, edge=0.05, feat=0.2, seed=9)
     for t in range(1, g_ref.T):
@@ -161,7 +162,7 @@ def test_graph_delta_compact_block(ref, api, kind):
         torch.cuda.synchronize()
         want = g_ref.agg_scratch(t, kind, g_ref.feats(t))
         assert nrel(a["values"].cpu().numpy(), want["values"]) < 1e-5, t
-        assert torch.equal(a["values"], b["values"]), t
+        assert nrel(a["values"].cpu().numpy(), b["values"].cpu().numpy().astype(np.float64)) < 1e-6, t
         if kind == "mean":
             assert np.array_equal(a["degree"].cpu().numpy(), want["degree"].astype(np.float32))
 
@@ -221,9 +222,11 @@ ARCHS = ["gcrn_m2", "tgcn", "gcrn_m1", "cd_gcn"]
 
 
 @pytest.mark.parametrize("arch", ARCHS)
-@pytest.mark.parametrize("aggr", ["sum", "max"])
+@pytest.mark.parametrize("aggr", ["sum", "mean", "max"])
 def test_sample_grads(ref, api, pair, arch, aggr):
-    """One sample: init params bit-exact, loss / prediction / gradients (rel 1e-4)."""
+    """One sample: init params bit-exact, loss / prediction / gradients (rel 1e-4).
+    Integrated archs with sum / mean carry hidden aggregations across each
+    structural delta (agg_rebase), which must be what ran."""
     g_ref, g = pair
     cfg_r = ref.RunCfg(arch=arch, hidden=16, aggr=aggr)
     cfg = api.TrainConfig(arch=arch, hidden=16, aggr=aggr)
@@ -236,6 +239,13 @@ def test_sample_grads(ref, api, pair, arch, aggr):
         assert abs(loss - loss_r) <= 1e-5 * abs(loss_r), (loss, loss_r)
         assert nrel(pred, pred_r) < 1e-5
         assert nrel(grads, grads_r) < 1e-4
+    if arch in ("gcrn_m2", "tgcn") and aggr != "max":
+        api.prof_enable(True)
+        api.prof_reset()
+        s.sample_grads(0)
+        rebased = api.prof_get()["agg_rebase"]["launches"]
+        api.prof_enable(False)
+        assert rebased > 0
 
 
 def _events_match(ev, ev_ref):
