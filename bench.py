@@ -262,7 +262,10 @@ def main():
     def ncu_traffic(name):
         """DRAM bytes per launch (dram__bytes_read + write) of this kernel from
         the committed `ncu --set full` capture of the same workload, or None."""
-        path = os.path.join(ROOT, "profiles", f"r1_ncu_spmm_{args.workload}.json")
+        fname = f"r1_ncu_spmm_{args.workload}.json"
+        if name == "agg_delta" and args.workload == "c4":
+            fname = "r1_ncu_delta_v7.json"  # the folded-layout K2 at the C4 delta shape
+        path = os.path.join(ROOT, "profiles", fname)
         if name not in ncu_kernels or not os.path.exists(path):
             return None
         rows = [e for e in json.load(open(path)) if ncu_kernels[name] in e.get("kernel", "")]
