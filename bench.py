@@ -102,52 +102,99 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ reference arm
+def host_cpu():
+    """CPU model and core count of the box the reference runs on."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+# Same-config reference runs: the reference's seq-first / distsim epoch on the
+# workload's exact graph (N, E, d, h, churn), timed by its own EpochReport
+# clock (src/train.cpp:151, :203-204). C1 runs whole epochs; C2's epoch is
+# 1,991 identical-cost windows over a 207-node graph, so one reference step
+# is a contiguous prefix of them (the generator's first T' snapshots are the
+# same for any T >= T').
+SAME_CONFIG_T = {"c1": 16, "c2": 200}
+
+
+def reference_same_config(wl, name):
+    from oracle import refbind as R
+    T = SAME_CONFIG_T[name]
+    g = R.RefGraph.synth(wl["n"], wl["deg"], wl["dim"], T, wl["edge"], wl["feat"], seed=1)
+    r = g.run(R.RunCfg(arch=wl["arch"], hidden=wl["hidden"], workers=1, record_events=False))
+    rate = len(r.losses) * (L + H) / r.seconds
+    full = "the full epoch" if T == wl["T"] else f"the first {len(r.losses)} of the epoch's windows"
+    desc = (f"reference seq-first/distsim epoch (oracle/_ref, Eigen-subset shim, 1 thread) on the "
+            f"workload's own graph ({wl['n']} nodes, d={wl['dim']}, h={wl['hidden']}): {full}, "
+            f"{len(r.losses)} windows in {r.seconds:.1f}s")
+    return rate, r.seconds, desc
+
+
 def reference_sample(wl, budget_s=15.0):
-    """Times the reference's seq-first trainer (oracle/_ref) on a bounded
-    sample of the workload: same degree / feature / hidden / churn, N scaled
-    down, T = L+H+2 snapshots (one window, SURVEY §0 T-1 rule). Returns
-    (C3-equivalent snapshots/sec, raw rate, description)."""
+    """Workloads the reference cannot hold (C3: ~43 GB of materialised fp64
+    snapshots, C4: ~348 GB): times its seq-first trainer on a bounded sample
+    — same degree / feature / hidden / churn, N scaled down, T = L+H+2 (one
+    window, SURVEY §0 T-1 rule) — and scales the rate linearly in N. An
+    extrapolation, not a same-config measurement. Returns (scaled rate, raw
+    rate, seconds, description)."""
     from oracle import refbind as R
     cfg = R.RunCfg(arch=wl["arch"], hidden=wl["hidden"], workers=1, record_events=False)
 
     def run(n):
         g = R.RefGraph.synth(n, wl["deg"], wl["dim"], L + H + 2, wl["edge"], wl["feat"], seed=1)
-        t0 = time.perf_counter()
         r = g.run(cfg)
-        wall = time.perf_counter() - t0
-        return len(r.losses) * (L + H) / r.seconds, r.seconds, wall
+        return len(r.losses) * (L + H) / r.seconds, r.seconds
 
     probe_n = 2000
-    rate, secs, _ = run(probe_n)
+    rate, secs = run(probe_n)
     n = int(min(max(probe_n * budget_s / max(secs, 1e-3), probe_n), wl["n"]))
-    rate, secs, _ = run(n)
+    rate, secs = run(n)
     scaled = rate * n / wl["n"]
-    desc = (f"reference seq-first/distsim epoch (oracle/_ref, Eigen-subset shim, 1 thread) on a "
-            f"{n}-node sample of the workload (avg degree {wl['deg']:g}, d={wl['dim']}, h={wl['hidden']}, "
-            f"{wl['edge']:.0%} churn, T={L + H + 2}: 1 window); {rate:.3f} snapshots/s at the sample, "
-            f"scaled x{n}/{wl['n']} (cost linear in N and E) to the full workload; {secs:.1f}s per sample")
+    desc = (f"EXTRAPOLATED: reference seq-first/distsim epoch (oracle/_ref, Eigen-subset shim, 1 thread) "
+            f"on a {n}-node sample of the workload (avg degree {wl['deg']:g}, d={wl['dim']}, "
+            f"h={wl['hidden']}, {wl['edge']:.0%} churn, T={L + H + 2}: 1 window); {rate:.3f} snapshots/s "
+            f"at the sample, scaled x{n}/{wl['n']} (cost linear in N and E) to the full workload; "
+            f"{secs:.1f}s per sample")
     return scaled, rate, secs, desc
+
+
+def reference_step(wl, name):
+    """One reference-arm step: (rate, same_config, description)."""
+    if name in SAME_CONFIG_T:
+        rate, _, desc = reference_same_config(wl, name)
+        return rate, True, desc
+    v, _, _, desc = reference_sample(wl)
+    return v, False, desc
 
 
 def run_reference_arm(args, wl):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    for _ in range(args.warmup if args.warmup < 1 else 1):
-        pass
-    vals = []
-    desc = ""
+    # a single-threaded CPU code path has no device or JIT to warm: the
+    # warm-up steps are untimed repetitions of the same step, capped at one
+    for _ in range(min(args.warmup, 1)):
+        reference_step(wl, args.workload)
+    vals, same, desc = [], False, ""
     for _ in range(max(args.steps, 1)):
-        v, raw, secs, desc = reference_sample(wl)
+        v, same, desc = reference_step(wl, args.workload)
         vals.append(v)
     value = statistics.median(vals)
     line = {
         "impl": "reference", "metric": "training snapshots/sec", "value": value,
-        "unit": "snapshots/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "unit": "snapshots/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": min(args.warmup, 1),
         "higher_is_better": True, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.workload, "desc": wl["desc"]},
+        "same_config": same,
         "cpu_baseline": {"value": value, "unit": "snapshots/s", "cores": 1, "kind": "reference",
-                         "sample": desc},
+                         "sample": desc, **host_cpu()},
         "e2e": {"value": value, "unit": "snapshots/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "vs_baseline": None,
     }
@@ -165,6 +212,9 @@ def main():
     ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--hbm-cache-gb", type=float, default=0.0,
+                    help="second cache level: HBM budget of unborrowed cached aggregations "
+                         "(0 = everything stays in HBM; C4 spills below ~16 GB)")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
@@ -198,7 +248,8 @@ def main():
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
     log(f"[rank {rank}] synth {t_synth:.1f}s, device graph build {t_build:.2f}s")
-    cfg = api.TrainConfig(arch=wl["arch"], hidden=wl["hidden"], workers=world)
+    cfg = api.TrainConfig(arch=wl["arch"], hidden=wl["hidden"], workers=world,
+                          hbm_cache_budget_bytes=int(args.hbm_cache_gb * 1e9))
     sess = api.TrainSession(graph, cfg, rank=rank, stream=stream)
     W_total, wb, we = sess.windows()
     P = sess.num_params
@@ -308,8 +359,9 @@ def main():
               "pool_reserved_high_gb": round(pool["reserved_high"] / 1e9, 1),
               "graph_store_gb": round(graph.device_bytes() / 1e9, 1),
               "feature_versions": graph.feature_stats(),
-              "cache": {k: st[k] for k in ("hits", "misses", "evictions", "expirations", "spills",
-                                           "refills", "resident_peak_units")}}
+              "cache": {k: st[k] for k in ("hits", "misses", "evictions", "expirations",
+                                           "resident_peak_units")},
+              "cache_tier": {"hbm_budget_gb": args.hbm_cache_gb, **sess.tier_stats()}}
     # the e2e leg builds its own graph + session: release the timed ones first (C4 is ~150 GB)
     del sess, graph
     torch.cuda.synchronize()
@@ -352,11 +404,12 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            v, raw, secs, desc = reference_sample(wl)
-            cpu = {"value": v, "unit": "snapshots/s", "cores": 1, "kind": "reference", "sample": desc}
+            v, same, desc = reference_step(wl, args.workload)
+            cpu = {"value": v, "unit": "snapshots/s", "cores": 1, "kind": "reference", "sample": desc,
+                   "same_config": same, **host_cpu()}
         except Exception as e:  # reference not built on this box
             cpu = {"value": None, "unit": "snapshots/s", "cores": 1, "kind": "reference",
-                   "sample": f"unavailable: {e}"}
+                   "sample": f"unavailable: {e}", **host_cpu()}
 
     if rank == 0:
         line = {
@@ -366,6 +419,7 @@ def main():
             "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.workload, "desc": wl["desc"], "windows": W_total,
+                       "hbm_cache_budget_gb": args.hbm_cache_gb,
                        "seq_len": L, "horizon": H, "nodes": wl["n"],
                        "edges": int(synth.sizes[0]), "snapshots": wl["T"],
                        "parallelism": f"window-shard x{world} (consecutive_block)",

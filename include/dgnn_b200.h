@@ -276,6 +276,10 @@ int dgnn_session_cache_events(dgnn_session* s, int64_t* out, int64_t* n);
 /* Cumulative stats: hits misses evictions expirations invalidations rejected
  * scratch incremental fallbacks spills refills peak_units(as int64). */
 int dgnn_session_stats(dgnn_session* s, int64_t* out12);
+/* Second cache level (HBM <-> pinned host, B200 addition; no reference
+ * counterpart): spills refills prefetches demand_refills spill_bytes
+ * refill_bytes pinned_bytes hbm_resident_bytes. */
+int dgnn_session_tier_stats(dgnn_session* s, int64_t* out8);
 
 /* ------------------------------------------------------- host-side plan logic
  * Pure host functions (no device needed). */

@@ -383,3 +383,59 @@ def adam_step(p, g, m, v, step, lr=0.01, b1=0.9, b2=0.999, eps=1e-8, sgd=False):
     bc1 = 1 - b1 ** step
     bc2 = 1 - b2 ** step
     return p - lr * (m / bc1) / (np.sqrt(v / bc2) + eps), m, v
+
+
+# ------------------------------------------------------------------ large-graph helpers
+# The scale parity tests (1M nodes / 20M edges) need the same restatement at
+# sizes where per-edge Python loops and np.add.at are too slow; these are the
+# same operations in vectorised form (sum / transposed sum only).
+def apply_structural_delta(prev_keys, del_src, del_dst, ins_src, ins_dst):
+    """apply_delta's edge part (src/snapshot.cpp:142-154) on sorted unique
+    (src<<32|dst) keys: (prev \\ deletions) U insertions."""
+    dk = np.unique(edge_keys(del_src, del_dst))
+    ik = np.unique(edge_keys(ins_src, ins_dst))
+    if len(dk):
+        pos = np.searchsorted(prev_keys, dk)
+        ok = pos < len(prev_keys)
+        ok[ok] = prev_keys[pos[ok]] == dk[ok]
+        prev_keys = np.delete(prev_keys, pos[ok])
+    if len(ik):
+        pos = np.searchsorted(prev_keys, ik)
+        present = pos < len(prev_keys)
+        present[present] = prev_keys[pos[present]] == ik[present]
+        prev_keys = np.insert(prev_keys, pos[~present], ik[~present])
+    return prev_keys
+
+
+def in_csr_from_keys(keys, n):
+    """In-CSR (sources ascending per destination) of sorted (src,dst) keys."""
+    s, d = split_keys(keys)
+    rk = np.sort((d.astype(np.int64) << 32) | s.astype(np.int64))
+    in_src = (rk & 0xFFFFFFFF).astype(np.int32)
+    in_ptr = np.zeros(n + 1, np.int64)
+    in_ptr[1:] = np.cumsum(np.bincount((rk >> 32).astype(np.int64), minlength=n))
+    return in_ptr, in_src
+
+
+def out_csr_from_keys(keys, n):
+    s, d = split_keys(keys)
+    out_ptr = np.zeros(n + 1, np.int64)
+    out_ptr[1:] = np.cumsum(np.bincount(s.astype(np.int64), minlength=n))
+    return out_ptr, d
+
+
+def sum_aggregate_sparse(in_ptr, in_src, feats):
+    """aggregate_scratch, sum (src/aggregate.cpp:75-81), as a sparse product
+    in fp64 (summation order differs from the per-row loop by fp64 rounding)."""
+    import scipy.sparse as sp
+    n = len(in_ptr) - 1
+    A = sp.csr_matrix((np.ones(len(in_src)), in_src, in_ptr), shape=(n, feats.shape[0]))
+    return A @ np.asarray(feats, np.float64)
+
+
+def sum_backward_sparse(in_ptr, in_src, upstream):
+    """aggregate_backward, sum (src/aggregate.cpp:221-226): grad = A^T up."""
+    import scipy.sparse as sp
+    n = len(in_ptr) - 1
+    A = sp.csr_matrix((np.ones(len(in_src)), in_src, in_ptr), shape=(n, upstream.shape[0]))
+    return A.T @ np.asarray(upstream, np.float64)

@@ -109,6 +109,7 @@ SIGNATURES = {
     "dgnn_session_invocations": (C.c_int, [P, P, C.POINTER(I64)]),
     "dgnn_session_cache_events": (C.c_int, [P, P, C.POINTER(I64)]),
     "dgnn_session_stats": (C.c_int, [P, P]),
+    "dgnn_session_tier_stats": (C.c_int, [P, P]),
     "dgnn_sliding_windows": (I64, [I32, I32, I32, I32, P, I64]),
     "dgnn_plan": (C.c_int, [I32, I32, I32, I32, I32, P]),
     "dgnn_cache_scores": (C.c_int, [P, C.POINTER(I32), C.POINTER(I32)]),

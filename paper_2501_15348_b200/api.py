@@ -708,6 +708,14 @@ class TrainSession:
                 "resident_peak_units"]
         return dict(zip(keys, out.tolist()))
 
+    def tier_stats(self) -> dict:
+        """Second cache level (HBM <-> pinned host placement) counters."""
+        out = np.empty(8, np.int64)
+        check(lib().dgnn_session_tier_stats(self.h, _np_ptr(out)))
+        keys = ["spills", "refills", "prefetches", "demand_refills", "spill_bytes", "refill_bytes",
+                "pinned_bytes", "hbm_resident_bytes"]
+        return dict(zip(keys, out.tolist()))
+
 
 # ------------------------------------------------------------------ profiling
 PROF_CLASSES = ["agg_scratch", "agg_delta", "agg_backward", "cell_fwd", "cell_bwd",

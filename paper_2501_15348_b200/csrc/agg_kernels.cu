@@ -813,14 +813,28 @@ void agg_delta(int kind, int n_rows, int w, const int32_t* rows, const int32_t* 
                   ent, f_prev, f_curr, values, degree, mean_sums, argext))));
 }
 
+namespace {
+int struct_unroll(int w) {
+  int U = w % 8 == 0 && w >= 32 ? 2 : 1;
+  if (w % 16 == 0 && w >= 64) U = 4;
+  return U;
+}
+}  // namespace
+
+bool agg_delta_struct_supported(int kind, int w, const float* h) {
+  if (kind != kAggSum && kind != kAggMean) return false;
+  // outputs are fresh pool blocks (256 B aligned): only h's alignment varies
+  if (pick_vec(w, h, nullptr) != 4) return false;
+  return w <= 128 * struct_unroll(w);
+}
+
 bool agg_delta_struct(int kind, int n_rows, int w, const int32_t* rows, const int32_t* row_ptr_c,
                       const int32_t* ent_c, int32_t num_nodes, const int32_t* changed,
                       const float* h, float* values, float* degree, float* mean_sums,
                       cudaStream_t stream) {
   if (kind != kAggSum && kind != kAggMean) return false;
   if (pick_vec(w, h, values) != 4 || pick_vec(w, mean_sums, nullptr) != 4) return false;
-  int U = w % 8 == 0 && w >= 32 ? 2 : 1;
-  if (w % 16 == 0 && w >= 64) U = 4;
+  const int U = struct_unroll(w);
   if (w > 128 * U) return false;
   if (n_rows <= 0) return true;
   const int g = pick_group(w, 4 * U);

@@ -40,6 +40,8 @@ void agg_delta(int kind, int n_rows, int w, const int32_t* rows, const int32_t* 
 // edges subtract H[src], added edges add it, persisting edges of
 // feature-changed nodes are skipped. Returns false (nothing launched) when
 // the shape / kind is not supported; the caller then aggregates from scratch.
+// shape / alignment check for agg_delta_struct (callers fall back to scratch)
+bool agg_delta_struct_supported(int kind, int w, const float* h);
 bool agg_delta_struct(int kind, int n_rows, int w, const int32_t* rows, const int32_t* row_ptr_c,
                       const int32_t* ent_c, int32_t num_nodes, const int32_t* changed,
                       const float* h, float* values, float* degree, float* mean_sums,

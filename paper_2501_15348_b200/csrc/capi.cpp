@@ -1128,6 +1128,17 @@ int dgnn_session_stats(dgnn_session* s, int64_t* out12) {
   });
 }
 
+int dgnn_session_tier_stats(dgnn_session* s, int64_t* out8) {
+  return guarded([&] {
+    CacheStore* store = s->worker().store();
+    CacheStats cs = store ? store->stats() : CacheStats{};
+    const int64_t v[8] = {cs.spills, cs.refills, cs.prefetches, cs.demand_refills, cs.spill_bytes,
+                          cs.refill_bytes, store ? store->pinned_bytes() : 0,
+                          store ? store->hbm_resident_bytes() : 0};
+    std::memcpy(out8, v, sizeof(v));
+  });
+}
+
 // ------------------------------------------------------- host-side plan logic
 int64_t dgnn_sliding_windows(int32_t total, int32_t L, int32_t S, int32_t H, int32_t* starts,
                              int64_t cap) {

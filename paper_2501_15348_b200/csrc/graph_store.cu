@@ -314,6 +314,9 @@ struct Cub {
       DGNN_CUDA(cudaMemcpyAsync(out, na ? a : b, sizeof(uint64_t) * (na + nb), cudaMemcpyDeviceToDevice, st));
       return;
     }
+    // DeviceMerge counts in int: refuse rather than truncate
+    if (na + nb > static_cast<int64_t>(INT32_MAX))
+      throw std::invalid_argument("incremental snapshot build supports up to 2^31-1 edges");
     size_t bytes = 0;
     DGNN_CUDA(cub::DeviceMerge::MergeKeys(nullptr, bytes, a, static_cast<int>(na), b,
                                           static_cast<int>(nb), out, ::cuda::std::less<>{}, st));

@@ -337,6 +337,10 @@ std::shared_ptr<AggResult> aggregate_scratch(const GraphView& graph, const float
   return r;
 }
 
+bool rebase_supported(const AggrFn& fn, int32_t dim, const float* feats) {
+  return cuda::agg_delta_struct_supported(kind_i(fn.kind), dim, feats);
+}
+
 std::shared_ptr<AggResult> aggregate_rebase(const AggResult& base, const GraphView& graph,
                                             const float* feats, int32_t dim, const DevDelta& delta,
                                             const AggrFn& fn, cudaStream_t stream) {

@@ -104,6 +104,9 @@ std::shared_ptr<AggResult> aggregate_scratch(const GraphView& graph, const float
 // plus the structural part of delta t (removed edges subtract H[src], added
 // edges add it). Same values as aggregate_scratch(graph, H) up to fp32
 // summation order. Sum / mean only; graph must be the full snapshot t.
+// Whether aggregate_rebase handles (fn, dim, feats); otherwise aggregate from
+// scratch.
+bool rebase_supported(const AggrFn& fn, int32_t dim, const float* feats);
 std::shared_ptr<AggResult> aggregate_rebase(const AggResult& base, const GraphView& graph,
                                             const float* feats, int32_t dim, const DevDelta& delta,
                                             const AggrFn& fn, cudaStream_t stream);

@@ -832,12 +832,17 @@ void Lanes::dep(cudaStream_t from, cudaStream_t to) {
 
 ForwardArtifacts model_forward(DgnnModel& model, const SeqSample& sample, AggProvider& provider,
                                Lanes& lanes) {
-  if (is_stacked(model.cfg_.arch)) return stacked_forward(model, sample, provider);
+  if (is_stacked(model.cfg_.arch)) {
+    provider.begin_forward(false);
+    ForwardArtifacts out = stacked_forward(model, sample, provider);
+    provider.end_forward();
+    return out;
+  }
   cudaStream_t prev = provider.stream();
   provider.set_stream(lanes.main());
-  provider.clear_hidden_bases();
+  provider.begin_forward(true);
   ForwardArtifacts out = seq2seq_forward(model, sample, provider, lanes);
-  provider.clear_hidden_bases();
+  provider.end_forward();
   provider.set_stream(prev);
   return out;
 }

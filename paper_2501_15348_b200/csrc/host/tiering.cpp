@@ -1,0 +1,193 @@
+// HBM <-> pinned-host placement of cached aggregations (see tiering.hpp).
+#include "tiering.hpp"
+
+#include <utility>
+
+namespace dgnn {
+
+// ---------------------------------------------------------------- PinnedPool
+PinnedPool::~PinnedPool() {
+  for (void* p : all_) cudaFreeHost(p);
+}
+
+void* PinnedPool::take(size_t bytes) {
+  auto it = free_.find(bytes);
+  if (it != free_.end() && !it->second.empty()) {
+    void* p = it->second.back();
+    it->second.pop_back();
+    return p;
+  }
+  void* p = nullptr;
+  DGNN_CUDA(cudaHostAlloc(&p, bytes, cudaHostAllocPortable));
+  all_.push_back(p);
+  reserved_ += static_cast<int64_t>(bytes);
+  return p;
+}
+
+void PinnedPool::give(void* p, size_t bytes) {
+  if (p) free_[bytes].push_back(p);
+}
+
+// ---------------------------------------------------------------- HbmTier
+namespace {
+
+// The payload's device arrays in one fixed order; the host block is their
+// concatenation. Sizes follow from (kind, rows, dim), so a refill re-creates
+// exactly the arrays alloc_result made.
+template <typename F, typename I>
+void each_array(AggResult& r, F&& on_float, I&& on_int) {
+  on_float(r.values);
+  on_float(r.degree);
+  on_float(r.mean_sums);
+  on_float(r.dense);
+  on_int(r.argext);
+}
+
+struct Shape {
+  size_t values = 0, degree = 0, mean_sums = 0, dense = 0, argext = 0;
+  size_t bytes() const { return 4 * (values + degree + mean_sums + dense + argext); }
+};
+
+Shape shape_of(const AggResult& r) {
+  Shape s;
+  const size_t nw = static_cast<size_t>(r.rows) * r.dim;
+  s.values = nw;
+  if (r.kind == AggrKind::kMean) {
+    s.degree = static_cast<size_t>(r.rows);
+    s.mean_sums = nw;
+  }
+  if (r.extremal()) {
+    s.dense = nw;
+    s.argext = nw;
+  }
+  return s;
+}
+
+}  // namespace
+
+HbmTier::HbmTier(int64_t budget_bytes, cudaStream_t compute) : budget_(budget_bytes), compute_(compute) {
+  DGNN_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
+}
+
+HbmTier::~HbmTier() {
+  if (copy_) cudaStreamSynchronize(copy_);
+  reap(true);
+  for (cudaEvent_t e : events_) cudaEventDestroy(e);
+  if (copy_) cudaStreamDestroy(copy_);
+}
+
+cudaEvent_t HbmTier::take_event() {
+  if (!events_.empty()) {
+    cudaEvent_t e = events_.back();
+    events_.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  DGNN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return e;
+}
+
+int64_t HbmTier::device_bytes(const AggResult& r) {
+  return static_cast<int64_t>(shape_of(r).bytes());
+}
+
+void HbmTier::spill(AggResult& r, Placement& p) {
+  const Shape s = shape_of(r);
+  p.host_bytes = s.bytes();
+  p.host = pool_.take(p.host_bytes);
+  // the copy starts after everything the compute stream has queued so far
+  // (the payload's producer and every reader issued before the spill)
+  cudaEvent_t produced = take_event();
+  DGNN_CUDA(cudaEventRecord(produced, compute_));
+  DGNN_CUDA(cudaStreamWaitEvent(copy_, produced, 0));
+  give_event(produced);
+  Retiring ret;
+  ret.done = take_event();
+  char* dst = static_cast<char*>(p.host);
+  auto out = [&](auto& arr, auto& keep) {
+    if (arr.size() == 0) return;
+    DGNN_CUDA(cudaMemcpyAsync(dst, arr.get(), arr.bytes(), cudaMemcpyDeviceToHost, copy_));
+    dst += arr.bytes();
+    keep.push_back(std::move(arr));
+  };
+  each_array(r, [&](cuda::DevArray<float>& a) { out(a, ret.f); },
+             [&](cuda::DevArray<int32_t>& a) { out(a, ret.i); });
+  DGNN_CUDA(cudaEventRecord(ret.done, copy_));
+  retiring_.push_back(std::move(ret));
+  p.where = Placement::Where::kHost;
+  ++stats_.spills;
+  stats_.spill_bytes += static_cast<int64_t>(p.host_bytes);
+}
+
+void HbmTier::fetch(AggResult& r, Placement& p, bool ahead) {
+  const Shape s = shape_of(r);
+  // device arrays come from the compute stream's allocator; the copy stream
+  // writes them only after the compute stream has reached this point
+  r.values = cuda::DevArray<float>(s.values, compute_);
+  r.degree = cuda::DevArray<float>(s.degree, compute_);
+  r.mean_sums = cuda::DevArray<float>(s.mean_sums, compute_);
+  r.dense = cuda::DevArray<float>(s.dense, compute_);
+  r.argext = cuda::DevArray<int32_t>(s.argext, compute_);
+  cudaEvent_t allocated = take_event();
+  DGNN_CUDA(cudaEventRecord(allocated, compute_));
+  DGNN_CUDA(cudaStreamWaitEvent(copy_, allocated, 0));
+  give_event(allocated);
+  const char* src = static_cast<const char*>(p.host);
+  auto in = [&](auto& arr) {
+    if (arr.size() == 0) return;
+    DGNN_CUDA(cudaMemcpyAsync(arr.get(), src, arr.bytes(), cudaMemcpyHostToDevice, copy_));
+    src += arr.bytes();
+  };
+  each_array(r, in, in);
+  p.inbound = take_event();
+  DGNN_CUDA(cudaEventRecord(p.inbound, copy_));
+  // later spills into this block are issued on the same copy stream, after
+  // this read of it
+  pool_.give(p.host, p.host_bytes);
+  p.host = nullptr;
+  p.where = Placement::Where::kInbound;
+  ++stats_.refills;
+  ++(ahead ? stats_.prefetches : stats_.demand_refills);
+  stats_.refill_bytes += static_cast<int64_t>(p.host_bytes);
+}
+
+void HbmTier::settle(Placement& p) {
+  if (p.where != Placement::Where::kInbound) return;
+  DGNN_CUDA(cudaStreamWaitEvent(compute_, p.inbound, 0));
+  give_event(p.inbound);
+  p.inbound = nullptr;
+  p.where = Placement::Where::kHbm;
+}
+
+void HbmTier::drop(AggResult& r, Placement& p) {
+  (void)r;
+  if (p.where == Placement::Where::kHost) {
+    pool_.give(p.host, p.host_bytes);
+    p.host = nullptr;
+  } else if (p.where == Placement::Where::kInbound) {
+    // the arrays are released in compute-stream order: order that after the
+    // copy that fills them
+    settle(p);
+  }
+  p.where = Placement::Where::kHbm;
+}
+
+void HbmTier::reap(bool wait) {
+  size_t keep = 0;
+  for (size_t k = 0; k < retiring_.size(); ++k) {
+    Retiring& r = retiring_[k];
+    const cudaError_t q = wait ? cudaEventSynchronize(r.done) : cudaEventQuery(r.done);
+    if (q == cudaSuccess) {
+      give_event(r.done);
+      r.f.clear();  // back to the compute stream's free lists
+      r.i.clear();
+      continue;
+    }
+    if (q != cudaErrorNotReady) DGNN_CUDA(q);
+    if (keep != k) retiring_[keep] = std::move(r);
+    ++keep;
+  }
+  retiring_.resize(keep);
+}
+
+}  // namespace dgnn

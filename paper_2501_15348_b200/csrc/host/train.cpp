@@ -64,9 +64,8 @@ Worker::Worker(const DeviceGraph& graph, DgnnModel& model, const TrainConfig& cf
     const double capacity = cfg.cache_capacity_frac * cache_data_size_units(graph, model.cfg_);
     store_ = std::make_unique<CacheStore>(*cfg.cache_policy, capacity);
     if (cfg.hbm_cache_budget_bytes > 0) {
-      cudaStream_t copy;
-      DGNN_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
-      store_->set_hbm_budget(cfg.hbm_cache_budget_bytes, stream, copy);
+      store_->set_hbm_budget(cfg.hbm_cache_budget_bytes, stream,
+                             model.cfg_.seq_len + model.cfg_.horizon);
     }
   }
   IncrementalOptions inc{cfg.fallback_threshold, cfg.rescratch_period};
@@ -119,6 +118,8 @@ void Worker::run_sample(const SequenceWindow& window, Timestep windows_remaining
     model_backward(model_, sample, fwd, dpred, grad, lanes);
     prof_add_host(kProfHostBwd, since(h2));
   }
+  // the sample's tape has released its aggregations: re-apply the HBM budget
+  if (store_) store_->rebalance();
   prof_add_host(kProfSampleHost, since(h0));
 }
 

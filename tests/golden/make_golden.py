@@ -85,8 +85,8 @@ def cell_fixture(out):
 
 def smoke_fixture():
     # the exact case __graft_entry__.smoke() runs
-    g = R.RefGraph.synth(300, 4, 8, 12, 0.05, 0.02, seed=1)
-    loss, pred0, grads = g.sample_grads(R.RunCfg(arch="gcrn_m2", hidden=16), 0)
+    g = R.RefGraph.synth(300, 4, 32, 12, 0.05, 0.02, seed=1)
+    loss, pred0, grads = g.sample_grads(R.RunCfg(arch="gcrn_m2", hidden=64), 0)
     np.savez_compressed(os.path.join(HERE, "smoke_gcrn_m2.npz"), loss=np.float64(loss), pred0=pred0,
                         grads=grads)
 

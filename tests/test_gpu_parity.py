@@ -422,3 +422,17 @@ print("ok")
         r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
                            timeout=300)
         assert r.returncode == 0 and "ok" in r.stdout, (s, r.stdout[-2000:], r.stderr[-2000:])
+
+
+@pytest.mark.parametrize("hidden", [10, 30])
+def test_sample_grads_hidden_without_rebase_shape(ref, api, pair, hidden):
+    """Hidden sizes the structural-rebase kernel does not take (hidden % 4 != 0):
+    the hidden aggregation falls back to scratch instead of failing."""
+    g_ref, g = pair
+    cfg_r = ref.RunCfg(arch="gcrn_m2", hidden=hidden)
+    s = api.TrainSession(g, api.TrainConfig(arch="gcrn_m2", hidden=hidden))
+    for w in (0, 1):
+        loss_r, pred_r, grads_r = g_ref.sample_grads(cfg_r, w)
+        loss, pred, grads = s.sample_grads(w)
+        assert abs(loss - loss_r) <= 1e-5 * abs(loss_r), (loss, loss_r)
+        assert nrel(grads, grads_r) < 1e-4

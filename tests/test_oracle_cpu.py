@@ -263,3 +263,34 @@ def test_product_raises_reference_errors_without_gpu():
         api.Synth(10, 0.5, 2, 3, 0.1, 0.0)
     with pytest.raises(ValueError, match="sliding_windows: L must be >= 1"):
         api.sliding_windows(10, 0, 1, 1)
+
+
+def test_large_graph_helpers_match_restatement():
+    """The vectorised helpers the scale tests use (apply_structural_delta,
+    in/out CSR from keys, sparse sum / transposed sum) equal the per-edge
+    restatement (build_csr, apply_delta, aggregate_scratch, aggregate_backward)."""
+    rng = np.random.default_rng(21)
+    n = 400
+    keys = np.unique(O.edge_keys(rng.integers(0, n, 3000), rng.integers(0, n, 3000)))
+    feats = rng.uniform(-1, 1, (n, 6))
+    for _ in range(5):
+        dk = rng.choice(keys, 200, replace=False)
+        ik = np.setdiff1d(np.unique(O.edge_keys(rng.integers(0, n, 300), rng.integers(0, n, 300))), keys)
+        ds, dd = O.split_keys(dk)
+        is_, id_ = O.split_keys(ik)
+        want, _ = O.apply_delta(keys, feats, {"del_src": ds, "del_dst": dd, "ins_src": is_,
+                                              "ins_dst": id_, "changed": np.zeros(0, np.int64),
+                                              "changed_feats": np.zeros((0, 6))})
+        keys = O.apply_structural_delta(keys, ds, dd, is_, id_)
+        assert np.array_equal(keys, want)
+    s, d = O.split_keys(keys)
+    csr = O.build_csr(s, d, n)
+    ip, isrc = O.in_csr_from_keys(keys, n)
+    assert np.array_equal(ip, csr["in_ptr"]) and np.array_equal(isrc, csr["in_src"])
+    op, od = O.out_csr_from_keys(keys, n)
+    assert np.array_equal(op, csr["out_ptr"]) and np.array_equal(od, csr["out_dst"])
+    agg = O.aggregate_scratch(ip, isrc, feats, "sum")["values"]
+    assert np.allclose(O.sum_aggregate_sparse(ip, isrc, feats), agg, rtol=1e-12, atol=1e-12)
+    up = rng.standard_normal((n, 6))
+    assert np.allclose(O.sum_backward_sparse(ip, isrc, up), O.aggregate_backward(ip, isrc, up, "sum"),
+                       rtol=1e-12, atol=1e-12)
