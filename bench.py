@@ -236,10 +236,6 @@ def main():
         if world > 1:
             dist.barrier()
 
-    def allreduce(t):
-        if world > 1:
-            dist.all_reduce(t)
-
     t0 = time.perf_counter()
     synth = api.Synth(wl["n"], wl["deg"], wl["dim"], wl["T"], wl["edge"], wl["feat"], seed=1)
     t_synth = time.perf_counter() - t0
@@ -252,13 +248,13 @@ def main():
                           hbm_cache_budget_bytes=int(args.hbm_cache_gb * 1e9))
     sess = api.TrainSession(graph, cfg, rank=rank, stream=stream)
     W_total, wb, we = sess.windows()
-    P = sess.num_params
-    grad = torch.empty(P, device="cuda")
 
-    from paper_2501_15348_b200.sharding import run_sharded_epoch
+    # the gradient all-reduce runs inside the library (NCCL communicator of
+    # the C ABI; the id is exchanged over torch.distributed)
+    comm = api.comm_from_torch(world, rank)
 
     def epoch():
-        run_sharded_epoch(sess, grad, allreduce if world > 1 else None)
+        sess.run_dist_epoch(comm)
 
     for _ in range(args.warmup):
         epoch()
@@ -383,7 +379,7 @@ def main():
         for _ in range(e_steps):
             g2 = synth.to_graph(stream)          # H2D of the compact graph + device build
             s2 = api.TrainSession(g2, cfg, rank=rank, stream=stream)
-            run_sharded_epoch(s2, grad, allreduce if world > 1 else None)  # + D2H of window losses
+            s2.run_dist_epoch(comm)  # + D2H of window losses
             d2h = 8 * len(s2.losses())
             del s2, g2
         ev3.record(stream)

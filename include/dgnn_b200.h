@@ -2,7 +2,7 @@
  * dgnn_b200.h — C ABI of the B200-native ReInc dynamic-GNN training hot path.
  *
  * This is the drop-in boundary. The reference is a C++
- * library (proj/include/dgnn/*.hpp) with no FFI of its own; every entry point
+ * library (proj/include/dgnn/ headers) with no FFI of its own; every entry point
  * below names the reference interface it replaces (file:line into
  * /root/reference/proj). Plain pointers and sizes only: device pointers are
  * fp32 / int32 / int64 HBM buffers, `stream` is a cudaStream_t (NULL = the
@@ -33,12 +33,15 @@ typedef struct dgnn_session dgnn_session;
 typedef struct dgnn_dataset dgnn_dataset;
 typedef struct dgnn_cg dgnn_cg;
 typedef struct dgnn_cg_update dgnn_cg_update;
+typedef struct dgnn_comm dgnn_comm;
 
 const char* dgnn_last_error(void);
 const char* dgnn_version(void);
 /* Number of this library's kernels launched so far (process-wide). */
 int64_t dgnn_launch_count(void);
 int dgnn_synchronize(void* stream);
+/* cudaSetDevice for callers without their own CUDA runtime (one GPU per process). */
+int dgnn_set_device(int32_t device);
 
 /* ------------------------------------------------------------------ graph
  * Replaces dgnn::DynamicGraph / Snapshot / DeltaGraph / extract_delta /
@@ -262,6 +265,22 @@ int dgnn_session_begin_epoch(dgnn_session* s, int64_t* num_batches);
 int dgnn_session_local_grads(dgnn_session* s, int64_t batch, float* grad_sum);
 int dgnn_session_apply(dgnn_session* s, const float* grad_sum, int32_t* applied);
 int dgnn_session_end_epoch(dgnn_session* s);
+/* The gradient all-reduce of the sharded trainer (allreduce_sim,
+ * inc/distsim.hpp:75 / src/distsim.cpp:248-260) over NCCL: one communicator
+ * per rank (NVLink / NVSwitch inside a box). Rank 0 calls dgnn_comm_unique_id
+ * and hands the 128 bytes to every rank (file, socket, MPI, ...); each rank
+ * then calls dgnn_comm_create with its cudaSetDevice already done. */
+int dgnn_comm_unique_id(uint8_t* out128);
+int dgnn_comm_create(const uint8_t* id128, int32_t world, int32_t rank, dgnn_comm** out);
+void dgnn_comm_free(dgnn_comm* c);
+/* In-place fp32 sum over ranks of n values (device pointer), stream-ordered. */
+int dgnn_grad_allreduce(dgnn_comm* c, float* data, int64_t n, void* stream);
+/* One whole sharded epoch natively (run_distributed_epoch, inc/distsim.hpp:
+ * 104-108, src/distsim.cpp:197-272): per batch this rank's window-gradient
+ * sum, dgnn_grad_allreduce, the identical optimizer step on every rank.
+ * comm may be NULL when cfg.workers == 1. report->seconds is device-timed,
+ * max over ranks; sample losses via dgnn_session_losses. */
+int dgnn_session_run_dist_epoch(dgnn_session* s, dgnn_comm* comm, dgnn_epoch_report* report);
 /* Sample losses of the last epoch (visit order). */
 int dgnn_session_losses(dgnn_session* s, double* out, int64_t* n);
 /* One sample's forward + backward at the current parameters with a fresh

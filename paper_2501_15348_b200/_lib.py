@@ -104,6 +104,12 @@ SIGNATURES = {
     "dgnn_session_local_grads": (C.c_int, [P, I64, P]),
     "dgnn_session_apply": (C.c_int, [P, P, C.POINTER(I32)]),
     "dgnn_session_end_epoch": (C.c_int, [P]),
+    "dgnn_set_device": (C.c_int, [I32]),
+    "dgnn_comm_unique_id": (C.c_int, [P]),
+    "dgnn_comm_create": (C.c_int, [P, I32, I32, C.POINTER(P)]),
+    "dgnn_comm_free": (None, [P]),
+    "dgnn_grad_allreduce": (C.c_int, [P, P, I64, P]),
+    "dgnn_session_run_dist_epoch": (C.c_int, [P, P, C.POINTER(EpochReport)]),
     "dgnn_session_losses": (C.c_int, [P, P, C.POINTER(I64)]),
     "dgnn_session_sample_grads": (C.c_int, [P, I32, C.POINTER(D), P, P]),
     "dgnn_session_invocations": (C.c_int, [P, P, C.POINTER(I64)]),

@@ -600,6 +600,49 @@ class TrainConfig:
         return c
 
 
+class Comm:
+    """The sharded trainer's gradient all-reduce (NCCL, in the library).
+    `Comm.unique_id()` on rank 0, the 128 bytes shared with every rank by the
+    caller, then `Comm(uid, world, rank)` on each (device already selected)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(lib().dgnn_comm_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, uid: bytes, world: int, rank: int):
+        assert len(uid) == 128
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        check(lib().dgnn_comm_create(buf, world, rank, C.byref(h)))
+        self.h, self.world, self.rank = h, world, rank
+
+    def allreduce(self, t, stream=None):
+        """In-place fp32 sum over ranks of a CUDA tensor."""
+        if stream is None:
+            stream = current_stream()
+        check(lib().dgnn_grad_allreduce(self.h, _ptr(t), t.numel(), _stream_handle(stream)))
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None and _lib._lib is not None:
+            lib().dgnn_comm_free(self.h)
+            self.h = None
+
+
+def comm_from_torch(world: int, rank: int) -> "Comm | None":
+    """Build the library's communicator, exchanging the NCCL id over the
+    default torch.distributed group (None for one rank)."""
+    if world <= 1:
+        return None
+    import torch
+    import torch.distributed as dist
+    uid = Comm.unique_id() if rank == 0 else bytes(128)
+    t = torch.tensor(list(uid), dtype=torch.uint8, device="cuda")
+    dist.broadcast(t, 0)
+    return Comm(bytes(t.cpu().tolist()), world, rank)
+
+
 class TrainSession:
     """TrainSession / DistSession rank over a device graph (ref inc/train.hpp:92-114,
     inc/distsim.hpp:82-102). workers == 0: seq-first; workers >= 1: rank `rank` of
@@ -662,6 +705,16 @@ class TrainSession:
 
     def end_epoch(self):
         check(lib().dgnn_session_end_epoch(self.h))
+
+    def run_dist_epoch(self, comm: "Comm | None" = None) -> dict:
+        """One whole sharded epoch in the library (NCCL all-reduce through
+        `comm`; None for a single rank). seconds = device time, max over ranks."""
+        r = _lib.EpochReport()
+        check(lib().dgnn_session_run_dist_epoch(self.h, comm.h if comm is not None else None,
+                                                C.byref(r)))
+        out = {k: getattr(r, k) for k, _ in _lib.EpochReport._fields_}
+        out["sample_losses"] = self.losses()
+        return out
 
     def run_sharded_epoch(self, allreduce=None) -> list[float]:
         """One distsim epoch on this rank; `allreduce(tensor)` sums over ranks."""

@@ -528,11 +528,16 @@ __global__ void k_deleted_contributor(int64_t n_del, int w, const uint64_t* __re
 
 // ---------------------------------------------------------------- K3 backward
 // grad[u] = sum_{v in out(u), ascending} s_v * up[v]; s_v = 1 (sum), 1/deg(v) (mean).
-template <int V, int G, bool MEAN>
+// EXT (max / min): element (v, c) contributes only where argext[v][c] == u —
+// the reference's scatter to the recorded contributor (ref src/aggregate.cpp:
+// 234-243, v ascending) restated as a pull, so the sum order per element is
+// the reference's and the result is deterministic (no atomics).
+template <int V, int G, bool MEAN, bool EXT = false>
 __global__ void __launch_bounds__(kThreads)
 k_agg_backward(int n, int w, int c0, int wc, const int64_t* __restrict__ ptr,
                const int32_t* __restrict__ idx, const float* __restrict__ up,
-               const float* __restrict__ degree, float* grad, const float* addend) {
+               const float* __restrict__ degree, float* grad, const float* addend,
+               const int32_t* __restrict__ argext = nullptr) {
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
   constexpr int kRowsPerWarp = 32 / G;
@@ -569,14 +574,28 @@ k_agg_backward(int n, int w, int c0, int wc, const int64_t* __restrict__ ptr,
           for (int q = 0; q < kUnroll; ++q) {
             const int32_t vv = __shfl_sync(0xffffffffu, my_v, (j0 + q) & (G - 1), G);
             sc[q] = MEAN ? __shfl_sync(0xffffffffu, my_s, (j0 + q) & (G - 1), G) : 1.f;
-            if (cact && j0 + q < cnt && eb + j0 + q < deg)
+            if (cact && j0 + q < cnt && eb + j0 + q < deg) {
               VecLoad<V>::ld(x[q], up + static_cast<int64_t>(vv) * w + c);
+              if (EXT) {
+                float a[V];
+                VecLoad<V>::ld(a, reinterpret_cast<const float*>(argext + static_cast<int64_t>(vv) * w + c));
+#pragma unroll
+                for (int i = 0; i < V; ++i)
+                  if (__float_as_int(a[i]) != static_cast<int32_t>(u)) x[q][i] = 0.f;
+              }
+            }
           }
 #pragma unroll
           for (int q = 0; q < kUnroll; ++q) {
             if (cact && j0 + q < cnt && eb + j0 + q < deg) {
 #pragma unroll
-              for (int i = 0; i < V; ++i) acc[i] += MEAN ? sc[q] * x[q][i] : x[q][i];
+              for (int i = 0; i < V; ++i) {
+                if (EXT) {
+                  if (__float_as_int(x[q][i]) != 0) acc[i] += x[q][i];  // skip non-contributors exactly
+                } else {
+                  acc[i] += MEAN ? sc[q] * x[q][i] : x[q][i];
+                }
+              }
             }
           }
         }
@@ -586,18 +605,6 @@ k_agg_backward(int n, int w, int c0, int wc, const int64_t* __restrict__ ptr,
   }
 }
 
-// max/min backward: route upstream to the recorded contributor.
-__global__ void k_agg_backward_ext(int64_t total, int w, const float* __restrict__ up,
-                                   const int32_t* __restrict__ argext, float* __restrict__ grad) {
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int32_t u = argext[i];
-    if (u >= 0) {
-      const int d = static_cast<int>(i % w);
-      atomicAdd(grad + static_cast<int64_t>(u) * w + d, up[i]);
-    }
-  }
-}
 
 __global__ void k_mask_empty(int64_t total, int w, const int32_t* __restrict__ argext,
                              const float* __restrict__ in, float* __restrict__ out) {
@@ -867,18 +874,6 @@ void agg_backward(int kind, int n, int w, const int64_t* out_ptr, const int32_t*
                   const float* up, const float* degree, const int32_t* argext, float* grad,
                   cudaStream_t stream, const float* addend) {
   if (n <= 0 || w <= 0) return;
-  if (kind == kAggMax || kind == kAggMin) {
-    if (addend == nullptr) {
-      DGNN_CUDA(cudaMemsetAsync(grad, 0, sizeof(float) * static_cast<size_t>(n) * w, stream));
-    } else if (addend != grad) {
-      DGNN_CUDA(cudaMemcpyAsync(grad, addend, sizeof(float) * static_cast<size_t>(n) * w,
-                                cudaMemcpyDeviceToDevice, stream));
-    }
-    const int64_t total = static_cast<int64_t>(n) * w;
-    DGNN_LAUNCH(k_agg_backward_ext, wave_grid(total, 256, 8), 256, 0, stream, total, w, up, argext,
-                grad);
-    return;
-  }
   const int vec = std::min(pick_vec(w, up, grad), pick_vec(w, addend, nullptr));
   if (kind == kAggSum && vec == 4 && std::getenv("DGNN_SPMM_L2_MB") == nullptr &&
       std::getenv("DGNN_SPMM_SLICES") == nullptr) {
@@ -895,6 +890,10 @@ void agg_backward(int kind, int n, int w, const int64_t* out_ptr, const int32_t*
       DGNN_DISPATCH_V(vec, DGNN_DISPATCH_G(g,
           DGNN_LAUNCH((k_agg_backward<V, G, true>), grid, kThreads, 0, stream, n, w, c0, wc,
                       out_ptr, out_dst, up, degree, grad, addend)));
+    } else if (kind == kAggMax || kind == kAggMin) {
+      DGNN_DISPATCH_V(vec, DGNN_DISPATCH_G(g,
+          DGNN_LAUNCH((k_agg_backward<V, G, false, true>), grid, kThreads, 0, stream, n, w, c0, wc,
+                      out_ptr, out_dst, up, degree, grad, addend, argext)));
     } else {
       DGNN_DISPATCH_V(vec, DGNN_DISPATCH_G(g,
           DGNN_LAUNCH((k_agg_backward<V, G, false>), grid, kThreads, 0, stream, n, w, c0, wc,

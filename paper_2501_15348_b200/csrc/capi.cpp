@@ -162,6 +162,10 @@ int dgnn_synchronize(void* stream) {
   return guarded([&] { DGNN_CUDA(cudaStreamSynchronize(as_stream(stream))); });
 }
 
+int dgnn_set_device(int32_t device) {
+  return guarded([&] { DGNN_CUDA(cudaSetDevice(device)); });
+}
+
 // ------------------------------------------------------------------ graph
 int dgnn_graph_create(int32_t num_nodes, int32_t feature_dim, void* stream, dgnn_graph** out) {
   return guarded([&] {
@@ -834,7 +838,7 @@ int dgnn_cell_backward(int32_t lstm, int32_t n, int32_t in, int32_t H, const flo
     cuda::DevArray<float> G(static_cast<size_t>(n) * 4 * H, st), WT(static_cast<size_t>(K) * 4 * H, st);
     cuda::DevArray<float> dW(static_cast<size_t>(K) * 4 * H, st), db(4 * H, st);
     const bool tc = cuda::umma_cell_supported(in, H);
-    cuda::DevArray<float> ws(tc ? cuda::umma_wgrad_workspace(in, H) : cuda::gemm_tn_workspace(n, K, 4 * H), st);
+    cuda::DevArray<float> ws(tc ? cuda::umma_wgrad_workspace(n, in, H) : cuda::gemm_tn_workspace(n, K, 4 * H), st);
     dW.zero(st);
     db.zero(st);
     cuda::transpose(K, 4 * H, W, WT.get(), st);
@@ -1020,6 +1024,62 @@ int dgnn_session_run_epoch(dgnn_session* s, dgnn_epoch_report* report) {
       report->skipped_steps = r.skipped_steps;
       report->spills = r.cache.spills;
       report->refills = r.cache.refills;
+    }
+  });
+}
+
+// ------------------------------------------------------- gradient all-reduce
+struct dgnn_comm {
+  std::unique_ptr<NcclComm> c;
+};
+
+int dgnn_comm_unique_id(uint8_t* out) {
+  return guarded([&] { NcclComm::unique_id(out); });
+}
+
+int dgnn_comm_create(const uint8_t* id, int32_t world, int32_t rank, dgnn_comm** out) {
+  return guarded([&] {
+    auto c = std::make_unique<dgnn_comm>();
+    c->c = std::make_unique<NcclComm>(id, world, rank);
+    *out = c.release();
+  });
+}
+
+void dgnn_comm_free(dgnn_comm* c) { delete c; }
+
+int dgnn_grad_allreduce(dgnn_comm* c, float* data, int64_t n, void* stream) {
+  return guarded([&] { c->c->allreduce_sum(data, n, static_cast<cudaStream_t>(stream)); });
+}
+
+int dgnn_session_run_dist_epoch(dgnn_session* s, dgnn_comm* comm, dgnn_epoch_report* report) {
+  return guarded([&] {
+    check(s->dist != nullptr, "sharded epochs need workers >= 1");
+    check(comm != nullptr || s->cfg.workers <= 1, "a sharded epoch over several ranks needs a comm");
+    if (comm) check(comm->c->world() == s->cfg.workers, "comm size differs from cfg.workers");
+    const DistWorker::EpochResult r = s->dist->run_epoch(comm ? comm->c.get() : nullptr);
+    s->losses = s->dist->take_losses();
+    if (report) {
+      std::memset(report, 0, sizeof(*report));
+      double sum = 0.0;
+      for (double v : s->losses) sum += v;
+      report->loss = s->losses.empty() ? 0.0 : sum / static_cast<double>(s->losses.size());
+      report->seconds = r.seconds;
+      report->samples = static_cast<int64_t>(s->losses.size());
+      CacheStore* store = s->worker().store();
+      const CacheStats cs = store ? store->stats() : CacheStats{};
+      const ExecutionStats& es = s->worker().provider().stats();
+      report->hits = cs.hits;
+      report->misses = cs.misses;
+      report->evictions = cs.evictions;
+      report->expirations = cs.expirations;
+      report->invalidations = cs.invalidations;
+      report->rejected = cs.rejected;
+      report->scratch_calls = es.scratch_calls;
+      report->incremental_calls = es.incremental_calls;
+      report->fallbacks = es.fallbacks;
+      report->skipped_steps = r.skipped;
+      report->spills = cs.spills;
+      report->refills = cs.refills;
     }
   });
 }

@@ -140,6 +140,17 @@ __global__ void k_composite(int64_t n, const uint64_t* __restrict__ keys, uint64
   }
 }
 
+// source-grouped twin of k_composite: source, then deletions before
+// insertions, then destination
+__global__ void k_composite_t(int64_t n, const uint64_t* __restrict__ keys, uint64_t is_ins,
+                              uint64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t s = keys[i] >> 32, d = keys[i] & 0xffffffffu;
+    out[i] = (s << 33) | (is_ins << 32) | d;
+  }
+}
+
 __global__ void k_split_composite(int64_t n, const uint64_t* __restrict__ comp,
                                   int32_t* __restrict__ dsts, int32_t* __restrict__ ent) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -848,6 +859,37 @@ void DeviceGraph::build_delta(int32_t t, const float* prev_feats, const float* f
     if (dd.n_ent_c)
       DGNN_CUDA(cudaMemcpyAsync(dd.ent_c.get(), tmp.get(), sizeof(int32_t) * dd.n_ent_c,
                                 cudaMemcpyDeviceToDevice, st));
+  }
+  // source-grouped structural delta (DevDelta::rows_t)
+  {
+    DevArray<uint8_t> keep_d(dd.n_del, st), keep_i(dd.n_ins, st);
+    DevArray<uint64_t> rem(dd.n_del, st), add(dd.n_ins, st);
+    if (dd.n_del)
+      DGNN_LAUNCH(k_mark, grid_for(dd.n_del), kT, 0, st, dd.n_del, dd.del.get(), dd.n_ins,
+                  dd.ins.get(), 0, keep_d.get());
+    if (dd.n_ins)
+      DGNN_LAUNCH(k_mark, grid_for(dd.n_ins), kT, 0, st, dd.n_ins, dd.ins.get(), dd.n_del,
+                  dd.del.get(), 0, keep_i.get());
+    const int64_t nr_ = cub.select_flagged(dd.del.get(), keep_d.get(), rem.get(), dd.n_del);
+    const int64_t na_ = cub.select_flagged(dd.ins.get(), keep_i.get(), add.get(), dd.n_ins);
+    const int64_t nt = nr_ + na_;
+    dd.n_ent_t = nt;
+    DevArray<uint64_t> ct(nt, st), ct_sorted(nt, st);
+    if (nr_) DGNN_LAUNCH(k_composite_t, grid_for(nr_), kT, 0, st, nr_, rem.get(), 0ull, ct.get());
+    if (na_) DGNN_LAUNCH(k_composite_t, grid_for(na_), kT, 0, st, na_, add.get(), 1ull, ct.get() + nr_);
+    cub.sort(ct.get(), ct_sorted.get(), nt);
+    DevArray<int32_t> srcs(nt, st), uq(nt, st), cn(nt + 1, st);
+    dd.ent_t = DevArray<int32_t>(nt, st);
+    if (nt) DGNN_LAUNCH(k_split_composite, grid_for(nt), kT, 0, st, nt, ct_sorted.get(), srcs.get(), dd.ent_t.get());
+    const int64_t nrt = cub.rle(srcs.get(), uq.get(), cn.get(), nt);
+    dd.n_rows_t = static_cast<int32_t>(nrt);
+    dd.rows_t = DevArray<int32_t>(nrt, st);
+    dd.row_ptr_t = DevArray<int32_t>(nrt + 1, st);
+    if (nrt) {
+      DGNN_CUDA(cudaMemcpyAsync(dd.rows_t.get(), uq.get(), sizeof(int32_t) * nrt, cudaMemcpyDeviceToDevice, st));
+      DGNN_CUDA(cudaMemsetAsync(cn.get() + nrt, 0, sizeof(int32_t), st));
+    }
+    cub.exclusive_sum(cn.get(), dd.row_ptr_t.get(), nrt + 1);
   }
   DGNN_CUDA(cudaStreamSynchronize(st));
   deltas_[t] = std::move(dd);

@@ -87,6 +87,15 @@ struct DevDelta {
   int64_t n_ent_c = 0;
   cuda::DevArray<int32_t> ent_c, row_ptr_c;
   cuda::DevArray<float> compact;
+  // Source-grouped structural delta (the transposed structural part of G_t vs
+  // G_{t-1}: edges removed = del \ ins, added = ins \ del; persisting
+  // feature-changed pairs cancel): rows_t = sources, entries ~dst (removed) /
+  // dst (added). A_t^T y = A_{t-1}^T y + (this layout) y — used by the
+  // backward to push a hidden gradient through A_{t-1}^T together with the
+  // layer above's input gradient (one transposed SpMM instead of two).
+  int32_t n_rows_t = 0;
+  int64_t n_ent_t = 0;
+  cuda::DevArray<int32_t> rows_t, row_ptr_t, ent_t;
   // distinct deletion / insertion sources (algorithmic-byte accounting)
   int64_t u_minus = 0, u_plus = 0;
   int64_t change_count() const { return n_del + n_ins; }

@@ -367,6 +367,18 @@ std::shared_ptr<AggResult> aggregate_rebase(const AggResult& base, const GraphVi
   return r;
 }
 
+bool aggregate_backward_delta(const DevDelta& delta, int32_t num_nodes, const float* upstream,
+                              int32_t dim, float* grad, cudaStream_t stream) {
+  if (!cuda::agg_delta_struct_supported(kind_i(AggrKind::kSum), dim, upstream) ||
+      !cuda::agg_delta_struct_supported(kind_i(AggrKind::kSum), dim, grad))
+    return false;
+  const double bytes = 8.0 * delta.n_ent_t + 4.0 * dim * delta.n_ent_t + 8.0 * dim * delta.n_rows_t;
+  ProfScope ps(kProfAggRebase, stream, bytes);
+  return cuda::agg_delta_struct(kind_i(AggrKind::kSum), delta.n_rows_t, dim, delta.rows_t.get(),
+                                delta.row_ptr_t.get(), delta.ent_t.get(), num_nodes, nullptr, upstream,
+                                grad, nullptr, nullptr, stream);
+}
+
 IncrementalResult aggregate_incremental(const AggResult& prev, const GraphView& prev_graph,
                                         const GraphView& curr_graph, const float* prev_feats,
                                         const float* curr_feats, const DevDelta& delta,

@@ -98,8 +98,6 @@ double change_ratio(const DevDelta& delta, EdgeIdx base_edges);
 std::shared_ptr<AggResult> aggregate_scratch(const GraphView& graph, const float* feats,
                                              int32_t dim, const AggrFn& fn, cudaStream_t stream);
 
-// Eq. 2 incremental update from prev (ref src/aggregate.cpp:117-207): the
-// new result is out of place (prev stays valid for its co-owners).
 // Agg_{G_t}(H) from base = Agg_{G_{t-1}}(H) of the SAME matrix H: a copy
 // plus the structural part of delta t (removed edges subtract H[src], added
 // edges add it). Same values as aggregate_scratch(graph, H) up to fp32
@@ -111,6 +109,8 @@ std::shared_ptr<AggResult> aggregate_rebase(const AggResult& base, const GraphVi
                                             const float* feats, int32_t dim, const DevDelta& delta,
                                             const AggrFn& fn, cudaStream_t stream);
 
+// Eq. 2 incremental update from prev (ref src/aggregate.cpp:117-207): the
+// new result is out of place (prev stays valid for its co-owners).
 IncrementalResult aggregate_incremental(const AggResult& prev, const GraphView& prev_graph,
                                         const GraphView& curr_graph, const float* prev_feats,
                                         const float* curr_feats, const DevDelta& delta,
@@ -122,6 +122,13 @@ IncrementalResult aggregate_incremental(const AggResult& prev, const GraphView& 
 void aggregate_backward(const GraphView& graph, const float* upstream, int32_t dim,
                         const AggrFn& fn, const AggResult& forward, float* grad,
                         cudaStream_t stream, const float* addend = nullptr);
+
+// grad[u] += sum over the structural part of delta t (source-grouped,
+// DevDelta::rows_t) of +-upstream[v], in place: turns A_{t-1}^T upstream into
+// A_t^T upstream (sum aggregation over full snapshots). Returns false, doing
+// nothing, when the shape is unsupported.
+bool aggregate_backward_delta(const DevDelta& delta, int32_t num_nodes, const float* upstream,
+                              int32_t dim, float* grad, cudaStream_t stream);
 
 // Per-kernel-class device timing (bench.py roofline): when enabled, the
 // wrappers bracket kernels with CUDA events and accumulate durations and

@@ -179,6 +179,22 @@ std::vector<std::string> visit_order(const ModelConfig& cfg) {
   return out;
 }
 
+namespace {
+// tcgen05 path of a linear layer (the GCN weight transforms and the head):
+// y = x W + b (ReLU) and dx = dy W^T through the row GEMM, dW / db through
+// the weight-gradient kernel with the output width padded to its 128 / 256
+// row tile (linear_wgrad_h)
+int linear_wgrad_h(const LinearSlot& l) { return l.out <= 128 ? 32 : 64; }
+void set_linear_umma(LinearSlot& l, cudaStream_t stream) {
+  l.umma = cuda::umma_enabled() && l.in % 16 == 0 && l.out % 16 == 0 && l.out <= 256;
+  l.umma_wgrad = l.umma && l.in % 4 == 0 && l.in + linear_wgrad_h(l) <= 192;
+  if (l.umma) {
+    l.Bf = cuda::DevArray<float>(cuda::umma_bimage_floats(l.out, l.in), stream);
+    l.Bb = cuda::DevArray<float>(cuda::umma_bimage_floats(l.in, l.out), stream);
+  }
+}
+}  // namespace
+
 std::unique_ptr<DgnnModel> DgnnModel::create(const ModelConfig& cfg, cudaStream_t stream) {
   check(cfg.layers >= 1, "model needs at least one layer");
   check(cfg.feature_dim >= 1 && cfg.hidden_dim >= 1, "model dims must be positive");
@@ -238,6 +254,7 @@ std::unique_ptr<DgnnModel> DgnnModel::create(const ModelConfig& cfg, cudaStream_
       g.off_b = off;
       add_slot(g.prefix + "/b");
       g.WT = cuda::DevArray<float>(static_cast<size_t>(g.in) * H, stream);
+      set_linear_umma(g, stream);
       m->gcn_.push_back(std::move(g));
     }
     for (int p = 0; p < cfg.layers; ++p) add_cell("rnn" + std::to_string(p + 1), H, &m->rnn_);
@@ -250,15 +267,7 @@ std::unique_ptr<DgnnModel> DgnnModel::create(const ModelConfig& cfg, cudaStream_
   m->head_.off_b = off;
   add_slot("head/b");
   m->head_.WT = cuda::DevArray<float>(static_cast<size_t>(H) * d, stream);
-  {
-    LinearSlot& h = m->head_;
-    h.umma = cuda::umma_enabled() && h.in % 16 == 0 && h.out % 16 == 0 && h.out <= 256;
-    h.umma_wgrad = h.umma && (h.out == 128 || h.out == 256) && h.in % 4 == 0 && h.in + h.out / 4 <= 192;
-    if (h.umma) {
-      h.Bf = cuda::DevArray<float>(cuda::umma_bimage_floats(h.out, h.in), stream);
-      h.Bb = cuda::DevArray<float>(cuda::umma_bimage_floats(h.in, h.out), stream);
-    }
-  }
+  set_linear_umma(m->head_, stream);
   m->num_params_ = off;
   m->params_ = cuda::DevArray<float>(off, stream);
   m->unflatten_params(m->init_);
@@ -294,13 +303,16 @@ void DgnnModel::refresh_packed() {
   for (auto& c : enc_) pack(c);
   for (auto& c : dec_) pack(c);
   for (auto& c : rnn_) pack(c);
-  for (auto& g : gcn_) cuda::transpose(g.in, g.out, params_.get() + g.off_w, g.WT.get(), stream_);
-  cuda::transpose(head_.in, head_.out, params_.get() + head_.off_w, head_.WT.get(), stream_);
-  if (head_.umma) {
-    const float* W = params_.get() + head_.off_w;  // in x out, row-major
-    cuda::umma_pack_b(W, head_.out, true, 0, head_.out, head_.in, head_.Bf.get(), stream_);   // W^T
-    cuda::umma_pack_b(W, head_.out, false, 0, head_.in, head_.out, head_.Bb.get(), stream_);  // W
-  }
+  auto pack_linear = [&](LinearSlot& l) {
+    cuda::transpose(l.in, l.out, params_.get() + l.off_w, l.WT.get(), stream_);
+    if (l.umma) {
+      const float* W = params_.get() + l.off_w;  // in x out, row-major
+      cuda::umma_pack_b(W, l.out, true, 0, l.out, l.in, l.Bf.get(), stream_);   // W^T
+      cuda::umma_pack_b(W, l.out, false, 0, l.in, l.out, l.Bb.get(), stream_);  // W
+    }
+  };
+  for (auto& g : gcn_) pack_linear(g);
+  pack_linear(head_);
 }
 
 SeqSample build_sample(const DeviceGraph& graph, const ModelConfig& mcfg,
@@ -316,6 +328,7 @@ SeqSample build_sample(const DeviceGraph& graph, const ModelConfig& mcfg,
   bool whole = true;  // full_fanouts (src/train.cpp:68-73)
   for (int32_t f : mcfg.fanouts)
     if (f != -1) whole = false;
+  if (whole) s.graph = &graph;
   std::vector<int32_t> seeds;
   if (!whole)
     for (NodeId v = node_range.first; v < node_range.second; ++v) seeds.push_back(v);
@@ -377,6 +390,16 @@ double cell_flops(int64_t n, int in, int H) { return 2.0 * n * (in + H) * 4.0 * 
 
 }  // namespace
 
+// DGNN_UMMA_PARTS (experiments): bit 1 cell forward / recompute, 2 the dX|dHm
+// contraction, 4 the weight gradient on tcgen05 (default all)
+static int umma_parts() {
+  static const int p = [] {
+    const char* e = std::getenv("DGNN_UMMA_PARTS");
+    return e ? std::atoi(e) : 7;
+  }();
+  return p;
+}
+
 bool gate_recompute_policy(const ModelConfig& cfg, int64_t num_nodes) {
   if (const char* e = std::getenv("DGNN_GATE_TAPE")) return e[0] == '0';
   // auto: drop the gates tape when it would take more than 24 GB per sample
@@ -389,7 +412,7 @@ bool gate_recompute_policy(const ModelConfig& cfg, int64_t num_nodes) {
 
 void DgnnModel::set_gate_recompute(bool on) {
   for (auto* cells : {&enc_, &dec_, &rnn_})
-    for (auto& c : *cells) c.recompute = c.umma && on;
+    for (auto& c : *cells) c.recompute = c.umma && on && (umma_parts() & 1);
 }
 
 namespace {
@@ -409,7 +432,7 @@ CellTape cell_forward(const CellSlot& c, NodeId n, const float* X, const float* 
   const double bytes =
       4.0 * n * (c.in + c.H + (c.recompute ? 0 : 4 * c.H) + c.H + (c.lstm ? 2 * c.H : c.H));
   ProfScope ps(kProfCellFwd, st, bytes, cell_flops(n, c.in, c.H));
-  if (c.umma) {
+  if (c.umma && (umma_parts() & 1)) {
     cuda::umma_cell_forward(c.lstm, n, c.in, c.H, X, Hm, h_skip->get(),
                             c.lstm ? c_prev->get() : nullptr, c.Bf.get(), c.bias.get(),
                             t.gates ? t.gates->get() : nullptr, c.lstm ? t.c->get() : nullptr,
@@ -426,9 +449,9 @@ Buf linear_forward(DgnnModel& m, const LinearSlot& lin, NodeId n, const float* x
                    cudaStream_t st) {
   Buf y = new_buf(static_cast<size_t>(n) * lin.out, st);
   ProfScope ps(kProfOther, st, 4.0 * n * (lin.in + lin.out), 2.0 * n * lin.in * lin.out);
-  if (lin.umma && !relu) {
+  if (lin.umma) {
     cuda::umma_gemm_store2(n, lin.in, x, lin.Bf.get(), lin.out, 0, y->get(), nullptr, st,
-                           m.params() + lin.off_b);
+                           m.params() + lin.off_b, false, 0, relu);
   } else {
     cuda::gemm_nn(n, lin.in, 0, lin.out, 0, x, nullptr, m.params() + lin.off_w, lin.out,
                   m.params() + lin.off_b, relu, false, y->get(), nullptr, st);
@@ -578,6 +601,14 @@ ForwardArtifacts stacked_forward(DgnnModel& model, const SeqSample& sample, AggP
 }
 
 // ---------------------------------------------------------------- backward
+bool backward_merge_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DGNN_BACKWARD_MERGE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 struct Grads {
   float* flat;
   float* ws;  // gemm_tn workspace
@@ -586,9 +617,9 @@ struct Grads {
 void linear_param_grads(DgnnModel& m, const LinearSlot& lin, NodeId n, const float* x,
                         const float* dy, Grads& g, cudaStream_t st) {
   ProfScope ps(kProfWeightGrad, st, 4.0 * n * (lin.in + lin.out), 2.0 * n * lin.in * lin.out);
-  if (lin.umma_wgrad) {  // dW (in x out) += x^T dy, db += colsum(dy): out = 4 * (out / 4)
-    cuda::umma_wgrad(n, lin.in, lin.out / 4, dy, x, nullptr, g.flat + lin.off_w, lin.out,
-                     g.flat + lin.off_b, g.ws, st);
+  if (lin.umma_wgrad) {  // dW (in x out) += x^T dy, db += colsum(dy)
+    cuda::umma_wgrad(n, lin.in, linear_wgrad_h(lin), dy, x, nullptr, g.flat + lin.off_w, lin.out,
+                     g.flat + lin.off_b, g.ws, st, lin.out);
   } else {
     cuda::gemm_tn_acc(n, lin.in, 0, lin.out, x, nullptr, dy, g.flat + lin.off_w, lin.out,
                       g.flat + lin.off_b, g.ws, st);
@@ -598,6 +629,20 @@ void linear_param_grads(DgnnModel& m, const LinearSlot& lin, NodeId n, const flo
 
 struct StepGrads {
   Buf dx, dh_prev, dc_prev;
+  Buf dHm_deferred;  // HmRoute::kDefer: dHm, still to go through A_{t-1}^T
+};
+
+// How a graph step's hidden gradient dHm reaches dh_prev.
+//   kFull   dh_prev = A_t^T dHm (+ GRU skip)
+//   kSkip   the step is the window's first: dh_prev is the gradient of the
+//           zero initial state, which nothing reads — no transposed SpMM
+//   kDefer  dh_prev = (GRU skip) + Delta_t^T dHm, dHm handed back: the layer
+//           above folds it into its input gradient at step t-1, whose
+//           transposed SpMM runs over A_{t-1} (A_t = A_{t-1} + Delta_t), so
+//           two SpMMs over the snapshot become one plus the structural delta
+struct HmRoute {
+  enum Mode { kFull, kSkip, kDefer } mode = kFull;
+  const DevDelta* delta = nullptr;  // kDefer: delta t (snapshot t from t-1)
 };
 
 // cell_core_backward + the graph-step scatter (ref src/cells.cpp:134-236).
@@ -606,9 +651,12 @@ struct StepGrads {
 StepGrads cell_step_backward(CellSlot& c, const CellTape& tape, const float* X, const float* Hm,
                              const AggResult* agg_x, const AggResult* agg_h, const GraphView* view,
                              const Buf& dh, const Buf& dc, bool need_dx, Grads& g, cudaStream_t st,
-                             float* dx_into = nullptr) {
+                             float* dx_into = nullptr, const Buf& dx_fold = nullptr,
+                             HmRoute hm_route = {}) {
   // dx_into (graph steps): accumulate the input gradient straight into the
   // layer below's running dh instead of returning dx
+  // dx_fold: the layer below's deferred dHm of step t+1 (n x in), added to dX
+  // before its transposed SpMM (over A_t; see HmRoute)
   const NodeId n = view ? view->num_nodes : static_cast<NodeId>(tape.h->size() / c.H);
   const int H = c.H, in = c.in;
   Buf G = new_buf(static_cast<size_t>(n) * 4 * H, st);
@@ -640,7 +688,7 @@ StepGrads cell_step_backward(CellSlot& c, const CellTape& tape, const float* X, 
   }
   {
     ProfScope ps(kProfWeightGrad, st, 4.0 * n * (in + H + 4 * H), cell_flops(n, in, H));
-    if (c.umma) {
+    if (c.umma && (umma_parts() & 4)) {
       cuda::umma_wgrad(n, in, H, G->get(), X, Hm, c.dW.get(), c.lstm ? 4 * H : 3 * H, c.db.get(),
                        g.ws, st);
     } else {
@@ -648,15 +696,21 @@ StepGrads cell_step_backward(CellSlot& c, const CellTape& tape, const float* X, 
                         c.db.get(), g.ws, st);
     }
   }
-  Buf dX = need_dx ? new_buf(static_cast<size_t>(n) * in, st) : nullptr;
-  Buf dHm = new_buf(static_cast<size_t>(n) * H, st);
-  {
-    ProfScope ps(kProfCellBwdGemm, st, 4.0 * n * (4 * H + (need_dx ? in : 0) + H),
+  // dX accumulates onto dx_fold in the GEMM epilogue where it can
+  const bool fold_in_gemm = dx_fold && c.umma && (umma_parts() & 2) && in % 16 == 0 && H % 16 == 0;
+  Buf dX = need_dx ? (fold_in_gemm ? dx_fold : new_buf(static_cast<size_t>(n) * in, st)) : nullptr;
+  // the window's first step needs no dHm (HmRoute::kSkip); without dX either
+  // the contraction is skipped
+  const bool skip_gemm = view != nullptr && hm_route.mode == HmRoute::kSkip && !need_dx;
+  Buf dHm = skip_gemm ? nullptr : new_buf(static_cast<size_t>(n) * H, st);
+  if (!skip_gemm) {
+    ProfScope ps(kProfCellBwdGemm, st,
+                 4.0 * n * (4 * H + (need_dx ? in : 0) + H + (fold_in_gemm ? in : 0)),
                  2.0 * n * 4 * H * ((need_dx ? in : 0) + H));
-    if (c.umma) {
+    if (c.umma && (umma_parts() & 2)) {
       if (need_dx) {
         cuda::umma_gemm_store2(n, 4 * H, G->get(), c.Bb.get(), in, H, dX->get(), dHm->get(), st,
-                               nullptr, false, c.lstm ? 0 : H);
+                               nullptr, fold_in_gemm, c.lstm ? 0 : H);
       } else {
         cuda::umma_gemm_store2(n, 4 * H, G->get(), c.Bbh.get(), H, 0, dHm->get(), nullptr, st,
                                nullptr, false, c.lstm ? 0 : H);
@@ -669,6 +723,8 @@ StepGrads cell_step_backward(CellSlot& c, const CellTape& tape, const float* X, 
                     false, dHm->get(), nullptr, st);
     }
   }
+  if (need_dx && dx_fold && !fold_in_gemm)
+    cuda::axpy(static_cast<int64_t>(n) * in, 1.f, dx_fold->get(), dX->get(), st);
   if (view == nullptr) {  // dense step (stacked RNN): dx = dX, dh_prev = dHm (+ skip)
     out.dx = dX;
     out.dh_prev = dHm;
@@ -678,11 +734,20 @@ StepGrads cell_step_backward(CellSlot& c, const CellTape& tape, const float* X, 
   // empty max/min rows contributed zeros; their gradient stops (src/cells.cpp:222-230)
   if (agg_x->extremal() && need_dx)
     cuda::mask_empty_rows(n, in, agg_x->argext.get(), dX->get(), dX->get(), st);
-  if (agg_h->extremal()) cuda::mask_empty_rows(n, H, agg_h->argext.get(), dHm->get(), dHm->get(), st);
+  if (agg_h->extremal() && dHm) cuda::mask_empty_rows(n, H, agg_h->argext.get(), dHm->get(), dHm->get(), st);
   // GRU: dh_prev = A^T dHm + dh_skip, the skip term added inside the SpMM
-  out.dh_prev = new_buf(static_cast<size_t>(n) * H, st);
-  aggregate_backward(*view, dHm->get(), H, AggrFn{agg_h->kind}, *agg_h, out.dh_prev->get(), st,
-                     c.lstm ? nullptr : dh_skip->get());
+  if (hm_route.mode == HmRoute::kSkip) {
+    out.dh_prev = c.lstm ? nullptr : dh_skip;
+  } else if (hm_route.mode == HmRoute::kDefer) {
+    out.dh_prev = c.lstm ? zero_buf(static_cast<size_t>(n) * H, st) : dh_skip;
+    check(aggregate_backward_delta(*hm_route.delta, n, dHm->get(), H, out.dh_prev->get(), st),
+          "deferred hidden gradient: unsupported shape");
+    out.dHm_deferred = dHm;
+  } else {
+    out.dh_prev = new_buf(static_cast<size_t>(n) * H, st);
+    aggregate_backward(*view, dHm->get(), H, AggrFn{agg_h->kind}, *agg_h, out.dh_prev->get(), st,
+                       c.lstm ? nullptr : dh_skip->get());
+  }
   if (need_dx) {
     if (dx_into != nullptr) {
       aggregate_backward(*view, dX->get(), in, AggrFn{agg_x->kind}, *agg_x, dx_into, st, dx_into);
@@ -728,12 +793,16 @@ void integrated_backward(DgnnModel& model, const SeqSample& sample, const Forwar
   const bool lstm = cell_kind_of(cfg.arch) == CellKind::kLstm;
   auto lane_of = [&](int l) { return lanes.two ? (l - 1) & 1 : 0; };
   std::vector<Buf> dh(D), dc(D);
+  // layer l's dHm of the step after the current one, deferred to layer l+1's
+  // input gradient (HmRoute::kDefer)
+  std::vector<Buf> deferred(D);
+  const bool merge = sample.graph != nullptr && backward_merge_enabled();
   for (int l = 0; l < D; ++l) {
     dh[l] = zero_buf(static_cast<size_t>(n) * cfg.hidden_dim, lanes.of(l + 1));
     if (lstm) dc[l] = zero_buf(static_cast<size_t>(n) * cfg.hidden_dim, lanes.of(l + 1));
   }
   auto step = [&](std::vector<CellSlot>& cells, const std::vector<GraphStepTape>& tapes,
-                  const GraphView& view) {
+                  const GraphView& view, Timestep pos) {
     for (int l = D; l >= 1; --l) {
       cudaStream_t st = lanes.of(l);
       const GraphStepTape& tape = tapes[l - 1];
@@ -743,11 +812,22 @@ void integrated_backward(DgnnModel& model, const SeqSample& sample, const Forwar
       // ordered after its last write and before its next use
       float* dx_into = l > 1 ? dh[l - 2]->get() : nullptr;
       if (l > 1) lanes.dep(lanes.of(l - 1), st);
+      HmRoute route;
+      const bool sum_h = tape.agg_h->kind == AggrKind::kSum;
+      if (pos == 0) {
+        route.mode = HmRoute::kSkip;
+      } else if (merge && l < D && sum_h && tapes[l].agg_x->kind == AggrKind::kSum &&
+                 cells[l].in == cells[l - 1].H && view.t >= 1 && view.t < sample.graph->length()) {
+        route.mode = HmRoute::kDefer;
+        route.delta = &sample.graph->delta(view.t);
+      }
+      Buf fold = l > 1 ? std::move(deferred[l - 2]) : nullptr;
       StepGrads sg = cell_step_backward(cells[l - 1], tape.core, tape.agg_x->dense_values(),
                                         tape.agg_h->dense_values(), tape.agg_x.get(),
                                         tape.agg_h.get(), &view, dh[l - 1], lstm ? dc[l - 1] : nullptr,
-                                        l > 1, g[lane_of(l)], st, dx_into);
+                                        l > 1, g[lane_of(l)], st, dx_into, fold, route);
       if (l > 1) lanes.dep(st, lanes.of(l - 1));
+      deferred[l - 1] = std::move(sg.dHm_deferred);
       dh[l - 1] = sg.dh_prev;
       if (lstm) dc[l - 1] = sg.dc_prev;
       // layer-1 inputs are data or stop-gradient feedback: dx is never formed
@@ -757,9 +837,9 @@ void integrated_backward(DgnnModel& model, const SeqSample& sample, const Forwar
   for (Timestep j = H - 1; j >= 0; --j) {
     const GraphStepTape& ts = fwd.dec_steps[j][D - 1];
     head_backward(model, n, ts.core.h->get(), dpred[j], dh[D - 1], g[lane_of(D)], top);
-    step(model.dec_, fwd.dec_steps[j], sample.views[L + j]);
+    step(model.dec_, fwd.dec_steps[j], sample.views[L + j], L + j);
   }
-  for (Timestep idx = L - 1; idx >= 0; --idx) step(model.enc_, fwd.enc_steps[idx], sample.views[idx]);
+  for (Timestep idx = L - 1; idx >= 0; --idx) step(model.enc_, fwd.enc_steps[idx], sample.views[idx], idx);
   lanes.join();
 }
 
@@ -795,8 +875,15 @@ void stacked_backward(DgnnModel& model, const SeqSample& sample, const ForwardAr
       linear_param_grads(model, gcn, n, gt.agg->dense_values(), dpre->get(), g, st);
       if (p == 0) continue;  // pair-1 input gradient is discarded by the reference
       Buf dnormed = new_buf(static_cast<size_t>(n) * gcn.in, st);
-      cuda::gemm_nn(n, Hd, 0, gcn.in, 0, dpre->get(), nullptr, gcn.WT.get(), gcn.in, nullptr, false,
-                    false, dnormed->get(), nullptr, st);
+      {
+        ProfScope ps(kProfOther, st, 4.0 * n * (Hd + gcn.in), 2.0 * n * Hd * gcn.in);
+        if (gcn.umma) {
+          cuda::umma_gemm_store2(n, Hd, dpre->get(), gcn.Bb.get(), gcn.in, 0, dnormed->get(), nullptr, st);
+        } else {
+          cuda::gemm_nn(n, Hd, 0, gcn.in, 0, dpre->get(), nullptr, gcn.WT.get(), gcn.in, nullptr, false,
+                        false, dnormed->get(), nullptr, st);
+        }
+      }
       if (gt.agg->extremal())
         cuda::mask_empty_rows(n, gcn.in, gt.agg->argext.get(), dnormed->get(), dnormed->get(), st);
       Buf dinput = new_buf(static_cast<size_t>(n) * gcn.in, st);
@@ -872,9 +959,11 @@ void model_backward(DgnnModel& model, const SeqSample& sample, const ForwardArti
   }
   ws_n = std::max(ws_n, cuda::gemm_tn_workspace(n, H, d));             // head
   for (int in : {d, H})
-    if (cuda::umma_cell_supported(in, H)) ws_n = std::max(ws_n, cuda::umma_wgrad_workspace(in, H));
+    if (cuda::umma_cell_supported(in, H)) ws_n = std::max(ws_n, cuda::umma_wgrad_workspace(n, in, H));
   if (model.head_.umma_wgrad)
-    ws_n = std::max(ws_n, cuda::umma_wgrad_workspace(model.head_.in, model.head_.out / 4));
+    ws_n = std::max(ws_n, cuda::umma_wgrad_workspace(n, model.head_.in, linear_wgrad_h(model.head_)));
+  for (const LinearSlot& gl : model.gcn_)
+    if (gl.umma_wgrad) ws_n = std::max(ws_n, cuda::umma_wgrad_workspace(n, gl.in, linear_wgrad_h(gl)));
   cuda::DevArray<float> ws(ws_n, stream);
   zero_cell_accumulators(model.enc_, stream);
   zero_cell_accumulators(model.dec_, stream);

@@ -146,6 +146,9 @@ struct SeqSample {
   std::vector<std::shared_ptr<DevSnapshot>> owned;  // sampled k-hop views (to_view)
   std::vector<const float*> feats;    // L+H+1 feature matrices (device)
   std::vector<FeatRef> feat_refs;     // their version leases (resident while the sample lives)
+  // the full snapshots the views are (null for sampled k-hop views): their
+  // deltas let the backward merge transposed SpMMs across steps
+  const DeviceGraph* graph = nullptr;
   NodeId seed_begin = 0, seed_end = 0;  // loss rows (contiguous node range)
   int64_t batch_id = 0;
   Timestep windows_remaining = 0;

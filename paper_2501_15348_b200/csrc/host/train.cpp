@@ -360,6 +360,31 @@ bool DistWorker::apply(const float* grad_sum) {
 
 void DistWorker::end_epoch() { ++epoch_index_; }
 
+DistWorker::EpochResult DistWorker::run_epoch(NcclComm* comm) {
+  cudaStream_t st = worker_->stream();
+  if (grad_sum_.size() == 0) grad_sum_ = cuda::DevArray<float>(model_->num_params(), st);
+  cudaEvent_t ev[2];
+  for (auto& e : ev) DGNN_CUDA(cudaEventCreate(&e));
+  EpochResult r;
+  DGNN_CUDA(cudaEventRecord(ev[0], st));
+  begin_epoch();
+  r.batches = num_batches();
+  for (int64_t b = 0; b < r.batches; ++b) {
+    local_grads(b, grad_sum_.get());
+    if (comm != nullptr && comm->world() > 1) comm->allreduce_sum(grad_sum_.get(), model_->num_params(), st);
+    if (!apply(grad_sum_.get())) ++r.skipped;
+  }
+  DGNN_CUDA(cudaEventRecord(ev[1], st));
+  DGNN_CUDA(cudaEventSynchronize(ev[1]));
+  float ms = 0.f;
+  DGNN_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+  for (auto& e : ev) cudaEventDestroy(e);
+  r.seconds = ms / 1e3;
+  if (comm != nullptr && comm->world() > 1) r.seconds = comm->allreduce_max(r.seconds, st);
+  end_epoch();
+  return r;
+}
+
 std::vector<double> DistWorker::take_losses() {
   std::vector<double> out(n_loss_);
   copy_to_host(out.data(), losses_.get(), sizeof(double) * n_loss_, worker_->stream());

@@ -7,6 +7,7 @@
 #include <utility>
 #include <vector>
 
+#include "comm.hpp"
 #include "model.hpp"
 
 namespace dgnn {
@@ -167,6 +168,15 @@ class DistWorker {
   Worker& worker() { return *worker_; }
   OptimizerState& opt() { return opt_; }
   std::vector<double> take_losses();  // per local sample of the epoch (visit order)
+  // The whole epoch natively (ref run_distributed_epoch, src/distsim.cpp:
+  // 197-272): per batch local_grads -> NCCL sum over ranks (comm null: this
+  // rank alone) -> apply. Device-timed with CUDA events; `seconds` is the max
+  // over ranks. Sample losses via take_losses().
+  struct EpochResult {
+    int64_t batches = 0, skipped = 0;
+    double seconds = 0.0;
+  };
+  EpochResult run_epoch(NcclComm* comm);
   int64_t epoch_index() const { return epoch_index_; }
 
  private:
@@ -179,7 +189,7 @@ class DistWorker {
   OptimizerState opt_;
   std::vector<std::pair<NodeId, NodeId>> batches_;
   int64_t epoch_index_ = 0;
-  cuda::DevArray<float> grad_w_;
+  cuda::DevArray<float> grad_w_, grad_sum_;
   cuda::DevArray<double> losses_;
   int64_t n_loss_ = 0;
 };

@@ -153,6 +153,11 @@ __device__ __forceinline__ void tmem_wait_ld() {
 
 // 3xTF32 split: hi keeps the top 19 bits (exactly representable in TF32),
 // lo = x - hi is exact in fp32 and carries the next ~11 bits.
+// 3xTF32 operand split: hi = x truncated to TF32 (the bits the tensor core
+// reads), lo = x - hi exactly (the tensor core truncates it to TF32 in turn).
+// Rounding both halves to nearest instead (cvt.rna) measured no accuracy
+// gain on C4-shaped cells (the tensor core's truncating accumulation
+// dominates, see RowGemmArgs::split_acc) and costs producer issue slots.
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
   hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
   lo = x - hi;

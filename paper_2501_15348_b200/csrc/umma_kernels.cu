@@ -22,6 +22,7 @@
 // tile i overlaps the MMAs of tile i+1.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <string>
 #include <type_traits>
@@ -47,7 +48,6 @@ __device__ __forceinline__ float ftanh(float x) {
   const float e = __expf(-2.f * fabsf(x));
   return copysignf(__fdividef(1.f - e, 1.f + e), x);
 }
-
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, float a, float b, float c, float d) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
                : "memory");
@@ -121,6 +121,7 @@ struct RowGemmArgs {
   float* C1;
   float* C2;
   int store_accumulate;
+  int relu;  // store2: C1 = max(C1, 0) after bias / accumulate (the GCN layer's ReLU)
   // GRU block-sparse contraction (0 = off, else H): the B image holds the
   // gate columns as [n | r | z | hn]; X-only K chunks skip the hn block
   // (X has no h-part of the candidate gate) and Hm-only chunks skip the
@@ -131,10 +132,27 @@ struct RowGemmArgs {
   // K chunks of the n block feed only the x columns [0, s2_nx), chunks of
   // the hn block only the h columns [s2_h0, s2_h0 + H); r / z chunks all.
   int s2_gru, s2_nx, s2_h0;
+  // cell epilogues: the hi*hi products accumulate in TMEM columns [0, 256)
+  // and the two correction products in [256, 512), summed (RN) in the
+  // epilogue. The tensor core adds into its fp32 accumulator with truncation,
+  // and that bias grows with every accumulate into a large-magnitude sum:
+  // keeping the 2/3 of the MMAs that carry the small correction terms out of
+  // the big accumulator cuts the pre-activation error ~3x (measured against
+  // the fp64 reference on C4-shaped cells). Costs the TMEM double buffer.
+  int split_acc;
   // profiling switches (env DGNN_UMMA_DEBUG): 1 skip epilogue math/stores,
   // 2 skip the B copy, 4 skip the A split/stores
   int debug;
 };
+
+// DGNN_SPLIT_ACC bit 1: cell forward, bit 2: backward gate recompute
+int umma_split_acc() {
+  static const int v = [] {
+    const char* e = std::getenv("DGNN_SPLIT_ACC");
+    return e ? std::atoi(e) : 3;
+  }();
+  return v;
+}
 
 int umma_debug_flags() {
   static const int f = [] {
@@ -317,9 +335,10 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
     const uint32_t idesc3 = gs ? idesc_tf32(kTileM, 3 * gs) : idesc;
     const uint32_t boffH = static_cast<uint32_t>(gs / 8) * 128u;  // B rows [H, 4H)
     uint32_t g = 0, it = 0;
+    const bool split = kEpiCell<EPI> && p.split_acc;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-      const uint32_t b = it & 1u;
-      mbar_wait(&tempty[b], ((it >> 1) & 1u) ^ 1u);
+      const uint32_t b = split ? 0u : (it & 1u);
+      mbar_wait(&tempty[b], (split ? (it & 1u) : ((it >> 1) & 1u)) ^ 1u);
       fence_after_sync();
       const uint32_t d = tmem + b * 256;
       for (int c = 0; c < p.nchunks; ++c, ++g) {
@@ -357,9 +376,11 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
             const uint64_t alo = make_desc(st + S::kA + 2 * ks * lboA, lboA, 128);
             const uint64_t bhi = make_desc(st + 2 * S::kA + 2 * ks * lboB + bo, lboB, 128);
             const uint64_t blo = make_desc(st + 2 * S::kA + S::kB + 2 * ks * lboB + bo, lboB, 128);
-            mma_tf32(dd, ahi, bhi, id, (c > 0 || ks > 0) ? 1u : 0u);
-            mma_tf32(dd, ahi, blo, id, 1u);
-            mma_tf32(dd, alo, bhi, id, 1u);
+            const uint32_t first = (c > 0 || ks > 0) ? 1u : 0u;
+            mma_tf32(dd, ahi, bhi, id, first);
+            const uint32_t dc = split ? dd + 256u : dd;
+            mma_tf32(dc, ahi, blo, id, split ? first : 1u);
+            mma_tf32(dc, alo, bhi, id, 1u);
           }
           commit(&empty[s]);
           if (c == p.nchunks - 1) commit(&tfull[b]);
@@ -371,13 +392,43 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
     // ---------------- epilogue
     const int q = warp & 3, half = (warp - kEpiWarp0) >> 2;
     uint32_t it = 0;
+    const bool split = kEpiCell<EPI> && p.split_acc;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-      const uint32_t b = it & 1u;
-      mbar_wait(&tfull[b], (it >> 1) & 1u);
+      const uint32_t b = split ? 0u : (it & 1u);
+      mbar_wait(&tfull[b], split ? (it & 1u) : ((it >> 1) & 1u));
       fence_after_sync();
       const int64_t row0 = static_cast<int64_t>(tile) * kTileM + q * 32;  // this warp's 32 rows
       const int64_t row = row0 + lane;
       const uint32_t trow = tmem + b * 256 + (static_cast<uint32_t>(q * 32) << 16);
+      // the four gate blocks of hidden units [j0, j0 + 16): hi*hi sums (+ the
+      // correction sums when split)
+      auto ld_gates = [&](int c0, int c1, int c2, int c3, float (&a0)[16], float (&a1)[16],
+                          float (&a2)[16], float (&a3)[16]) {
+        tmem_ld16(trow + c0, a0);
+        tmem_ld16(trow + c1, a1);
+        tmem_ld16(trow + c2, a2);
+        tmem_ld16(trow + c3, a3);
+        tmem_wait_ld();
+        if (split) {
+          float t0[16], t1[16];
+          tmem_ld16(trow + 256 + c0, t0);
+          tmem_ld16(trow + 256 + c1, t1);
+          tmem_wait_ld();
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            a0[u] += t0[u];
+            a1[u] += t1[u];
+          }
+          tmem_ld16(trow + 256 + c2, t0);
+          tmem_ld16(trow + 256 + c3, t1);
+          tmem_wait_ld();
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            a2[u] += t0[u];
+            a3[u] += t1[u];
+          }
+        }
+      };
       // Coalesced store of a 32-row x 16-column register block (lane = row):
       // transposed through a per-warp smem buffer so each st.global.v4 covers
       // 8 rows x 64 contiguous bytes instead of 32 rows x 16 bytes.
@@ -423,11 +474,7 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
         for (int j0 = half * U; j0 < (half + 1) * U; j0 += 16) {
           float a0[16], a1[16], a2[16], a3[16];
           float cv[16];  // out: dc_prev (LSTM) / dh_skip (GRU)
-          tmem_ld16(trow + cb0 + j0, a0);
-          tmem_ld16(trow + cb1 + j0, a1);
-          tmem_ld16(trow + cb2 + j0, a2);
-          tmem_ld16(trow + 3 * H + j0, a3);
-          tmem_wait_ld();
+          ld_gates(cb0 + j0, cb1 + j0, cb2 + j0, 3 * H + j0, a0, a1, a2, a3);
           // per-row operands 4 columns at a time (register budget of 152)
           const float* sp = (EPI == kEpiLstmBwd ? p.c_prev : p.h_skip) + row * H + j0;
           const float* dp = p.dh + row * H + j0;
@@ -486,11 +533,7 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
           // state row prefetch overlaps the TMEM reads
           float sv[16];
           load16(EPI == kEpiLstm ? p.c_prev : p.h_skip, j0, sv);
-          tmem_ld16(trow + cb0 + j0, a0);
-          tmem_ld16(trow + cb1 + j0, a1);
-          tmem_ld16(trow + cb2 + j0, a2);
-          tmem_ld16(trow + 3 * H + j0, a3);
-          tmem_wait_ld();
+          ld_gates(cb0 + j0, cb1 + j0, cb2 + j0, 3 * H + j0, a0, a1, a2, a3);
           if (!(p.debug & 1)) {
             float ho[16], co[16];
 #pragma unroll
@@ -547,6 +590,10 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
                 const float4 e = *reinterpret_cast<const float4*>(ep + u);
                 a[u] += e.x; a[u + 1] += e.y; a[u + 2] += e.z; a[u + 3] += e.w;
               }
+            }
+            if (p.relu) {
+#pragma unroll
+              for (int u = 0; u < 16; ++u) a[u] = a[u] > 0.f ? a[u] : 0.f;  // ref src/nn.cpp:19-25
             }
             stage_store(a, p.C1, p.n1, cb);
           } else {
@@ -617,7 +664,9 @@ __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
 template <int MG, int NPAD>
 __global__ void __launch_bounds__(kThreads, 1)
 k_wgrad(int M, int in, int H, const float* __restrict__ G, const float* __restrict__ X,
-        const float* __restrict__ Hm, float* __restrict__ ws) {
+        const float* __restrict__ Hm, float* __restrict__ ws, int gw) {
+  // gw: columns of G (<= MG; the rest of A' is zero — a linear layer with
+  // fewer than 128 outputs)
   using S = WgradSmem<MG, NPAD>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kBars);
@@ -672,7 +721,7 @@ k_wgrad(int M, int in, int H, const float* __restrict__ G, const float* __restri
       const uint32_t slot = raw0 + r * S::kRaw;
       const int64_t q0 = rb + static_cast<int64_t>(c) * kKW;
       const int live = static_cast<int>(re - q0 < kKW ? re - q0 : kKW);
-      copy_region(slot, G + q0 * MG, MG, live);
+      copy_region(slot, G + q0 * gw, gw, live);
       copy_region(slot + kKW * MG * 4, X + q0 * in, in, live);
       // Hm absent (a plain linear layer's weight gradient): zero columns
       copy_region(slot + kKW * (MG + in) * 4, Hm ? Hm + q0 * H : G, H, Hm ? live : 0);
@@ -697,7 +746,7 @@ k_wgrad(int M, int in, int H, const float* __restrict__ G, const float* __restri
         const int m = task % MG, k4 = task / MG;
         float h[4], l[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) split_tf32(rawG[(k4 * 4 + q) * MG + m], h[q], l[q]);
+        for (int q = 0; q < 4; ++q) split_tf32(m < gw ? rawG[(k4 * 4 + q) * gw + m] : 0.f, h[q], l[q]);
         const uint32_t off = tile_offset(MG, m, k4 * 4);
         st_shared_v4(st + off, h[0], h[1], h[2], h[3]);
         st_shared_v4(st + S::kA + off, l[0], l[1], l[2], l[3]);
@@ -786,10 +835,10 @@ k_wgrad(int M, int in, int H, const float* __restrict__ G, const float* __restri
 }
 
 // dW[k][m] += sum_cta D'[cta][m][k] (k < in+H); db[m] += sum_cta D'[cta][m][in+H] (m < nb)
-__global__ void k_wgrad_reduce(int nctas, int MG, int NPAD, int KXH, int wrows, int nb,
+__global__ void k_wgrad_reduce(int nctas, int MG, int NPAD, int KXH, int wrows, int nb, int gw,
                                const float* __restrict__ ws, float* __restrict__ dW,
                                float* __restrict__ db) {
-  const int64_t total = static_cast<int64_t>(MG) * (KXH + 1);
+  const int64_t total = static_cast<int64_t>(gw) * (KXH + 1);
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int m = static_cast<int>(i / (KXH + 1));
@@ -797,7 +846,7 @@ __global__ void k_wgrad_reduce(int nctas, int MG, int NPAD, int KXH, int wrows, 
     float acc = 0.f;
     for (int c = 0; c < nctas; ++c) acc += ws[(static_cast<int64_t>(c) * MG + m) * NPAD + k];
     if (k < KXH) {
-      if (k < wrows) dW[static_cast<int64_t>(k) * MG + m] += acc;
+      if (k < wrows) dW[static_cast<int64_t>(k) * gw + m] += acc;
     } else if (m < nb) {
       db[m] += acc;
     }
@@ -899,6 +948,7 @@ void umma_cell_forward(bool lstm, int n, int in, int H, const float* X, const fl
   a.c_out = c;
   a.h_out = h;
   a.gru_split = umma_gru_split(lstm, in, H) ? H : 0;
+  a.split_acc = umma_split_acc() & 1;
   a.debug = umma_debug_flags();
   const int npad = umma_npad(4 * H);
   if (lstm) dispatch_row_gemm<kEpiLstm>(npad, a, stream);
@@ -927,6 +977,7 @@ void umma_cell_backward_recompute(bool lstm, int n, int in, int H, const float* 
   a.G = G;
   a.dstate = dstate;
   a.gru_split = umma_gru_split(lstm, in, H) ? H : 0;
+  a.split_acc = (umma_split_acc() >> 1) & 1;
   a.debug = umma_debug_flags();
   const int npad = umma_npad(4 * H);
   if (lstm) dispatch_row_gemm<kEpiLstmBwd>(npad, a, stream);
@@ -934,11 +985,13 @@ void umma_cell_backward_recompute(bool lstm, int n, int in, int H, const float* 
 }
 
 void umma_gemm_store2(int n, int K, const float* A, const float* Bimg, int n1, int n2, float* C1,
-                      float* C2, cudaStream_t stream, const float* bias, bool accumulate, int gru_h) {
-  if ((bias || accumulate) && !(n1 % 16 == 0 && n2 % 16 == 0 && n1 <= 256))
-    throw std::invalid_argument("umma_gemm_store2: bias / accumulate need 16-column blocks");
+                      float* C2, cudaStream_t stream, const float* bias, bool accumulate, int gru_h,
+                      bool relu) {
+  if ((bias || accumulate || relu) && !(n1 % 16 == 0 && n2 % 16 == 0 && n1 <= 256))
+    throw std::invalid_argument("umma_gemm_store2: bias / accumulate / relu need 16-column blocks");
   RowGemmArgs a{};
   a.bias = bias;
+  a.relu = relu ? 1 : 0;
   a.store_accumulate = accumulate ? 1 : 0;
   a.M = n;
   a.k1 = K;
@@ -963,17 +1016,32 @@ void umma_gemm_store2(int n, int K, const float* A, const float* Bimg, int n1, i
   dispatch_row_gemm<kEpiStore2>(umma_npad(n1 + n2), a, stream);
 }
 
-int64_t umma_wgrad_workspace(int in, int H) {
+// CTAs of the weight gradient for n rows: >= ~512 rows each (every CTA writes
+// a 4H x Npad partial the reduction reads back) and <= kWgRowsPerCta rows
+// each. The tensor core adds into its fp32 accumulator with truncation, so
+// the error of one CTA's partial grows with the rows it sums; capping them
+// bounds it (1M rows / 148 CTAs measured 4.8e-5 norm-relative vs fp64) and
+// the fixed-order reduction of the partials is exact-rounded fp32.
+constexpr int64_t kWgRowsPerCta = 8192;
+int wgrad_grid(int64_t n) {
+  const int64_t cap = (n + kWgRowsPerCta - 1) / kWgRowsPerCta;
+  if (cap > kNumSMs) return static_cast<int>((cap + kNumSMs - 1) / kNumSMs * kNumSMs);
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kNumSMs, n / 512)));
+}
+
+int64_t umma_wgrad_workspace(int64_t n, int in, int H) {
   const int need = round_up(in + H + 1, 16);
   const int npad = need <= 144 ? 144 : (need <= 208 ? 208 : 256);
-  return static_cast<int64_t>(kNumSMs) * 4 * H * npad;
+  return static_cast<int64_t>(wgrad_grid(n)) * 4 * H * npad;
 }
 
 void umma_wgrad(int n, int in, int H, const float* G, const float* X, const float* Hm, float* dW,
-                int nb, float* db, float* ws, cudaStream_t stream) {
+                int nb, float* db, float* ws, cudaStream_t stream, int gw) {
+  if (gw <= 0) gw = 4 * H;
+  if (gw > 4 * H) throw std::invalid_argument("umma_wgrad: G wider than 4H");
   const int need = round_up(in + H + 1, 16);
   const int npad = need <= 144 ? 144 : (need <= 208 ? 208 : 256);
-  const int grid = kNumSMs;
+  const int grid = wgrad_grid(n);
   auto go = [&](auto mg_tag, auto np_tag) {
     constexpr int MG = decltype(mg_tag)::value, NP = decltype(np_tag)::value;
     const uint32_t smem = WgradSmem<MG, NP>::kBytes;
@@ -982,7 +1050,7 @@ void umma_wgrad(int n, int in, int H, const float* G, const float* X, const floa
       DGNN_CUDA(cudaFuncSetAttribute(k_wgrad<MG, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       configured = true;
     }
-    DGNN_LAUNCH((k_wgrad<MG, NP>), grid, kThreads, smem, stream, n, in, H, G, X, Hm, ws);
+    DGNN_LAUNCH((k_wgrad<MG, NP>), grid, kThreads, smem, stream, n, in, H, G, X, Hm, ws, gw);
   };
   if (H == 64) {
     if (npad == 144) go(std::integral_constant<int, 256>{}, std::integral_constant<int, 144>{});
@@ -993,9 +1061,9 @@ void umma_wgrad(int n, int in, int H, const float* G, const float* X, const floa
     else if (npad == 208) go(std::integral_constant<int, 128>{}, std::integral_constant<int, 208>{});
     else go(std::integral_constant<int, 128>{}, std::integral_constant<int, 256>{});
   }
-  const int64_t total = static_cast<int64_t>(4 * H) * (in + H + 1);
+  const int64_t total = static_cast<int64_t>(gw) * (in + H + 1);
   DGNN_LAUNCH(k_wgrad_reduce, wave_grid(total, 256, 4), 256, 0, stream, grid, 4 * H, npad, in + H,
-              Hm ? in + H : in, nb, ws, dW, db);
+              Hm ? in + H : in, nb, gw, ws, dW, db);
 }
 
 }  // namespace cuda

@@ -45,13 +45,14 @@ void umma_cell_backward_recompute(bool lstm, int n, int in, int H, const float* 
 // (both need 16-column blocks).
 void umma_gemm_store2(int n, int K, const float* A, const float* Bimg, int n1, int n2, float* C1,
                       float* C2, cudaStream_t stream, const float* bias = nullptr,
-                      bool accumulate = false, int gru_h = 0);
+                      bool accumulate = false, int gru_h = 0, bool relu = false);
 
 // dW ((in+H) x 4H) += [X|Hm]^T G, db (nb) += colsum(G[:, :nb]); deterministic.
-// Hm == nullptr: a plain linear layer's gradient, dW (in x 4H) += X^T G.
-int64_t umma_wgrad_workspace(int in, int H);
+// Hm == nullptr: a plain linear layer's gradient, dW (in x gw) += X^T G with
+// G n x gw, gw <= 4H (default 4H; H then only sizes the tile: 4H in {128, 256}).
+int64_t umma_wgrad_workspace(int64_t n, int in, int H);
 void umma_wgrad(int n, int in, int H, const float* G, const float* X, const float* Hm, float* dW,
-                int nb, float* db, float* ws, cudaStream_t stream);
+                int nb, float* db, float* ws, cudaStream_t stream, int gw = 0);
 
 }  // namespace cuda
 }  // namespace dgnn

