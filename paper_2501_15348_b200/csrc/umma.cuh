@@ -151,8 +151,6 @@ __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// 3xTF32 split: hi keeps the top 19 bits (exactly representable in TF32),
-// lo = x - hi is exact in fp32 and carries the next ~11 bits.
 // 3xTF32 operand split: hi = x truncated to TF32 (the bits the tensor core
 // reads), lo = x - hi exactly (the tensor core truncates it to TF32 in turn).
 // Rounding both halves to nearest instead (cvt.rna) measured no accuracy

@@ -145,11 +145,14 @@ struct RowGemmArgs {
   int debug;
 };
 
-// DGNN_SPLIT_ACC bit 1: cell forward, bit 2: backward gate recompute
+// DGNN_SPLIT_ACC bit 1: cell forward, bit 2: backward gate recompute. The
+// forward's split sets the accuracy of h / predictions (and through them the
+// gradients); splitting the recompute as well measured no further gain on
+// the C4-shaped gradients and costs ~0.7 s per C4 epoch, so it is off.
 int umma_split_acc() {
   static const int v = [] {
     const char* e = std::getenv("DGNN_SPLIT_ACC");
-    return e ? std::atoi(e) : 3;
+    return e ? std::atoi(e) : 1;
   }();
   return v;
 }
@@ -1042,6 +1045,15 @@ void umma_wgrad(int n, int in, int H, const float* G, const float* X, const floa
   const int need = round_up(in + H + 1, 16);
   const int npad = need <= 144 ? 144 : (need <= 208 ? 208 : 256);
   const int grid = wgrad_grid(n);
+  if (umma_wgrad_mn_supported(in, H, gw, G, X, Hm)) {
+    // TMA-fed MN-major kernel (umma_wgrad.cu)
+    const int np = umma_wgrad_mn(n, in, H, G, gw, X, Hm, ws, grid, stream);
+    const int kxh = in + (Hm ? H : 0);
+    const int64_t total = static_cast<int64_t>(gw) * (kxh + 1);
+    DGNN_LAUNCH(k_wgrad_reduce, wave_grid(total, 256, 4), 256, 0, stream, grid, 4 * H, np, kxh, kxh, nb, gw, ws,
+                dW, db);
+    return;
+  }
   auto go = [&](auto mg_tag, auto np_tag) {
     constexpr int MG = decltype(mg_tag)::value, NP = decltype(np_tag)::value;
     const uint32_t smem = WgradSmem<MG, NP>::kBytes;

@@ -51,6 +51,12 @@ void umma_gemm_store2(int n, int K, const float* A, const float* Bimg, int n1, i
 // Hm == nullptr: a plain linear layer's gradient, dW (in x gw) += X^T G with
 // G n x gw, gw <= 4H (default 4H; H then only sizes the tile: 4H in {128, 256}).
 int64_t umma_wgrad_workspace(int64_t n, int in, int H);
+// TMA-fed MN-major variant (umma_wgrad.cu): shapes it covers, and the
+// partials of `grid` CTAs into ws (returns the partial's column pitch)
+bool umma_wgrad_mn_supported(int in, int H, int gw, const float* G, const float* X, const float* Hm);
+int umma_wgrad_mn_npad(int in, int H, bool has_hm);
+int umma_wgrad_mn(int64_t n, int in, int H, const float* G, int gw, const float* X, const float* Hm,
+                  float* ws, int grid, cudaStream_t stream);
 void umma_wgrad(int n, int in, int H, const float* G, const float* X, const float* Hm, float* dW,
                 int nb, float* db, float* ws, cudaStream_t stream, int gw = 0);
 

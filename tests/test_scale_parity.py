@@ -103,14 +103,15 @@ def test_c1_full_epoch_matches_reference(ref, api):
 def test_c4_downscaled_epoch_matches_reference(ref, api):
     """C4's model and dynamics on 1,500 nodes: tgcn (GRU), d=128, h=64, T=64
     (55 windows), 2% structural + 2% feature churn. The input aggregation chain
-    runs incrementally from t=0 to t=63 (depth 63) inside the epoch."""
+    runs incrementally from t=0 to t=62 (the last window's last step) inside
+    the epoch."""
     s, r = _epoch_vs_reference(ref, api, (1_500, 20.0, 128, 64, 0.02, 0.02),
                                dict(arch="tgcn", hidden=64), trajectory=False)
     assert len(r.losses) == 55
     inv = s.invocations()
     # (layer, t, kind, incremental): the layer-1 input chain reaches t = 63 incrementally
     inc = inv[(inv[:, 0] == 1) & (inv[:, 2] == 0) & (inv[:, 3] == 1)]
-    assert inc[:, 1].max() == 63
+    assert inc[:, 1].max() == 62  # the last window (start 54) ends at t = 62
 
 
 def test_c4_downscaled_sample_grads(ref, api):
