@@ -212,11 +212,20 @@ def main():
     ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--prof-in-timed", type=int, default=-1,
+                    help="1: per-kernel-class CUDA-event profiling inside the timed region (the "
+                         "roofline's launch times are those of the timed steps); 0: the timed steps "
+                         "run unprofiled and one extra profiled step gives the class breakdown. "
+                         "Default: 1 for the bandwidth-bound workloads (c3, c4), 0 for the "
+                         "launch-latency-bound ones (c1, c2), where two events per kernel class "
+                         "scope measurably slow the host issue loop")
     ap.add_argument("--hbm-cache-gb", type=float, default=0.0,
                     help="second cache level: HBM budget of unborrowed cached aggregations "
                          "(0 = everything stays in HBM; C4 spills below ~16 GB)")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
+    if args.prof_in_timed < 0:
+        args.prof_in_timed = 0 if args.workload in ("c1", "c2") else 1
     if args.impl == "reference":
         return run_reference_arm(args, wl)
 
@@ -263,7 +272,7 @@ def main():
 
     # ---------------- timed region (device time, max over ranks)
     api.prof_reset()
-    api.prof_enable(True)
+    api.prof_enable(bool(args.prof_in_timed))
     launches0 = api.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
@@ -279,6 +288,14 @@ def main():
         barrier()
     api.prof_enable(False)
     launches = api.launch_count() - launches0
+    prof_steps = args.steps
+    if not args.prof_in_timed:  # one extra, profiled step for the class breakdown
+        api.prof_reset()
+        api.prof_enable(True)
+        epoch()
+        torch.cuda.synchronize()
+        api.prof_enable(False)
+        prof_steps = 1
     if world > 1:  # whole-job kernel launches (every rank's)
         lt = torch.tensor([launches], device="cuda", dtype=torch.int64)
         dist.all_reduce(lt)
@@ -291,6 +308,7 @@ def main():
     snaps_per_step = W_total * (L + H)
     value = snaps_per_step / (ms_step / 1e3)
     prof = api.prof_get()
+    scopes = api.prof_get(scopes=True)
     losses = sess.losses()
 
     # ---------------- roofline of the dominant kernel class (+ the graded delta-SpMM)
@@ -422,7 +440,10 @@ def main():
                        "l2": f"inputs exceed the 126 MB L2 (graph store {memory['graph_store_gb']} GB; "
                              f"one feature matrix {wl['n'] * wl['dim'] * 4 / 1e9:.2f} GB)"},
             "roofline": roofline, "roofline_delta_spmm": delta_roof,
-            "kernel_ms_by_class": {k: round(v["ms"] / args.steps, 2) for k, v in prof.items()},
+            "kernel_ms_by_class": {k: round(v["ms"] / prof_steps, 2) for k, v in prof.items()},
+            "profiled": "timed steps" if args.prof_in_timed else "one extra step after the timed ones",
+            "host_ms_per_sample": {k: round(v["ms"] / max(scopes["sample_host"]["launches"], 1), 3)
+                                   for k, v in scopes.items() if k.startswith("host") or k == "sample_host"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "memory": memory,
             "clocks": clocks.summary(), "epoch_loss": float(losses.mean()) if len(losses) else None,
             "setup_s": {"synth": round(t_synth, 1), "device_graph_build": round(t_build, 2)},

@@ -151,8 +151,12 @@ void* dev_alloc(size_t bytes, cudaStream_t stream) {
                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   if (e != cudaSuccess) {
     (void)cudaGetLastError();
-    throw std::runtime_error("device allocation of " + std::to_string(bytes) +
-                             " bytes failed: " + cudaGetErrorString(e));
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    throw std::runtime_error("device allocation of " + std::to_string(bytes) + " bytes failed: " +
+                             cudaGetErrorString(e) + " (live " + std::to_string(dev_bytes_live() >> 20) +
+                             " MiB in buffers, device free " + std::to_string(free_b >> 20) + " of " +
+                             std::to_string(total_b >> 20) + " MiB)");
   }
   dev_bytes_live() += static_cast<int64_t>(r);
   return p;

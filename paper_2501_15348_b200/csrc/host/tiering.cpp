@@ -1,31 +1,37 @@
 // HBM <-> pinned-host placement of cached aggregations (see tiering.hpp).
 #include "tiering.hpp"
 
+#include <algorithm>
 #include <utility>
 
 namespace dgnn {
 
 // ---------------------------------------------------------------- PinnedPool
 PinnedPool::~PinnedPool() {
+  for (auto& [sz, v] : free_)
+    for (auto& [p, e] : v)
+      if (e) cudaEventDestroy(e);
   for (void* p : all_) cudaFreeHost(p);
 }
 
-void* PinnedPool::take(size_t bytes) {
+void* PinnedPool::take(size_t bytes, cudaEvent_t* last_use) {
   auto it = free_.find(bytes);
   if (it != free_.end() && !it->second.empty()) {
-    void* p = it->second.back();
+    auto [p, e] = it->second.back();
     it->second.pop_back();
+    *last_use = e;
     return p;
   }
   void* p = nullptr;
   DGNN_CUDA(cudaHostAlloc(&p, bytes, cudaHostAllocPortable));
   all_.push_back(p);
   reserved_ += static_cast<int64_t>(bytes);
+  *last_use = nullptr;
   return p;
 }
 
-void PinnedPool::give(void* p, size_t bytes) {
-  if (p) free_[bytes].push_back(p);
+void PinnedPool::give(void* p, size_t bytes, cudaEvent_t last_use) {
+  if (p) free_[bytes].emplace_back(p, last_use);
 }
 
 // ---------------------------------------------------------------- HbmTier
@@ -65,15 +71,19 @@ Shape shape_of(const AggResult& r) {
 
 }  // namespace
 
-HbmTier::HbmTier(int64_t budget_bytes, cudaStream_t compute) : budget_(budget_bytes), compute_(compute) {
-  DGNN_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
+HbmTier::HbmTier(int64_t budget_bytes, cudaStream_t compute)
+    : budget_(budget_bytes), retiring_cap_(std::max<int64_t>(budget_bytes, int64_t{4} << 30)), compute_(compute) {
+  DGNN_CUDA(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
+  DGNN_CUDA(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
 }
 
 HbmTier::~HbmTier() {
-  if (copy_) cudaStreamSynchronize(copy_);
+  if (d2h_) cudaStreamSynchronize(d2h_);
+  if (h2d_) cudaStreamSynchronize(h2d_);
   reap(true);
   for (cudaEvent_t e : events_) cudaEventDestroy(e);
-  if (copy_) cudaStreamDestroy(copy_);
+  if (d2h_) cudaStreamDestroy(d2h_);
+  if (h2d_) cudaStreamDestroy(h2d_);
 }
 
 cudaEvent_t HbmTier::take_event() {
@@ -93,26 +103,43 @@ int64_t HbmTier::device_bytes(const AggResult& r) {
 
 void HbmTier::spill(AggResult& r, Placement& p) {
   const Shape s = shape_of(r);
+  // backpressure: bound the device bytes held by spills still in flight
+  reap();
+  while (retiring_bytes_ + static_cast<int64_t>(s.bytes()) > retiring_cap_ && !retiring_.empty()) {
+    DGNN_CUDA(cudaEventSynchronize(retiring_.front().done));
+    reap();
+  }
   p.host_bytes = s.bytes();
-  p.host = pool_.take(p.host_bytes);
+  cudaEvent_t last_read = nullptr;
+  p.host = pool_.take(p.host_bytes, &last_read);
+  // the block's previous refill must have read it before this spill writes it
+  if (last_read) {
+    DGNN_CUDA(cudaStreamWaitEvent(d2h_, last_read, 0));
+    give_event(last_read);
+  }
   // the copy starts after everything the compute stream has queued so far
   // (the payload's producer and every reader issued before the spill)
   cudaEvent_t produced = take_event();
   DGNN_CUDA(cudaEventRecord(produced, compute_));
-  DGNN_CUDA(cudaStreamWaitEvent(copy_, produced, 0));
+  DGNN_CUDA(cudaStreamWaitEvent(d2h_, produced, 0));
   give_event(produced);
   Retiring ret;
   ret.done = take_event();
+  ret.bytes = static_cast<int64_t>(s.bytes());
   char* dst = static_cast<char*>(p.host);
   auto out = [&](auto& arr, auto& keep) {
     if (arr.size() == 0) return;
-    DGNN_CUDA(cudaMemcpyAsync(dst, arr.get(), arr.bytes(), cudaMemcpyDeviceToHost, copy_));
+    DGNN_CUDA(cudaMemcpyAsync(dst, arr.get(), arr.bytes(), cudaMemcpyDeviceToHost, d2h_));
     dst += arr.bytes();
     keep.push_back(std::move(arr));
   };
   each_array(r, [&](cuda::DevArray<float>& a) { out(a, ret.f); },
              [&](cuda::DevArray<int32_t>& a) { out(a, ret.i); });
-  DGNN_CUDA(cudaEventRecord(ret.done, copy_));
+  DGNN_CUDA(cudaEventRecord(ret.done, d2h_));
+  // the refill of this payload reads the block after this write
+  p.host_written = take_event();
+  DGNN_CUDA(cudaEventRecord(p.host_written, d2h_));
+  retiring_bytes_ += ret.bytes;
   retiring_.push_back(std::move(ret));
   p.where = Placement::Where::kHost;
   ++stats_.spills;
@@ -130,20 +157,27 @@ void HbmTier::fetch(AggResult& r, Placement& p, bool ahead) {
   r.argext = cuda::DevArray<int32_t>(s.argext, compute_);
   cudaEvent_t allocated = take_event();
   DGNN_CUDA(cudaEventRecord(allocated, compute_));
-  DGNN_CUDA(cudaStreamWaitEvent(copy_, allocated, 0));
+  DGNN_CUDA(cudaStreamWaitEvent(h2d_, allocated, 0));
   give_event(allocated);
+  // the spill that wrote the block has completed before it is read
+  if (p.host_written) {
+    DGNN_CUDA(cudaStreamWaitEvent(h2d_, p.host_written, 0));
+    give_event(p.host_written);
+    p.host_written = nullptr;
+  }
   const char* src = static_cast<const char*>(p.host);
   auto in = [&](auto& arr) {
     if (arr.size() == 0) return;
-    DGNN_CUDA(cudaMemcpyAsync(arr.get(), src, arr.bytes(), cudaMemcpyHostToDevice, copy_));
+    DGNN_CUDA(cudaMemcpyAsync(arr.get(), src, arr.bytes(), cudaMemcpyHostToDevice, h2d_));
     src += arr.bytes();
   };
   each_array(r, in, in);
   p.inbound = take_event();
-  DGNN_CUDA(cudaEventRecord(p.inbound, copy_));
-  // later spills into this block are issued on the same copy stream, after
-  // this read of it
-  pool_.give(p.host, p.host_bytes);
+  DGNN_CUDA(cudaEventRecord(p.inbound, h2d_));
+  // the next spill into this block waits for this read of it
+  cudaEvent_t read_done = take_event();
+  DGNN_CUDA(cudaEventRecord(read_done, h2d_));
+  pool_.give(p.host, p.host_bytes, read_done);
   p.host = nullptr;
   p.where = Placement::Where::kInbound;
   ++stats_.refills;
@@ -162,7 +196,9 @@ void HbmTier::settle(Placement& p) {
 void HbmTier::drop(AggResult& r, Placement& p) {
   (void)r;
   if (p.where == Placement::Where::kHost) {
-    pool_.give(p.host, p.host_bytes);
+    // its last use is the spill that wrote it
+    pool_.give(p.host, p.host_bytes, p.host_written);
+    p.host_written = nullptr;
     p.host = nullptr;
   } else if (p.where == Placement::Where::kInbound) {
     // the arrays are released in compute-stream order: order that after the
@@ -181,6 +217,7 @@ void HbmTier::reap(bool wait) {
       give_event(r.done);
       r.f.clear();  // back to the compute stream's free lists
       r.i.clear();
+      retiring_bytes_ -= r.bytes;
       continue;
     }
     if (q != cudaErrorNotReady) DGNN_CUDA(q);

@@ -7,11 +7,16 @@
 //   kHbm     device arrays present, usable by kernels
 //   kHost    bytes in a pinned host block, device arrays released
 //   kInbound host->device copy issued on the copy stream, not yet waited on
-// Every copy runs on one copy stream, so a pinned block is reused strictly in
-// stream order; device buffers a spill reads are released to the compute
-// stream's allocator only after the spill copy has completed (polled, never
-// synchronised on the hot path). The compute stream waits on an inbound
-// payload's event only when the payload is handed out (get / peek).
+// Spills (device -> host) and refills (host -> device) run on two copy
+// streams, so PCIe carries both directions at once. A pinned block carries
+// the event of its last use: a refill reading it waits for the spill that
+// wrote it, a later spill into it waits for that refill. Device buffers a
+// spill reads are released to the compute stream's allocator only after the
+// spill copy has completed (polled); when the spills in flight exceed the
+// in-flight cap the host waits for the oldest (backpressure: a saturated
+// link must not turn into unbounded HBM held by retiring buffers). The
+// compute stream waits on an inbound payload's event only when the payload
+// is handed out (get / peek).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -32,12 +37,13 @@ class PinnedPool {
   ~PinnedPool();
   PinnedPool(const PinnedPool&) = delete;
   PinnedPool& operator=(const PinnedPool&) = delete;
-  void* take(size_t bytes);
-  void give(void* p, size_t bytes);
+  // a block and the event of its last copy (null: never used)
+  void* take(size_t bytes, cudaEvent_t* last_use);
+  void give(void* p, size_t bytes, cudaEvent_t last_use);
   int64_t reserved_bytes() const { return reserved_; }
 
  private:
-  std::map<size_t, std::vector<void*>> free_;
+  std::map<size_t, std::vector<std::pair<void*, cudaEvent_t>>> free_;
   std::vector<void*> all_;
   int64_t reserved_ = 0;
 };
@@ -47,7 +53,8 @@ struct Placement {
   Where where = Where::kHbm;
   void* host = nullptr;
   size_t host_bytes = 0;
-  cudaEvent_t inbound = nullptr;  // H2D completion while kInbound
+  cudaEvent_t host_written = nullptr;  // D2H completion into `host` while kHost
+  cudaEvent_t inbound = nullptr;       // H2D completion while kInbound
 };
 
 struct TierStats {
@@ -68,7 +75,7 @@ class HbmTier {
 
   int64_t budget() const { return budget_; }
   cudaStream_t compute() const { return compute_; }
-  cudaStream_t copy() const { return copy_; }
+  cudaStream_t copy() const { return d2h_; }
   const TierStats& stats() const { return stats_; }
   int64_t pinned_bytes() const { return pool_.reserved_bytes(); }
 
@@ -87,15 +94,20 @@ class HbmTier {
  private:
   struct Retiring {
     cudaEvent_t done;
+    int64_t bytes = 0;
     std::vector<cuda::DevArray<float>> f;
     std::vector<cuda::DevArray<int32_t>> i;
   };
   cudaEvent_t take_event();
-  void give_event(cudaEvent_t e) { events_.push_back(e); }
+  void give_event(cudaEvent_t e) {
+    if (e) events_.push_back(e);
+  }
 
   int64_t budget_;
+  int64_t retiring_cap_;  // device bytes of spills in flight before the host waits
+  int64_t retiring_bytes_ = 0;
   cudaStream_t compute_;
-  cudaStream_t copy_ = nullptr;
+  cudaStream_t d2h_ = nullptr, h2d_ = nullptr;
   PinnedPool pool_;
   std::vector<Retiring> retiring_;
   std::vector<cudaEvent_t> events_;

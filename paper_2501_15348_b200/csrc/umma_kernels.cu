@@ -139,6 +139,10 @@ struct RowGemmArgs {
   // keeping the 2/3 of the MMAs that carry the small correction terms out of
   // the big accumulator cuts the pre-activation error ~3x (measured against
   // the fp64 reference on C4-shaped cells). Costs the TMEM double buffer.
+  // (Measured alternative with the same accuracy and no extra TMEM: two
+  // passes over K per tile, corrections first, then hi*hi — the same ~40%
+  // forward-kernel cost from re-reading / re-splitting A, and slower in the
+  // C4 epoch, so not kept.)
   int split_acc;
   // profiling switches (env DGNN_UMMA_DEBUG): 1 skip epilogue math/stores,
   // 2 skip the B copy, 4 skip the A split/stores
@@ -1019,7 +1023,7 @@ void umma_gemm_store2(int n, int K, const float* A, const float* Bimg, int n1, i
   dispatch_row_gemm<kEpiStore2>(umma_npad(n1 + n2), a, stream);
 }
 
-// CTAs of the weight gradient for n rows: >= ~512 rows each (every CTA writes
+// CTAs of the weight gradient for n rows: >= ~256 rows each (every CTA writes
 // a 4H x Npad partial the reduction reads back) and <= kWgRowsPerCta rows
 // each. The tensor core adds into its fp32 accumulator with truncation, so
 // the error of one CTA's partial grows with the rows it sums; capping them
@@ -1029,7 +1033,7 @@ constexpr int64_t kWgRowsPerCta = 8192;
 int wgrad_grid(int64_t n) {
   const int64_t cap = (n + kWgRowsPerCta - 1) / kWgRowsPerCta;
   if (cap > kNumSMs) return static_cast<int>((cap + kNumSMs - 1) / kNumSMs * kNumSMs);
-  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kNumSMs, n / 512)));
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kNumSMs, n / 256)));
 }
 
 int64_t umma_wgrad_workspace(int64_t n, int in, int H) {
