@@ -341,6 +341,16 @@ std::shared_ptr<AggResult> aggregate_scratch(const GraphView& graph, const float
   return r;
 }
 
+std::shared_ptr<AggResult> aggregate_zero_sum(const GraphView& graph, int32_t dim, cudaStream_t stream) {
+  auto r = alloc_result(AggrKind::kSum, graph.num_nodes, dim, stream);
+  r->num_edges = graph.num_edges;
+  r->t = graph.t;
+  const size_t nw = static_cast<size_t>(graph.num_nodes) * dim;
+  ProfScope ps(kProfAggScratch, stream, 4.0 * nw);
+  if (nw) DGNN_CUDA(cudaMemsetAsync(r->values.get(), 0, nw * sizeof(float), stream));
+  return r;
+}
+
 bool rebase_supported(const AggrFn& fn, int32_t dim, const float* feats) {
   return cuda::agg_delta_struct_supported(kind_i(fn.kind), dim, feats);
 }

@@ -109,6 +109,10 @@ std::shared_ptr<AggResult> aggregate_rebase(const AggResult& base, const GraphVi
                                             const float* feats, int32_t dim, const DevDelta& delta,
                                             const AggrFn& fn, cudaStream_t stream);
 
+// aggregate_scratch of an all-zero feature matrix under sum: zero values
+// without the SpMM (a GraphRNN's initial hidden state); false = not handled.
+std::shared_ptr<AggResult> aggregate_zero_sum(const GraphView& graph, int32_t dim, cudaStream_t stream);
+
 // Eq. 2 incremental update from prev (ref src/aggregate.cpp:117-207): the
 // new result is out of place (prev stays valid for its co-owners).
 IncrementalResult aggregate_incremental(const AggResult& prev, const GraphView& prev_graph,

@@ -511,7 +511,10 @@ ForwardArtifacts seq2seq_forward(DgnnModel& model, const SeqSample& sample, AggP
   const int D = cfg.layers;
   const bool lstm = cell_kind_of(cfg.arch) == CellKind::kLstm;
   std::vector<Buf> h(D), c;
-  for (int l = 0; l < D; ++l) h[l] = zero_buf(static_cast<size_t>(n) * cfg.hidden_dim, st);
+  for (int l = 0; l < D; ++l) {
+    h[l] = zero_buf(static_cast<size_t>(n) * cfg.hidden_dim, st);
+    provider.note_zero(h[l]->get());
+  }
   if (lstm) {
     c.resize(D);
     for (int l = 0; l < D; ++l) c[l] = zero_buf(static_cast<size_t>(n) * cfg.hidden_dim, st);
