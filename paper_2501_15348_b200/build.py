@@ -15,16 +15,23 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(ROOT, "build", "obj")
-OUT = os.path.join(PKG, "_dgnn_b200.so")
+BUILD = os.path.join(ROOT, "build", "obj_checked" if os.environ.get("DGNN_CHECKED") == "1" else "obj")
+OUT = os.path.join(PKG, "_dgnn_b200_checked.so" if os.environ.get("DGNN_CHECKED") == "1" else "_dgnn_b200.so")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# DGNN_CHECKED=1 builds the checked variant _dgnn_b200_checked.so (separate
+# objects): device-side bounds asserts in the aggregation kernels, CSR /
+# delta invariant checks after every device build, host asserts on. Selected
+# at run time with DGNN_LIB_PATH. It stands in for compute-sanitizer, which is
+# closed on this GPU pool.
+CHECKED = os.environ.get("DGNN_CHECKED") == "1"
+_NDEBUG = ["-DDGNN_CHECKED=1"] if CHECKED else ["-DNDEBUG"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                     "--expt-relaxed-constexpr", "-DNDEBUG"]
-CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-DNDEBUG", "-Wall", "-Wno-unused-function",
-             f"-I{CUDA}/include"]
+                     "--expt-relaxed-constexpr"] + _NDEBUG
+CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wno-unused-function",
+             f"-I{CUDA}/include"] + _NDEBUG
 
 
 def _sources():

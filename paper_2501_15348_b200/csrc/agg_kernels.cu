@@ -126,6 +126,7 @@ k_agg_scratch(int n, int w, int c0, int wc, const int64_t* __restrict__ ptr,
       for (int eb = 0; eb < maxdeg; eb += G) {
         const int my_e = eb + gl;
         const int32_t my_u = my_e < deg ? idx[beg + my_e] : 0;
+        DGNN_DCHECK(my_u >= 0 && my_u < n);
         const int cnt = min(G, maxdeg - eb);
         for (int j0 = 0; j0 < cnt; j0 += kUnroll) {
           float x[kUnroll][V];
@@ -338,6 +339,7 @@ k_agg_delta_v4(int n_rows, int w, int32_t num_nodes, const int32_t* __restrict__
       m.v = rows[r];
       m.beg = row_ptr[r];
       m.cnt = row_ptr[r + 1] - m.beg;
+      DGNN_DCHECK(m.v >= 0 && m.cnt >= 0);
     }
     return m;
   };
@@ -465,9 +467,11 @@ k_spmm_sum(int n, int w, const int64_t* __restrict__ ptr, const int32_t* __restr
         acc[u] = *reinterpret_cast<const float4*>(addend + v * w + c + 4 * G * u);
     }
     int32_t my_u = gl < deg ? idx[beg + gl] : 0;
+    DGNN_DCHECK(my_u >= 0 && my_u < n);
     for (int eb = 0; eb < maxdeg; eb += G) {
       // next batch's indices in flight with this batch's gathers
       const int32_t nxt_u = eb + G + gl < deg ? idx[beg + eb + G + gl] : 0;
+      DGNN_DCHECK(nxt_u >= 0 && nxt_u < n);
       const int cnt = min(G, maxdeg - eb);
       for (int j0 = 0; j0 < cnt; j0 += kUnroll) {
         float4 x[kUnroll][U];
@@ -564,6 +568,7 @@ k_agg_backward(int n, int w, int c0, int wc, const int64_t* __restrict__ ptr,
       for (int eb = 0; eb < maxdeg; eb += G) {
         const int my_e = eb + gl;
         const int32_t my_v = my_e < deg ? idx[beg + my_e] : 0;
+        DGNN_DCHECK(my_v >= 0 && my_v < n);
         float my_s = 1.f;
         if (MEAN && my_e < deg) my_s = 1.f / degree[my_v];
         const int cnt = min(G, maxdeg - eb);

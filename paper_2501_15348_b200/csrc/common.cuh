@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <stdexcept>
 #include <string>
 
@@ -21,6 +22,22 @@ inline void check(cudaError_t e, const char* what, const char* file, int line) {
 }
 
 #define DGNN_CUDA(call) ::dgnn::cuda::check((call), #call, __FILE__, __LINE__)
+
+// Device-side invariant checks of the checked build (DGNN_CHECKED=1, see
+// build.py): a failed check prints its condition and traps the kernel.
+#if defined(DGNN_CHECKED) && DGNN_CHECKED
+#define DGNN_DCHECK(cond)                                                                  \
+  do {                                                                                     \
+    if (!(cond)) {                                                                         \
+      printf("DGNN_DCHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond);                \
+      __trap();                                                                            \
+    }                                                                                      \
+  } while (0)
+#else
+#define DGNN_DCHECK(cond) \
+  do {                    \
+  } while (0)
+#endif
 
 #define DGNN_LAUNCH(kernel, grid, block, smem, stream, ...)                                \
   do {                                                                                      \

@@ -140,6 +140,23 @@ __global__ void k_composite(int64_t n, const uint64_t* __restrict__ keys, uint64
   }
 }
 
+// Checked build: CSR invariants of one direction (row pointers from 0 to E,
+// non-decreasing; indices in range and strictly ascending within a row).
+__global__ void k_check_csr(int32_t n, int64_t E, const int64_t* __restrict__ ptr,
+                            const int32_t* __restrict__ idx, int32_t* __restrict__ bad) {
+  for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; v < n;
+       v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = ptr[v], e = ptr[v + 1];
+    if (v == 0 && b != 0) atomicOr(bad, 1);
+    if (v == n - 1 && e != E) atomicOr(bad, 2);
+    if (e < b) atomicOr(bad, 4);
+    for (int64_t i = b; i < e && i < E; ++i) {
+      if (idx[i] < 0 || idx[i] >= n) atomicOr(bad, 8);
+      if (i > b && idx[i] <= idx[i - 1]) atomicOr(bad, 16);
+    }
+  }
+}
+
 // source-grouped twin of k_composite: source, then deletions before
 // insertions, then destination
 __global__ void k_composite_t(int64_t n, const uint64_t* __restrict__ keys, uint64_t is_ins,
@@ -730,6 +747,21 @@ void DeviceGraph::finish_snapshot(DevArray<uint64_t> keys, const float* prev_fea
   curr_swapped_ = std::move(swapped);
   if (snaps_.size() >= 2) build_delta(static_cast<int32_t>(snaps_.size()) - 1, prev_feats, feats, diff);
   prev_keys_.reset();
+#if defined(DGNN_CHECKED) && DGNN_CHECKED
+  {
+    const DevSnapshot& S = snaps_.back();
+    DevArray<int32_t> bad(1, stream_);
+    bad.zero(stream_);
+    if (n_ > 0) {
+      DGNN_LAUNCH(k_check_csr, grid_for(n_), kT, 0, stream_, n_, S.num_edges, S.in_ptr.get(), S.in_src.get(),
+                  bad.get());
+      DGNN_LAUNCH(k_check_csr, grid_for(n_), kT, 0, stream_, n_, S.num_edges, S.out_ptr.get(),
+                  S.out_dst.get(), bad.get());
+    }
+    const int32_t f = read_flag(bad, stream_);
+    if (f) throw std::runtime_error("checked build: CSR invariant violated (flags " + std::to_string(f) + ")");
+  }
+#endif
 }
 
 void DeviceGraph::build_delta(int32_t t, const float* prev_feats, const float* feats,
