@@ -107,6 +107,9 @@ void Worker::run_sample(const SequenceWindow& window, Timestep windows_remaining
     SeqSample sample =
         build_sample(graph_, model_.cfg_, window, windows_remaining, batch_id, node_range,
                      cfg_.seed, stream_);
+    // from-scratch runs (incremental = false, the ablation baseline) take no
+    // delta-based shortcut in the backward either
+    if (!cfg_.incremental) sample.graph = nullptr;
     prof_add_host(kProfHostBuild, since(h0));
     const auto h1 = clk::now();
     Lanes lanes(stream_, aux_);
