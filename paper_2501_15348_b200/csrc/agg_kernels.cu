@@ -666,6 +666,12 @@ int pick_group(int w, int vec) {
 // (n x wc fp32) is kept at or below an L2-resident budget so the ~E/N
 // re-gathers of every source row hit L2 instead of HBM; each slice re-reads
 // the index stream once. DGNN_SPMM_SLICES forces the slice count.
+// the SpMM slicing experiments are opt-in by environment (read once)
+bool spmm_slicing_requested() {
+  static const bool on = std::getenv("DGNN_SPMM_L2_MB") != nullptr || std::getenv("DGNN_SPMM_SLICES") != nullptr;
+  return on;
+}
+
 int spmm_slice_width(int n, int w, int vec) {
   static const int forced = [] {
     const char* e = std::getenv("DGNN_SPMM_SLICES");
@@ -679,7 +685,7 @@ int spmm_slice_width(int n, int w, int vec) {
   // Measured on B200 at C3 (1M x 64, 20M edges): 1 slice 0.84 ms, 2: 0.89,
   // 4: 1.04, 8: 2.07 — full-row 256 B gathers beat L2-resident 32-64 B ones,
   // so slicing is off unless an explicit L2 budget is requested.
-  if (std::getenv("DGNN_SPMM_L2_MB") == nullptr) return w;
+  if (!spmm_slicing_requested()) return w;
   int wc = w;
   while (static_cast<double>(n) * wc * 4.0 > budget && wc % (2 * vec) == 0 && wc / 2 >= 8) wc /= 2;
   return wc;
@@ -718,8 +724,7 @@ void agg_scratch(int kind, int n, int w, const int64_t* in_ptr, const int32_t* i
                  int32_t* argext, cudaStream_t stream) {
   if (n <= 0 || w <= 0) return;
   const int vec = pick_vec(w, feats, values);
-  if (kind == kAggSum && vec == 4 && std::getenv("DGNN_SPMM_L2_MB") == nullptr &&
-      std::getenv("DGNN_SPMM_SLICES") == nullptr) {
+  if (kind == kAggSum && vec == 4 && !spmm_slicing_requested()) {
     if (const int U = spmm_u(w)) {
       launch_spmm_sum(U, n, w, in_ptr, in_src, feats, values, nullptr, stream);
       return;
@@ -880,8 +885,7 @@ void agg_backward(int kind, int n, int w, const int64_t* out_ptr, const int32_t*
                   cudaStream_t stream, const float* addend) {
   if (n <= 0 || w <= 0) return;
   const int vec = std::min(pick_vec(w, up, grad), pick_vec(w, addend, nullptr));
-  if (kind == kAggSum && vec == 4 && std::getenv("DGNN_SPMM_L2_MB") == nullptr &&
-      std::getenv("DGNN_SPMM_SLICES") == nullptr) {
+  if (kind == kAggSum && vec == 4 && !spmm_slicing_requested()) {
     if (const int U = spmm_u(w)) {
       launch_spmm_sum(U, n, w, out_ptr, out_dst, up, grad, addend, stream);
       return;
