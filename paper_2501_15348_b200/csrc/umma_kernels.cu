@@ -402,10 +402,24 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
     const bool split = kEpiCell<EPI> && p.split_acc;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const uint32_t b = split ? 0u : (it & 1u);
-      mbar_wait(&tfull[b], split ? (it & 1u) : ((it >> 1) & 1u));
-      fence_after_sync();
       const int64_t row0 = static_cast<int64_t>(tile) * kTileM + q * 32;  // this warp's 32 rows
       const int64_t row = row0 + lane;
+      if (kEpiCell<EPI> && row < p.M) {
+        // the per-row state operands do not depend on the MMAs: pull this
+        // lane's segment of them into L1 while the tile's MMAs run (the
+        // epilogue's global loads were its largest stall, ncu long_scoreboard)
+        const int64_t off = row * p.H + half * (p.H / 2);
+        auto pf = [](const float* ptr) {
+          if (ptr) asm volatile("prefetch.global.L1 [%0];" ::"l"(ptr));
+        };
+        pf((EPI == kEpiLstm || EPI == kEpiLstmBwd) ? p.c_prev + off : p.h_skip + off);
+        if (EPI == kEpiLstmBwd || EPI == kEpiGruBwd) {
+          pf(p.dh + off);
+          if (EPI == kEpiLstmBwd && p.dc) pf(p.dc + off);
+        }
+      }
+      mbar_wait(&tfull[b], split ? (it & 1u) : ((it >> 1) & 1u));
+      fence_after_sync();
       const uint32_t trow = tmem + b * 256 + (static_cast<uint32_t>(q * 32) << 16);
       // the four gate blocks of hidden units [j0, j0 + 16): hi*hi sums (+ the
       // correction sums when split)
@@ -1023,7 +1037,7 @@ void umma_gemm_store2(int n, int K, const float* A, const float* Bimg, int n1, i
   dispatch_row_gemm<kEpiStore2>(umma_npad(n1 + n2), a, stream);
 }
 
-// CTAs of the weight gradient for n rows: >= ~256 rows each (every CTA writes
+// CTAs of the weight gradient for n rows: >= ~128 rows each (every CTA writes
 // a 4H x Npad partial the reduction reads back) and <= kWgRowsPerCta rows
 // each. The tensor core adds into its fp32 accumulator with truncation, so
 // the error of one CTA's partial grows with the rows it sums; capping them
@@ -1033,7 +1047,7 @@ constexpr int64_t kWgRowsPerCta = 8192;
 int wgrad_grid(int64_t n) {
   const int64_t cap = (n + kWgRowsPerCta - 1) / kWgRowsPerCta;
   if (cap > kNumSMs) return static_cast<int>((cap + kNumSMs - 1) / kNumSMs * kNumSMs);
-  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kNumSMs, n / 256)));
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kNumSMs, n / 128)));
 }
 
 int64_t umma_wgrad_workspace(int64_t n, int in, int H) {
