@@ -308,7 +308,7 @@ __device__ __forceinline__ float4 ld_hint(const float* p, uint64_t pol) {
 // instead of three. Entries are applied in the reference's order (deletions,
 // then insertions, ascending source); with the compact block a persisting
 // changed-source pair is one entry (its difference row) at the deletion's place.
-template <int G, int U, bool MEAN, int MINB = 1, bool STRUCT = false>
+template <int G, int U, bool MEAN, int MINB = 1, bool STRUCT = false, int KU = kUnroll>
 __global__ void __launch_bounds__(kThreads, MINB)
 k_agg_delta_v4(int n_rows, int w, int32_t num_nodes, const int32_t* __restrict__ rows,
                const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ ent,
@@ -365,11 +365,11 @@ k_agg_delta_v4(int n_rows, int w, int32_t num_nodes, const int32_t* __restrict__
     for (int eb = 0; eb < maxcnt; eb += G) {
       const int32_t my_s = eb == 0 ? e0 : (eb + gl < m0.cnt ? ent[m0.beg + eb + gl] : 0);
       const int cnt = min(G, maxcnt - eb);
-      for (int j0 = 0; j0 < cnt; j0 += kUnroll) {
-        float4 x[kUnroll][U];
-        int32_t s[kUnroll];
+      for (int j0 = 0; j0 < cnt; j0 += KU) {
+        float4 x[KU][U];
+        int32_t s[KU];
 #pragma unroll
-        for (int q = 0; q < kUnroll; ++q) {
+        for (int q = 0; q < KU; ++q) {
           s[q] = __shfl_sync(0xffffffffu, my_s, (j0 + q) & (G - 1), G);
           if (valid && cact && j0 + q < cnt && eb + j0 + q < m0.cnt &&
               !(STRUCT && s[q] < 0 && ~s[q] >= num_nodes)) {
@@ -385,7 +385,7 @@ k_agg_delta_v4(int n_rows, int w, int32_t num_nodes, const int32_t* __restrict__
           }
         }
 #pragma unroll
-        for (int q = 0; q < kUnroll; ++q) {
+        for (int q = 0; q < KU; ++q) {
           if (!(valid && j0 + q < cnt && eb + j0 + q < m0.cnt)) continue;
           if (STRUCT && s[q] < 0 && ~s[q] >= num_nodes) continue;  // persisting pair: cancels
           // a compact-block deletion is a folded (deletion, insertion) pair
