@@ -885,7 +885,14 @@ void launch_row_gemm(const RowGemmArgs& a, cudaStream_t st) {
     configured = true;
   }
   const int ntiles = (a.M + kTileM - 1) / kTileM;
-  const int grid = ntiles < kNumSMs ? ntiles : kNumSMs;
+  // DGNN_GEMM_SMS caps the persistent grid (experiments: leaving SMs to a
+  // concurrent SpMM on the other layer lane)
+  static const int cap = [] {
+    const char* e = std::getenv("DGNN_GEMM_SMS");
+    const int v = e ? std::atoi(e) : kNumSMs;
+    return v > 0 && v <= kNumSMs ? v : kNumSMs;
+  }();
+  const int grid = ntiles < cap ? ntiles : cap;
   DGNN_LAUNCH((k_row_gemm<EPI, NPAD>), grid, kRgThreads, smem, st, a);
 }
 
