@@ -186,8 +186,10 @@ namespace {
 // row tile (linear_wgrad_h)
 int linear_wgrad_h(const LinearSlot& l) { return l.out <= 128 ? 32 : 64; }
 void set_linear_umma(LinearSlot& l, cudaStream_t stream) {
-  l.umma = cuda::umma_enabled() && l.in % 16 == 0 && l.out % 16 == 0 && l.out <= 256;
-  l.umma_wgrad = l.umma && l.in % 4 == 0 && l.in + linear_wgrad_h(l) <= 192;
+  // any width up to the row GEMM's N = 256 (narrow / odd widths, e.g. C2's
+  // 2-feature head, take the element-copy producer and store epilogue)
+  l.umma = cuda::umma_enabled() && l.in >= 1 && l.out >= 1 && l.out <= 256 && l.in <= 256;
+  l.umma_wgrad = l.umma && l.out <= 256 && l.in + linear_wgrad_h(l) <= 192;
   if (l.umma) {
     l.Bf = cuda::DevArray<float>(cuda::umma_bimage_floats(l.out, l.in), stream);
     l.Bb = cuda::DevArray<float>(cuda::umma_bimage_floats(l.in, l.out), stream);

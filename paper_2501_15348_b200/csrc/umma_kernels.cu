@@ -144,6 +144,8 @@ struct RowGemmArgs {
   // forward-kernel cost from re-reading / re-splitting A, and slower in the
   // C4 epoch, so not kept.)
   int split_acc;
+  // A rows are not 16 B multiples (k1 % 4 or k2 % 4 != 0): element copies
+  int scalar_a;
   // profiling switches (env DGNN_UMMA_DEBUG): 1 skip epilogue math/stores,
   // 2 skip the B copy, 4 skip the A split/stores
   int debug;
@@ -213,6 +215,11 @@ __device__ __forceinline__ void cp_async16_zfill(uint32_t saddr, const void* g, 
   const int n = valid ? 16 : 0;
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(n) : "memory");
 }
+// 4-byte element copy (operands whose rows are not 16 B multiples)
+__device__ __forceinline__ void cp_async4_zfill(uint32_t saddr, const void* g, bool valid) {
+  const int n = valid ? 4 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(saddr), "l"(g), "r"(n) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -273,11 +280,27 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
         const float* base = k < p.k1 ? p.A1 + k : p.A2 + (k - p.k1);
         const int64_t ld = k < p.k1 ? p.k1 : p.k2;
         const uint32_t slot = raw0 + is_slot * S::kRaw + tid * 16;
+        if (p.scalar_a) {
+          // rows not 16 B multiples (K = in + H with in % 4 != 0, or a narrow
+          // A1 alone): element copies, each k from its own operand
 #pragma unroll
-        for (int it = 0; it < kRawPerThread; ++it) {
-          const int64_t grow = r0 + kProducerRows * it;
-          const bool valid = kin && grow < p.M;
-          cp_async16_zfill(slot + it * kProducerThreads * 16, valid ? base + grow * ld : p.A1, valid);
+          for (int it = 0; it < kRawPerThread; ++it) {
+            const int64_t grow = r0 + kProducerRows * it;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int ke = k + e;
+              const bool valid = ke < p.K && grow < p.M;
+              const float* src = ke < p.k1 ? p.A1 + grow * p.k1 + ke : p.A2 + grow * p.k2 + (ke - p.k1);
+              cp_async4_zfill(slot + it * kProducerThreads * 16 + 4 * e, valid ? src : p.A1, valid);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int it = 0; it < kRawPerThread; ++it) {
+            const int64_t grow = r0 + kProducerRows * it;
+            const bool valid = kin && grow < p.M;
+            cp_async16_zfill(slot + it * kProducerThreads * 16, valid ? base + grow * ld : p.A1, valid);
+          }
         }
         if (++is_chunk == p.nchunks) {
           is_chunk = 0;
@@ -623,17 +646,38 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
         }
       } else {
         const int ncol = p.n1 + p.n2;
+        const bool vec = p.n1 % 4 == 0 && p.n2 % 4 == 0 && p.bias == nullptr && !p.store_accumulate && !p.relu;
         for (int cb = half * 8; cb < ncol; cb += 16) {
           float a[8];
           tmem_ld8(trow + cb, a);
           tmem_wait_ld();
           if (row < p.M) {
+            if (vec) {
 #pragma unroll
-            for (int u = 0; u < 8; u += 4) {
-              const int col = cb + u;
-              if (col < ncol) {
-                float* dst = col < p.n1 ? p.C1 + row * p.n1 + col : p.C2 + row * p.n2 + (col - p.n1);
-                *reinterpret_cast<float4*>(dst) = make_float4(a[u], a[u + 1], a[u + 2], a[u + 3]);
+              for (int u = 0; u < 8; u += 4) {
+                const int col = cb + u;
+                if (col < ncol) {
+                  float* dst = col < p.n1 ? p.C1 + row * p.n1 + col : p.C2 + row * p.n2 + (col - p.n1);
+                  *reinterpret_cast<float4*>(dst) = make_float4(a[u], a[u + 1], a[u + 2], a[u + 3]);
+                }
+              }
+            } else {
+              // narrow / odd widths (e.g. a prediction head with d = 2):
+              // element stores with the bias / accumulate / ReLU epilogue
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const int col = cb + u;
+                if (col >= ncol) continue;
+                if (col < p.n1) {
+                  float v = a[u];
+                  if (p.bias != nullptr) v += sbias[col];
+                  float* dst = p.C1 + row * p.n1 + col;
+                  if (p.store_accumulate) v += *dst;
+                  if (p.relu) v = v > 0.f ? v : 0.f;
+                  *dst = v;
+                } else {
+                  p.C2[row * p.n2 + (col - p.n1)] = a[u];
+                }
               }
             }
           }
@@ -730,6 +774,14 @@ k_wgrad(int M, int in, int H, const float* __restrict__ G, const float* __restri
     // The 16 rows of each operand are one contiguous block in global memory, so
     // each region is a linear copy; rows past `re` are zero-filled.
     auto copy_region = [&](uint32_t dst, const float* src, int width, int live_rows) {
+      if (width % 4 != 0) {  // narrow operand (d = 2 input, a 2-wide head gradient): elements
+        const int n1 = kKW * width, valid1 = live_rows * width;
+        for (int f = tid; f < n1; f += kWgConv) {
+          const bool valid = f < valid1;
+          cp_async4_zfill(dst + f * 4, valid ? src + f : src, valid);
+        }
+        return;
+      }
       const int n4 = kKW * width / 4, valid4 = live_rows * width / 4;
       for (int f = tid; f < n4; f += kWgConv) {
         const bool valid = f < valid4;
@@ -918,8 +970,9 @@ bool umma_enabled() {
 }
 
 bool umma_cell_supported(int in, int H) {
-  // in + H <= 192: the weight-gradient kernel's raw [X | Hm] staging slot
-  return umma_enabled() && (H == 32 || H == 64) && in % 4 == 0 && in >= 4 && in + H <= 192;
+  // in + H <= 192: the weight-gradient kernel's raw [X | Hm] staging slot;
+  // any in >= 1 (rows that are not 16 B multiples are copied by element)
+  return umma_enabled() && (H == 32 || H == 64) && in >= 1 && in + H <= 192;
 }
 
 int umma_npad(int N) { return N <= 64 ? 64 : (N <= 128 ? 128 : (N <= 192 ? 192 : 256)); }
@@ -977,6 +1030,7 @@ void umma_cell_forward(bool lstm, int n, int in, int H, const float* X, const fl
   a.h_out = h;
   a.gru_split = umma_gru_split(lstm, in, H) ? H : 0;
   a.split_acc = umma_split_acc() & 1;
+  a.scalar_a = in % 4 != 0;
   a.debug = umma_debug_flags();
   const int npad = umma_npad(4 * H);
   if (lstm) dispatch_row_gemm<kEpiLstm>(npad, a, stream);
@@ -1006,6 +1060,7 @@ void umma_cell_backward_recompute(bool lstm, int n, int in, int H, const float* 
   a.dstate = dstate;
   a.gru_split = umma_gru_split(lstm, in, H) ? H : 0;
   a.split_acc = (umma_split_acc() >> 1) & 1;
+  a.scalar_a = in % 4 != 0;
   a.debug = umma_debug_flags();
   const int npad = umma_npad(4 * H);
   if (lstm) dispatch_row_gemm<kEpiLstmBwd>(npad, a, stream);
@@ -1015,9 +1070,9 @@ void umma_cell_backward_recompute(bool lstm, int n, int in, int H, const float* 
 void umma_gemm_store2(int n, int K, const float* A, const float* Bimg, int n1, int n2, float* C1,
                       float* C2, cudaStream_t stream, const float* bias, bool accumulate, int gru_h,
                       bool relu) {
-  if ((bias || accumulate || relu) && !(n1 % 16 == 0 && n2 % 16 == 0 && n1 <= 256))
-    throw std::invalid_argument("umma_gemm_store2: bias / accumulate / relu need 16-column blocks");
+  if (n1 > 256) throw std::invalid_argument("umma_gemm_store2: at most 256 bias columns");
   RowGemmArgs a{};
+  a.scalar_a = K % 4 != 0;
   a.bias = bias;
   a.relu = relu ? 1 : 0;
   a.store_accumulate = accumulate ? 1 : 0;
@@ -1067,6 +1122,7 @@ void umma_wgrad(int n, int in, int H, const float* G, const float* X, const floa
                 int nb, float* db, float* ws, cudaStream_t stream, int gw) {
   if (gw <= 0) gw = 4 * H;
   if (gw > 4 * H) throw std::invalid_argument("umma_wgrad: G wider than 4H");
+  if (n <= 0) return;  // no rows: nothing to accumulate
   const int need = round_up(in + H + 1, 16);
   const int npad = need <= 144 ? 144 : (need <= 208 ? 208 : 256);
   const int grid = wgrad_grid(n);

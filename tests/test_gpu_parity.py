@@ -388,6 +388,30 @@ def test_sample_grads_tensor_core_head(ref, api, arch, dim):
         assert nrel(grads, grads_r) < 1e-4
 
 
+@pytest.mark.parametrize("arch,dim", [("gcrn_m2", 2), ("tgcn", 2), ("gcrn_m2", 6), ("gcrn_m1", 2)])
+def test_narrow_features_on_tensor_cores(ref, api, arch, dim):
+    """C2's shapes (d = 2, hidden 64; a 207-node METR-LA-shaped graph where
+    every node's features change every step): the layer-1 cell with a
+    2-wide input, the 2-wide prediction head and (stacked) the GCN layer run
+    on tcgen05 — element-copy producers for rows that are not 16 B multiples,
+    element stores for the narrow head — against the reference: sample
+    gradients and a short epoch."""
+    g_ref, g = make_pair(ref, api, n=207, avg_degree=1515 / 207, dim=dim, T=13, edge=0.0, feat=1.0, seed=2)
+    cfg_r = ref.RunCfg(arch=arch, hidden=64)
+    s = api.TrainSession(g, api.TrainConfig(arch=arch, hidden=64))
+    for w in (0, 2):
+        loss_r, pred_r, grads_r = g_ref.sample_grads(cfg_r, w)
+        loss, pred, grads = s.sample_grads(w)
+        assert abs(loss - loss_r) <= 1e-5 * abs(loss_r), (loss, loss_r)
+        assert nrel(pred, pred_r) < 1e-5
+        assert nrel(grads, grads_r) < 1e-4
+    r = g_ref.run(ref.RunCfg(arch=arch, hidden=64, epochs=1, optimizer="sgd", lr=0.01))
+    s2 = api.TrainSession(g, api.TrainConfig(arch=arch, hidden=64, optimizer="sgd", lr=0.01))
+    losses = s2.run_epoch()["sample_losses"]
+    assert nrel(losses, r.losses) < 1e-4
+    assert np.array_equal(s2.invocations(), r.invocations[:, 1:])
+
+
 def test_spmm_column_slices_match_reference(ref):
     """The L2 column-sliced pull SpMMs (forced to 2 and 4 slices) in a fresh
     process, against the reference."""
