@@ -58,6 +58,34 @@ def load_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
+def measure_tf32_peak():
+    """Dense TF32 tensor-core throughput on this GPU, the MEASURED_PEAKS method
+    applied to fp32 with TF32 allowed: torch.matmul 8192^3 (2 N^3 flops), best
+    of 10 after 3 warm-ups, CUDA events. The cell GEMMs' tensor-pipe
+    denominator (each of their 3xTF32 products is one TF32 GEMM)."""
+    import torch
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        n = 8192
+        a = torch.randn(n, n, device="cuda")
+        b = torch.randn(n, n, device="cuda")
+        for _ in range(3):
+            torch.matmul(a, b)
+        best = float("inf")
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        del a, b
+        return 2.0 * n ** 3 / (best / 1e3) / 1e12
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
@@ -245,6 +273,12 @@ def main():
         if world > 1:
             dist.barrier()
 
+    try:
+        tf32_peak = measure_tf32_peak()
+    except Exception as e:  # noqa: BLE001 — report, do not fail the bench
+        log(f"tf32 peak measurement failed: {e}")
+        tf32_peak = None
+    torch.cuda.empty_cache()
     t0 = time.perf_counter()
     synth = api.Synth(wl["n"], wl["deg"], wl["dim"], wl["T"], wl["edge"], wl["feat"], seed=1)
     t_synth = time.perf_counter() - t0
@@ -320,20 +354,24 @@ def main():
     # kernel reported (and the one whose ncu DRAM traffic is in profiles/)
     if dom == "agg_scratch" and prof["agg_backward"]["ms"] >= 0.97 * prof["agg_scratch"]["ms"]:
         dom = "agg_backward"
-    # kernel names in the committed ncu capture (profiles/r1_ncu_spmm_<workload>.json,
-    # made by scripts/kernel_bench.py at the workload's shapes)
-    ncu_kernels = {"agg_backward": "k_spmm_sum<4, 4>", "agg_delta": "k_agg_delta"}
+    # kernel names in the committed ncu captures (profiles/r2_ncu_*.json: `ncu --set
+    # full` of the C4 bench / scripts/kernel_bench.py at C4 shapes)
+    ncu_kernels = {"agg_backward": "k_spmm_sum<4, 4>", "agg_scratch": "k_spmm_sum<4, 4>",
+                   "agg_delta": "k_agg_delta_v4<8, 4", "cell_bwd": "k_row_gemm<4, 256>",
+                   "cell_fwd": "k_row_gemm<1, 256>", "weight_grad": "k_wgrad_mn<256, 208>"}
+    ncu_files = ["r2_ncu_full_c4.json", "r2_ncu_row_gemm_epi4.json", "r2_ncu_row_gemm_epi1.json",
+                 "r2_ncu_wgrad_mn_c4.json"]
 
     def ncu_traffic(name):
         """DRAM bytes per launch (dram__bytes_read + write) of this kernel from
-        the committed `ncu --set full` capture of the same workload, or None."""
-        fname = f"r1_ncu_spmm_{args.workload}.json"
-        if name == "agg_delta" and args.workload == "c4":
-            fname = "r1_ncu_delta_v7.json"  # the folded-layout K2 at the C4 delta shape
-        path = os.path.join(ROOT, "profiles", fname)
-        if name not in ncu_kernels or not os.path.exists(path):
+        the committed `ncu --set full` captures of the C4 shapes, or None."""
+        if args.workload != "c4" or name not in ncu_kernels:
             return None
-        rows = [e for e in json.load(open(path)) if ncu_kernels[name] in e.get("kernel", "")]
+        rows = []
+        for fname in ncu_files:
+            path = os.path.join(ROOT, "profiles", fname)
+            if os.path.exists(path):
+                rows += [e for e in json.load(open(path)) if ncu_kernels[name] in e.get("kernel", "")]
         if not rows:
             return None
         return round(1e9 * statistics.mean(e["dram_read_GB"] + e["dram_write_GB"] for e in rows))
@@ -364,6 +402,18 @@ def main():
 
     roofline = roof(dom)
     delta_roof = roof("agg_delta")
+    # the cell GEMMs against both their bounds: algorithmic HBM bytes and the
+    # tensor pipe (3 TF32 products per fp32 product, against the measured TF32 peak)
+    gemm_roof = {}
+    for name in ("cell_fwd", "cell_bwd", "cell_bwd_gemm", "weight_grad"):
+        r = roof(name)
+        if r is None or not prof[name]["flops"]:
+            continue
+        tf = 3 * prof[name]["flops"] / (prof[name]["ms"] / 1e3) / 1e12
+        gemm_roof[name] = {"hbm_frac": r["frac"], "dram_frac": r.get("dram_frac"),
+                           "tf32_tflops_issued": round(tf, 1),
+                           "tensor_frac": round(tf / tf32_peak, 4) if tf32_peak else None,
+                           "avg_launch_us": r["avg_launch_us"]}
 
     free_b, total_b = torch.cuda.mem_get_info()
     st = sess.stats()
@@ -440,6 +490,9 @@ def main():
                        "l2": f"inputs exceed the 126 MB L2 (graph store {memory['graph_store_gb']} GB; "
                              f"one feature matrix {wl['n'] * wl['dim'] * 4 / 1e9:.2f} GB)"},
             "roofline": roofline, "roofline_delta_spmm": delta_roof,
+            "roofline_gemms": {"tf32_peak_tflops": round(tf32_peak, 1) if tf32_peak else None,
+                               "tf32_peak_source": "measured in this run (torch.matmul fp32 with TF32, "
+                                                   "8192^3, best of 10)", **gemm_roof},
             "kernel_ms_by_class": {k: round(v["ms"] / prof_steps, 2) for k, v in prof.items()},
             "profiled": "timed steps" if args.prof_in_timed else "one extra step after the timed ones",
             "host_ms_per_sample": {k: round(v["ms"] / max(scopes["sample_host"]["launches"], 1), 3)
