@@ -9,8 +9,8 @@
 // "MN-major": a 16-row chunk of G (row-major, n x gw) is already the K x M
 // tile the tensor core wants, and likewise X and Hm. The TMA engine copies
 // each chunk straight from the row-major activations into MN-major
-// 128 B-swizzled, 32 B-granule atoms (box = 32 columns x 16 rows); the tensor core reads those
-// raw fp32 tiles as the TF32 "hi" operand (it uses the top 19 bits, i.e.
+// 128 B-swizzled, 32 B-granule atoms (box = 32 columns x 16 rows); the tensor
+// core reads those raw fp32 tiles as the TF32 "hi" operand (top 19 bits, i.e.
 // trunc_tf32), and converter warps write only the "lo" = x - trunc(x) tiles,
 // elementwise at the same swizzled offsets — no transposition, no per-element
 // shuffling through registers. 3xTF32: hi*hi + hi*lo + lo*hi.
@@ -32,6 +32,7 @@
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 
 #include "common.cuh"
 #include "umma.cuh"
@@ -336,8 +337,6 @@ int umma_wgrad_mn(int64_t n, int in, int H, const float* G, int gw, const float*
     }
     DGNN_LAUNCH((k_wgrad_mn<MG, NP>), grid, kThreadsMn, smem, stream, tg, tx, th, n, gw, xa, ha, per, ws);
   };
-  using I = std::integral_constant<int, 0>;
-  (void)sizeof(I);
   if (H == 64) {
     if (npad == 144) go(std::integral_constant<int, 256>{}, std::integral_constant<int, 144>{});
     else if (npad == 208) go(std::integral_constant<int, 256>{}, std::integral_constant<int, 208>{});
