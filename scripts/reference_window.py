@@ -2,7 +2,7 @@
 whole epoch of (C3: ~43 GB of materialised fp64 snapshots for 32 snapshots;
 C4: ~348 GB): the compiled reference (oracle/_ref, 1 thread) runs its
 seq-first / distsim epoch on the workload's exact graph (N, E, d, h, churn)
-truncated to T = L + H + 2 = 11 snapshots, i.e. the first 2 windows of the
+truncated to T = L + H + 1 = 10 snapshots, i.e. the first window of the
 epoch at full size — no scaling in N. snapshots/s = windows x (L + H) /
 EpochReport.seconds (ref src/train.cpp:151, :203-204).
 usage: python scripts/reference_window.py c3 > profiles/r2_reference_window_c3.json"""
@@ -21,7 +21,7 @@ from oracle import refbind as R  # noqa: E402
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "c3"
     wl = WORKLOADS[name]
-    T = L + H + 2
+    T = L + H + 1  # sliding_windows(T - 1, L, S, H): exactly one window
     t0 = time.time()
     g = R.RefGraph.synth(wl["n"], wl["deg"], wl["dim"], T, wl["edge"], wl["feat"], seed=1)
     t_synth = time.time() - t0
@@ -30,8 +30,8 @@ def main():
     print(json.dumps({"impl": "reference", "workload": name, "desc": wl["desc"], "snapshots": T,
                       "windows": len(r.losses), "epoch_seconds": r.seconds, "snapshots_per_s": rate,
                       "synth_seconds": round(t_synth, 1), "cores": 1, "sample_losses": list(r.losses),
-                      "note": "full-size graph (N, E, d, h, churn of the workload), first T = L+H+2 "
-                              "snapshots: the epoch's first windows, timed by the reference's own clock",
+                      "note": "full-size graph (N, E, d, h, churn of the workload), first T = L+H+1 "
+                              "snapshots: the epoch's first window, timed by the reference's own clock",
                       **host_cpu()}))
 
 
