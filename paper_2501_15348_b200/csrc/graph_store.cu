@@ -2,6 +2,8 @@
 // Integer work only; every output is bit-exact with the reference
 // (src/snapshot.cpp:20-154). Sorting/selection/scans use CUB (CUDA toolkit
 // library primitives); the graph-specific passes are the kernels below.
+#include <chrono>
+#include <map>
 #include <cub/cub.cuh>
 #include <cub/device/device_merge.cuh>
 
@@ -297,6 +299,26 @@ __global__ void k_sub_inplace(int64_t n, float* __restrict__ dst, const float* _
 
 int grid_for(int64_t n) { return cuda::wave_grid(n, kT, 8); }
 
+// DGNN_BUILD_PROF=1: host-side phase timing of the device graph build (each
+// mark synchronises the build stream), printed by release_build_state
+struct BuildProf {
+  bool on = std::getenv("DGNN_BUILD_PROF") != nullptr;
+  std::map<std::string, double> ms;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* phase, cudaStream_t st) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    ms[phase] += std::chrono::duration<double, std::milli>(now - t).count();
+    t = now;
+  }
+  void restart() { t = std::chrono::steady_clock::now(); }
+};
+BuildProf& build_prof() {
+  static BuildProf p;
+  return p;
+}
+
 // Thin CUB wrappers with a growable temp buffer.
 struct Cub {
   cudaStream_t st;
@@ -569,11 +591,13 @@ void DeviceGraph::add_delta(const int32_t* del_src, const int32_t* del_dst, int6
   cudaStream_t st = stream_;
   // the previous build step's temporaries (sizes drift per snapshot) go back
   // to the pool instead of accumulating in the per-size free lists
+  build_prof().restart();
   cuda::release_stream_blocks(st);
   ensure_build_keys();
   Cub cub(st);
   DevArray<uint64_t> del = sorted_edge_keys(del_src, del_dst, n_del, n_, cub, false);
   DevArray<uint64_t> ins = sorted_edge_keys(ins_src, ins_dst, n_ins, n_, cub, true);
+  build_prof().mark("upload+sort delta keys", st);
   const int64_t E0 = static_cast<int64_t>(curr_keys_.size());
   // Incremental snapshot build: the work scales with |D| + |I| plus two
   // linear select / merge passes, not with sorts or searches over E.
@@ -617,6 +641,7 @@ void DeviceGraph::add_delta(const int32_t* del_src, const int32_t* del_dst, int6
     cub.merge(sw_kept.get(), nsk, swi_sorted.get(), ni, sw_new.get());
   }
   keep.reset();
+  build_prof().mark("merge (src,dst) and (dst,src) keys", st);
   // exact structural change for extract_delta: removed = (prev ∩ D) \ I, added = I \ prev
   StructDiff diff;
   {
@@ -639,6 +664,7 @@ void DeviceGraph::add_delta(const int32_t* del_src, const int32_t* del_dst, int6
       diff.n_added = cub.select_flagged(ins.get(), f.get(), diff.added.get(), n_ins);
     }
   }
+  build_prof().mark("structural diff", st);
   // features: prev rows with the changed rows replaced
   const int64_t nf = static_cast<int64_t>(n_) * d_;
   const int32_t t = length();
@@ -651,6 +677,7 @@ void DeviceGraph::add_delta(const int32_t* del_src, const int32_t* del_dst, int6
     DGNN_LAUNCH(k_scatter_rows, grid_for(n_changed * d_), kT, 0, st, n_changed, d_, nodes.get(),
                 rows.get(), cur->buf.get());
   }
+  build_prof().mark("features", st);
   finish_snapshot(std::move(exact), prev->get(), cur->buf.get(), std::move(sw_new), &diff);
   cur->t = t;
   cur->writer = st;
@@ -688,6 +715,10 @@ void DeviceGraph::ensure_build_keys() {
 
 void DeviceGraph::release_build_state() {
   DGNN_CUDA(cudaStreamSynchronize(stream_));
+  if (build_prof().on) {
+    for (const auto& [k, v] : build_prof().ms) std::fprintf(stderr, "[dgnn build] %-40s %9.1f ms\n", k.c_str(), v);
+    build_prof().ms.clear();
+  }
   curr_keys_.reset();
   curr_swapped_.reset();
   prev_keys_.reset();
@@ -741,11 +772,13 @@ void DeviceGraph::finish_snapshot(DevArray<uint64_t> keys, const float* prev_fea
     swapped.reset();
     snaps_.push_back(csr_from_keys(keys.get(), E, n_, stream_, nullptr, &swapped));
   }
+  build_prof().mark("CSRs", stream_);
   deltas_.emplace_back();
   prev_keys_ = std::move(curr_keys_);
   curr_keys_ = std::move(keys);
   curr_swapped_ = std::move(swapped);
   if (snaps_.size() >= 2) build_delta(static_cast<int32_t>(snaps_.size()) - 1, prev_feats, feats, diff);
+  build_prof().mark("extract_delta + delta layouts", stream_);
   prev_keys_.reset();
 #if defined(DGNN_CHECKED) && DGNN_CHECKED
   {
