@@ -61,6 +61,10 @@ int dgnn_graph_add_delta(dgnn_graph* g, const int32_t* del_src, const int32_t* d
                          int64_t n_ins, const int32_t* changed_nodes, int64_t n_changed,
                          const float* changed_feats);
 int32_t dgnn_graph_length(const dgnn_graph* g);
+/* Keep only snapshots / deltas / feature versions [t_first, t_last] (a rank's
+ * window block plus the L+H overlap: replicate_overlap, inc/distsim.hpp:49-54);
+ * indices stay global, access outside the range is status 2 (out_of_range). */
+int dgnn_graph_retain(dgnn_graph* g, int32_t t_first, int32_t t_last);
 int64_t dgnn_graph_num_edges(const dgnn_graph* g, int32_t t);
 /* HBM held by the graph store (CSRs, deltas, feature versions and patches);
  * the feature-version slot budget and how many versions were materialised. */

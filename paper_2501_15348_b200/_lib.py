@@ -105,6 +105,7 @@ SIGNATURES = {
     "dgnn_session_apply": (C.c_int, [P, P, C.POINTER(I32)]),
     "dgnn_session_end_epoch": (C.c_int, [P]),
     "dgnn_set_device": (C.c_int, [I32]),
+    "dgnn_graph_retain": (C.c_int, [P, I32, I32]),
     "dgnn_comm_unique_id": (C.c_int, [P]),
     "dgnn_comm_create": (C.c_int, [P, I32, I32, C.POINTER(P)]),
     "dgnn_comm_free": (None, [P]),

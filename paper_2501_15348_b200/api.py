@@ -352,6 +352,23 @@ class DynamicGraph:
     def length(self) -> int:
         return lib().dgnn_graph_length(self.h)
 
+    def retain(self, t_first: int, t_last: int):
+        """Keep only snapshots [t_first, t_last] in HBM (a rank's window block
+        plus the L+H overlap); indices stay global."""
+        check(lib().dgnn_graph_retain(self.h, t_first, t_last))
+
+    def retain_for_rank(self, world: int, rank: int, L: int, S: int, H: int):
+        """retain() the snapshots rank `rank` of a consecutive-block plan over
+        sliding_windows(length - 1, L, S, H) reads (windows, their targets)."""
+        row = plan(self.length() - 1, world, L, S, H)[rank]
+        wb, we = int(row[2]), int(row[3])
+        if we <= wb:  # no windows on this rank: keep everything
+            return 0, self.length() - 1
+        starts = sliding_windows(self.length() - 1, L, S, H)
+        first, last = starts[wb], min(self.length() - 1, starts[we - 1] + L + H)
+        self.retain(first, last)
+        return first, last
+
     def device_bytes(self) -> int:
         return lib().dgnn_graph_device_bytes(self.h)
 

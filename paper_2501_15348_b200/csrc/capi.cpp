@@ -211,6 +211,10 @@ int dgnn_graph_add_delta(dgnn_graph* g, const int32_t* del_src, const int32_t* d
   });
 }
 
+int dgnn_graph_retain(dgnn_graph* g, int32_t t_first, int32_t t_last) {
+  return guarded([&] { g->g->retain(t_first, t_last); });
+}
+
 int32_t dgnn_graph_length(const dgnn_graph* g) { return g->g->length(); }
 
 int64_t dgnn_graph_num_edges(const dgnn_graph* g, int32_t t) {

@@ -501,6 +501,7 @@ std::shared_ptr<FeatSlot> DeviceGraph::free_slot(cudaStream_t stream) const {
 
 FeatRef DeviceGraph::features(int32_t t, cudaStream_t stream) const {
   if (t < 0 || t >= length()) throw std::out_of_range("snapshot index out of range");
+  if (t < first_ || t > last_) throw std::out_of_range("snapshot not retained in this graph store");
   std::shared_ptr<FeatSlot> hit, base;
   for (const auto& s : slots_) {
     if (s->t == t) hit = s;
@@ -533,12 +534,39 @@ FeatRef DeviceGraph::features(int32_t t, cudaStream_t stream) const {
 
 const DevSnapshot& DeviceGraph::snapshot(int32_t t) const {
   if (t < 0 || t >= length()) throw std::out_of_range("snapshot index out of range");
+  if (t < first_ || t > last_) throw std::out_of_range("snapshot not retained in this graph store");
   return snaps_[t];
 }
 
 const DevDelta& DeviceGraph::delta(int32_t t) const {
   if (!(t >= 1 && t < length())) throw std::invalid_argument("delta index out of range");
+  if (t < first_ || t > last_) throw std::out_of_range("delta not retained in this graph store");
   return deltas_[t];
+}
+
+void DeviceGraph::retain(int32_t t_first, int32_t t_last) {
+  if (!(t_first >= first_ && t_first <= t_last && t_last <= last_ && t_last < length()))
+    throw std::invalid_argument("retain: range outside the retained snapshots");
+  if (t_first > first_) {
+    // the features of t_first as a resident base version (leased: never evicted)
+    retained_base_ = features(t_first, stream_);
+    DGNN_CUDA(cudaStreamSynchronize(stream_));
+    for (const auto& sl : slots_) {
+      if (sl->t >= 0 && sl->t < t_first && sl.use_count() == 1) {  // versions before the range
+        sl->t = -1;
+        if (sl == slots_[0]) sl->buf.reset();  // snapshot 0's matrix is no base any more
+      }
+    }
+  }
+  for (int32_t t = 0; t < length(); ++t) {
+    if (t >= t_first && t <= t_last) continue;
+    snaps_[t] = DevSnapshot{};
+    if (t >= 1) deltas_[t] = DevDelta{};
+  }
+  first_ = t_first;
+  last_ = t_last;
+  DGNN_CUDA(cudaStreamSynchronize(stream_));
+  cuda::release_stream_blocks(stream_);
 }
 
 int64_t DeviceGraph::device_bytes() const {

@@ -19,6 +19,7 @@
 
 #include <cuda_runtime.h>
 
+#include <climits>
 #include <cstdint>
 #include <memory>
 #include <string>
@@ -134,6 +135,15 @@ class DeviceGraph {
   int64_t feature_materialisations() const { return materialisations_; }
 
   int64_t device_bytes() const;
+  // Keep only snapshots / deltas / feature versions [t_first, t_last]: a rank
+  // of the window-sharded trainer needs its window block plus the L + H
+  // overlap (replicate_overlap, ref inc/distsim.hpp:49-54). The features of
+  // t_first become a resident base version (so earlier patches can go); the
+  // snapshot indices and length() stay global, anything outside the range
+  // throws std::out_of_range.
+  void retain(int32_t t_first, int32_t t_last);
+  int32_t retained_first() const { return first_; }
+  int32_t retained_last() const { return last_; }
   // Frees the build-time key arrays of the last snapshot (2 x 8 B per edge);
   // a later add_delta rebuilds them from the snapshot's CSRs.
   void release_build_state();
@@ -160,6 +170,8 @@ class DeviceGraph {
   cuda::DevArray<uint64_t> curr_swapped_;           // last snapshot's (dst,src) keys, sorted
   // feature versions (the per-t patch is the second half of delta(t).compact)
   mutable std::vector<std::shared_ptr<FeatSlot>> slots_;  // slots_[0] = snapshot 0
+  std::shared_ptr<const FeatLease> retained_base_;          // features(first_) after retain()
+  int32_t first_ = 0, last_ = INT32_MAX;
   mutable uint64_t clock_ = 0;
   mutable int64_t materialisations_ = 0;
   int32_t max_slots_ = 0;

@@ -329,6 +329,48 @@ def test_sharded_epoch_emulated_ranks(ref, api, pair, workers):
     assert np.array_equal(inv, ref_inv)
 
 
+@pytest.mark.parametrize("workers", [2, 3])
+def test_sharded_ranks_on_retained_graphs(ref, api, workers):
+    """replicate_overlap (ref inc/distsim.hpp:49-54): every rank keeps only its
+    window block plus the L+H overlap of the graph store (DynamicGraph.retain)
+    and trains exactly as with the whole store — same losses, invocation log
+    and parameters as the reference's distributed epoch; snapshots outside a
+    rank's range are gone (std::out_of_range)."""
+    import torch
+    args = (300, 4.0, 8, 16, 0.05, 0.05)
+    g_ref = ref.RefGraph.synth(*args, seed=1)
+    cfg_r = ref.RunCfg(arch="tgcn", hidden=16, workers=workers, epochs=2, optimizer="sgd", lr=0.1)
+    r = g_ref.run(cfg_r)
+    graphs = [api.Synth(*args, seed=1).to_graph() for _ in range(workers)]
+    spans = [gm.retain_for_rank(workers, m, 8, 1, 1) for m, gm in enumerate(graphs)]
+    assert spans[0][0] == 0 and spans[-1][1] == 15 and spans[1][0] > 0
+    with pytest.raises(IndexError, match="not retained"):
+        graphs[1].in_csr(0)
+    ranks = [api.TrainSession(graphs[m], api.TrainConfig(arch="tgcn", hidden=16, workers=workers,
+                                                         optimizer="sgd", lr=0.1), rank=m)
+             for m in range(workers)]
+    P = ranks[0].num_params
+    losses = []
+    for _ in range(2):
+        nbs = [s.begin_epoch() for s in ranks]
+        for b in range(nbs[0]):
+            bufs = [torch.empty(P, device="cuda") for _ in ranks]
+            for s, buf in zip(ranks, bufs):
+                s.local_grads(b, buf)
+            total = torch.stack(bufs).sum(0)
+            for s in ranks:
+                assert s.apply(total.clone())
+        for s in ranks:
+            s.end_epoch()
+            losses.append(s.losses())
+    assert nrel(np.concatenate(losses), r.losses) < 1e-4
+    for s in ranks:
+        assert nrel(s.params(), r.params) < 1e-5
+    inv = np.concatenate([s.invocations() for s in ranks])
+    ref_inv = np.concatenate([r.invocations[r.invocations[:, 0] == m][:, 1:] for m in range(workers)])
+    assert np.array_equal(inv, ref_inv)
+
+
 @pytest.mark.parametrize("arch", ARCHS)
 @pytest.mark.parametrize("gate_tape", [False, True])
 def test_sample_grads_tensor_core_cells(ref, api, pair, monkeypatch, arch, gate_tape):
