@@ -73,17 +73,24 @@ __global__ void k_unmark_present(int64_t nd, const uint64_t* __restrict__ d, int
   }
 }
 
-__global__ void k_hist_hi(int64_t n, const uint64_t* __restrict__ keys,
-                          unsigned long long* __restrict__ counts) {
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    atomicAdd(counts + (keys[i] >> 32), 1ull);
-}
-
 __global__ void k_low32(int64_t n, const uint64_t* __restrict__ keys, int32_t* __restrict__ out) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
     out[i] = static_cast<int32_t>(keys[i] & 0xffffffffu);
+}
+
+// CSR of keys sorted by their high half in one pass: idx[i] = low half, and
+// each row boundary writes the row pointers of the rows it closes (every
+// ptr[v], v in [0, n], written exactly once; no atomics, no scan).
+__global__ void k_csr_from_sorted(int64_t E, int32_t n, const uint64_t* __restrict__ keys,
+                                  int64_t* __restrict__ ptr, int32_t* __restrict__ idx) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i <= E;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t cur = i < E ? static_cast<int64_t>(keys[i] >> 32) : n;
+    const int64_t prev = i > 0 ? static_cast<int64_t>(keys[i - 1] >> 32) : -1;
+    for (int64_t v = prev + 1; v <= cur; ++v) ptr[v] = i;
+    if (i < E) idx[i] = static_cast<int32_t>(keys[i] & 0xffffffffu);
+  }
 }
 
 __global__ void k_swap_halves(int64_t n, const uint64_t* __restrict__ in, uint64_t* __restrict__ out) {
@@ -759,19 +766,12 @@ DevSnapshot csr_from_keys(const uint64_t* keys, int64_t E, int32_t n, cudaStream
   DevSnapshot s;
   s.num_edges = E;
   // out-CSR: keys already sorted by (src, dst)
-  DevArray<unsigned long long> cnt(n + 1, st);
-  cnt.zero(st);
   s.out_ptr = DevArray<int64_t>(n + 1, st);
   s.out_dst = DevArray<int32_t>(E, st);
-  if (E > 0) {
-    DGNN_LAUNCH(k_hist_hi, grid_for(E), kT, 0, st, E, keys, cnt.get());
-    DGNN_LAUNCH(k_low32, grid_for(E), kT, 0, st, E, keys, s.out_dst.get());
-  }
-  cub.exclusive_sum(reinterpret_cast<const int64_t*>(cnt.get()), s.out_ptr.get(), n + 1);
+  DGNN_LAUNCH(k_csr_from_sorted, grid_for(E + 1), kT, 0, st, E, n, keys, s.out_ptr.get(), s.out_dst.get());
   // in-CSR: sort by (dst, src)
   s.in_ptr = DevArray<int64_t>(n + 1, st);
   s.in_src = DevArray<int32_t>(E, st);
-  cnt.zero(st);
   if (E > 0) {
     DevArray<uint64_t> sw_sorted;
     const uint64_t* swk = swapped_sorted;
@@ -782,11 +782,11 @@ DevSnapshot csr_from_keys(const uint64_t* keys, int64_t E, int32_t n, cudaStream
       cub.sort(sw.get(), sw_sorted.get(), E);
       swk = sw_sorted.get();
     }
-    DGNN_LAUNCH(k_hist_hi, grid_for(E), kT, 0, st, E, swk, cnt.get());
-    DGNN_LAUNCH(k_low32, grid_for(E), kT, 0, st, E, swk, s.in_src.get());
+    DGNN_LAUNCH(k_csr_from_sorted, grid_for(E + 1), kT, 0, st, E, n, swk, s.in_ptr.get(), s.in_src.get());
     if (swapped_out && swapped_sorted == nullptr) *swapped_out = std::move(sw_sorted);
+  } else {
+    DGNN_LAUNCH(k_csr_from_sorted, 1, kT, 0, st, int64_t{0}, n, static_cast<const uint64_t*>(nullptr), s.in_ptr.get(), s.in_src.get());
   }
-  cub.exclusive_sum(reinterpret_cast<const int64_t*>(cnt.get()), s.in_ptr.get(), n + 1);
   return s;
 }
 
