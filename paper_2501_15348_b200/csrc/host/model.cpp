@@ -452,8 +452,10 @@ Buf linear_forward(DgnnModel& m, const LinearSlot& lin, NodeId n, const float* x
   Buf y = new_buf(static_cast<size_t>(n) * lin.out, st);
   ProfScope ps(kProfOther, st, 4.0 * n * (lin.in + lin.out), 2.0 * n * lin.in * lin.out);
   if (lin.umma) {
+    // split accumulators (RowGemmArgs::split_acc): the head's outputs are the
+    // predictions the MAE sign reads
     cuda::umma_gemm_store2(n, lin.in, x, lin.Bf.get(), lin.out, 0, y->get(), nullptr, st,
-                           m.params() + lin.off_b, false, 0, relu);
+                           m.params() + lin.off_b, false, 0, relu, true);
   } else {
     cuda::gemm_nn(n, lin.in, 0, lin.out, 0, x, nullptr, m.params() + lin.off_w, lin.out,
                   m.params() + lin.off_b, relu, false, y->get(), nullptr, st);

@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
     const uint32_t idesc3 = gs ? idesc_tf32(kTileM, 3 * gs) : idesc;
     const uint32_t boffH = static_cast<uint32_t>(gs / 8) * 128u;  // B rows [H, 4H)
     uint32_t g = 0, it = 0;
-    const bool split = kEpiCell<EPI> && p.split_acc;
+    const bool split = (kEpiCell<EPI> || EPI == kEpiStore2) && p.split_acc;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const uint32_t b = split ? 0u : (it & 1u);
       mbar_wait(&tempty[b], (split ? (it & 1u) : ((it >> 1) & 1u)) ^ 1u);
@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
     // ---------------- epilogue
     const int q = warp & 3, half = (warp - kEpiWarp0) >> 2;
     uint32_t it = 0;
-    const bool split = kEpiCell<EPI> && p.split_acc;
+    const bool split = (kEpiCell<EPI> || EPI == kEpiStore2) && p.split_acc;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const uint32_t b = split ? 0u : (it & 1u);
       const int64_t row0 = static_cast<int64_t>(tile) * kTileM + q * 32;  // this warp's 32 rows
@@ -622,6 +622,13 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
           float a[16];
           tmem_ld16(trow + cb, a);
           tmem_wait_ld();
+          if (split) {
+            float t2[16];
+            tmem_ld16(trow + 256 + cb, t2);
+            tmem_wait_ld();
+#pragma unroll
+            for (int u = 0; u < 16; ++u) a[u] += t2[u];
+          }
           if (cb < p.n1) {
             if (p.bias != nullptr) {
 #pragma unroll
@@ -651,6 +658,13 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
           float a[8];
           tmem_ld8(trow + cb, a);
           tmem_wait_ld();
+          if (split) {
+            float t2[8];
+            tmem_ld8(trow + 256 + cb, t2);
+            tmem_wait_ld();
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a[u] += t2[u];
+          }
           if (row < p.M) {
             if (vec) {
 #pragma unroll
@@ -1069,9 +1083,10 @@ void umma_cell_backward_recompute(bool lstm, int n, int in, int H, const float* 
 
 void umma_gemm_store2(int n, int K, const float* A, const float* Bimg, int n1, int n2, float* C1,
                       float* C2, cudaStream_t stream, const float* bias, bool accumulate, int gru_h,
-                      bool relu) {
+                      bool relu, bool split_acc) {
   if (n1 > 256) throw std::invalid_argument("umma_gemm_store2: at most 256 bias columns");
   RowGemmArgs a{};
+  a.split_acc = split_acc && (umma_split_acc() & 1);
   a.scalar_a = K % 4 != 0;
   a.bias = bias;
   a.relu = relu ? 1 : 0;

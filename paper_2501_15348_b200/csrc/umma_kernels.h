@@ -45,7 +45,8 @@ void umma_cell_backward_recompute(bool lstm, int n, int in, int H, const float* 
 // (both need 16-column blocks).
 void umma_gemm_store2(int n, int K, const float* A, const float* Bimg, int n1, int n2, float* C1,
                       float* C2, cudaStream_t stream, const float* bias = nullptr,
-                      bool accumulate = false, int gru_h = 0, bool relu = false);
+                      bool accumulate = false, int gru_h = 0, bool relu = false,
+                      bool split_acc = false);
 
 // dW ((in+H) x 4H) += [X|Hm]^T G, db (nb) += colsum(G[:, :nb]); deterministic.
 // Hm == nullptr: a plain linear layer's gradient, dW (in x gw) += X^T G with
