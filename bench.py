@@ -240,6 +240,7 @@ def main():
     ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-tf32-peak", action="store_true", help="skip the in-run TF32 peak measurement")
     ap.add_argument("--prof-in-timed", type=int, default=-1,
                     help="1: per-kernel-class CUDA-event profiling inside the timed region (the "
                          "roofline's launch times are those of the timed steps); 0: the timed steps "
@@ -273,11 +274,12 @@ def main():
         if world > 1:
             dist.barrier()
 
+    tf32_peak = None
     try:
-        tf32_peak = measure_tf32_peak()
+        if not args.no_tf32_peak:
+            tf32_peak = measure_tf32_peak()
     except Exception as e:  # noqa: BLE001 — report, do not fail the bench
         log(f"tf32 peak measurement failed: {e}")
-        tf32_peak = None
     torch.cuda.empty_cache()
     t0 = time.perf_counter()
     synth = api.Synth(wl["n"], wl["deg"], wl["dim"], wl["T"], wl["edge"], wl["feat"], seed=1)
