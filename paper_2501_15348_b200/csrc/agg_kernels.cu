@@ -782,7 +782,14 @@ void agg_delta(int kind, int n_rows, int w, const int32_t* rows, const int32_t* 
   if (u_env == 1 || u_env == 2) U = std::min(U, u_env);
   if (!pipe_off && (kind == kAggSum || kind == kAggMean) && vec == 4 && aligned && w <= 128 * U) {
     const int g = pick_group(w, 4 * U);
-    const int grid = rows_grid(n_rows, g);
+    // DGNN_DELTA_GRID: CTAs per SM of the grid-stride launch (experiments)
+    static const int per_sm = [] {
+      const char* e = std::getenv("DGNN_DELTA_GRID");
+      return e ? std::atoi(e) : 0;
+    }();
+    const int grid = per_sm > 0 ? cuda::wave_grid(static_cast<int64_t>(n_rows) * kThreads / ((kThreads / 32) * (32 / g)),
+                                                  kThreads, per_sm)
+                                : rows_grid(n_rows, g);
     const float* cp = compact;
     const float* cc = compact ? compact + n_changed * w : nullptr;
 #define DGNN_DELTA_LAUNCH(UU, MM)                                                                    \
