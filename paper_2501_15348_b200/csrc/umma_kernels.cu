@@ -514,8 +514,11 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
       const int cb0 = gsplit ? p.H : 0, cb1 = gsplit ? 2 * p.H : p.H, cb2 = gsplit ? 0 : 2 * p.H;
       if (EPI == kEpiLstmBwd || EPI == kEpiGruBwd) {
         const int H = p.H;
-        const int U = H / 2;
-        for (int j0 = half * U; j0 < (half + 1) * U; j0 += 16) {
+        // hidden units of this warp: one half each (H >= 32), or all of them
+        // in the first half (H = 16: one 16-column block)
+        const int jb = H >= 32 ? half * (H / 2) : (half ? H : 0);
+        const int je = H >= 32 ? jb + H / 2 : H;
+        for (int j0 = jb; j0 < je; j0 += 16) {
           float a0[16], a1[16], a2[16], a3[16];
           float cv[16];  // out: dc_prev (LSTM) / dh_skip (GRU)
           ld_gates(cb0 + j0, cb1 + j0, cb2 + j0, 3 * H + j0, a0, a1, a2, a3);
@@ -571,8 +574,11 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
         }
       } else if (EPI == kEpiLstm || EPI == kEpiGru) {
         const int H = p.H;
-        const int U = H / 2;
-        for (int j0 = half * U; j0 < (half + 1) * U; j0 += 16) {
+        // hidden units of this warp: one half each (H >= 32), or all of them
+        // in the first half (H = 16: one 16-column block)
+        const int jb = H >= 32 ? half * (H / 2) : (half ? H : 0);
+        const int je = H >= 32 ? jb + H / 2 : H;
+        for (int j0 = jb; j0 < je; j0 += 16) {
           float a0[16], a1[16], a2[16], a3[16];
           // state row prefetch overlaps the TMEM reads
           float sv[16];
@@ -985,8 +991,10 @@ bool umma_enabled() {
 
 bool umma_cell_supported(int in, int H) {
   // in + H <= 192: the weight-gradient kernel's raw [X | Hm] staging slot;
-  // any in >= 1 (rows that are not 16 B multiples are copied by element)
-  return umma_enabled() && (H == 32 || H == 64) && in >= 1 && in + H <= 192;
+  // any in >= 1 (rows that are not 16 B multiples are copied by element);
+  // H = 16 runs its 4H = 64 gate columns in the first epilogue half and pads
+  // the weight gradient's row tile to 128
+  return umma_enabled() && (H == 16 || H == 32 || H == 64) && in >= 1 && in + H <= 192;
 }
 
 int umma_npad(int N) { return N <= 64 ? 64 : (N <= 128 ? 128 : (N <= 192 ? 192 : 256)); }
@@ -1130,7 +1138,8 @@ int wgrad_grid(int64_t n) {
 int64_t umma_wgrad_workspace(int64_t n, int in, int H) {
   const int need = round_up(in + H + 1, 16);
   const int npad = need <= 144 ? 144 : (need <= 208 ? 208 : 256);
-  return static_cast<int64_t>(wgrad_grid(n)) * 4 * H * npad;
+  const int mg = H == 64 ? 256 : 128;  // the kernel's row tile (4H padded up to 128)
+  return static_cast<int64_t>(wgrad_grid(n)) * mg * npad;
 }
 
 void umma_wgrad(int n, int in, int H, const float* G, const float* X, const float* Hm, float* dW,
@@ -1170,7 +1179,7 @@ void umma_wgrad(int n, int in, int H, const float* G, const float* X, const floa
     else go(std::integral_constant<int, 128>{}, std::integral_constant<int, 256>{});
   }
   const int64_t total = static_cast<int64_t>(gw) * (in + H + 1);
-  DGNN_LAUNCH(k_wgrad_reduce, wave_grid(total, 256, 4), 256, 0, stream, grid, 4 * H, npad, in + H,
+  DGNN_LAUNCH(k_wgrad_reduce, wave_grid(total, 256, 4), 256, 0, stream, grid, H == 64 ? 256 : 128, npad, in + H,
               Hm ? in + H : in, nb, gw, ws, dW, db);
 }
 
