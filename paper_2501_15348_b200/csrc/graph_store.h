@@ -140,7 +140,8 @@ class DeviceGraph {
   // overlap (replicate_overlap, ref inc/distsim.hpp:49-54). The features of
   // t_first become a resident base version (so earlier patches can go); the
   // snapshot indices and length() stay global, anything outside the range
-  // throws std::out_of_range.
+  // throws std::out_of_range. Call it before sessions read the graph (it
+  // frees device arrays without waiting for other streams' readers).
   void retain(int32_t t_first, int32_t t_last);
   int32_t retained_first() const { return first_; }
   int32_t retained_last() const { return last_; }

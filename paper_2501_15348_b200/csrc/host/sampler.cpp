@@ -22,7 +22,7 @@ namespace dgnn {
 namespace {
 
 constexpr int kDepth = 24;
-constexpr int kMaxSamples = 400000;
+constexpr int kMaxSamples = 100000;
 void* g_frames[kMaxSamples][kDepth];
 int g_depth[kMaxSamples];
 std::atomic<int> g_n{0};
