@@ -446,8 +446,39 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
       const uint32_t trow = tmem + b * 256 + (static_cast<uint32_t>(q * 32) << 16);
       // the four gate blocks of hidden units [j0, j0 + 16): hi*hi sums (+ the
       // correction sums when split)
+      // H = 8: 8-column gate blocks (the first 8 entries of each array are
+      // live, the rest are never stored)
+      // (cell epilogues only: store2 leaves p.H unset)
+      const bool narrow = kEpiCell<EPI> && NPAD == 64 && p.H < 16;  // 4H = 32: only the 64-column tile
+      auto ld8_into = [&](uint32_t addr, float (&v)[16]) {
+        float t[8];
+        tmem_ld8(addr, t);
+        tmem_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = t[u];
+#pragma unroll
+        for (int u = 8; u < 16; ++u) v[u] = 0.f;
+      };
       auto ld_gates = [&](int c0, int c1, int c2, int c3, float (&a0)[16], float (&a1)[16],
                           float (&a2)[16], float (&a3)[16]) {
+        if (narrow) {
+          ld8_into(trow + c0, a0);
+          ld8_into(trow + c1, a1);
+          ld8_into(trow + c2, a2);
+          ld8_into(trow + c3, a3);
+          if (split) {
+            float t[16];
+            ld8_into(trow + 256 + c0, t);
+            for (int u = 0; u < 8; ++u) a0[u] += t[u];
+            ld8_into(trow + 256 + c1, t);
+            for (int u = 0; u < 8; ++u) a1[u] += t[u];
+            ld8_into(trow + 256 + c2, t);
+            for (int u = 0; u < 8; ++u) a2[u] += t[u];
+            ld8_into(trow + 256 + c3, t);
+            for (int u = 0; u < 8; ++u) a3[u] += t[u];
+          }
+          return;
+        }
         tmem_ld16(trow + c0, a0);
         tmem_ld16(trow + c1, a1);
         tmem_ld16(trow + c2, a2);
@@ -481,6 +512,7 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
       // bank-conflict free.
       float* wb = reinterpret_cast<float*>(smem + S::kOut) + (warp - kEpiWarp0) * (32 * 16);
       auto stage_store = [&](const float (&v)[16], float* base, int64_t stride, int col0) {
+        const int ncols = narrow ? 8 : 16;
 #pragma unroll
         for (int u = 0; u < 16; u += 4)
           *reinterpret_cast<float4*>(wb + lane * 16 + (((u >> 2) ^ ((lane >> 1) & 3)) << 2)) =
@@ -491,7 +523,7 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
         for (int bb = 0; bb < 4; ++bb) {
           const int rl = bb * 8 + i;
           const float4 x = *reinterpret_cast<const float4*>(wb + rl * 16 + ((k ^ ((rl >> 1) & 3)) << 2));
-          if (row0 + rl < p.M)
+          if (row0 + rl < p.M && k * 4 < ncols)
             *reinterpret_cast<float4*>(base + (row0 + rl) * stride + col0 + k * 4) = x;
         }
         __syncwarp();
@@ -501,7 +533,8 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
           const float* sp = base + row * p.H + j0;
 #pragma unroll
           for (int u = 0; u < 16; u += 4) {
-            const float4 x = __ldg(reinterpret_cast<const float4*>(sp + u));
+            float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (!narrow || u < 8) x = __ldg(reinterpret_cast<const float4*>(sp + u));
             v[u] = x.x; v[u + 1] = x.y; v[u + 2] = x.z; v[u + 3] = x.w;
           }
         } else {
@@ -516,8 +549,9 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
         const int H = p.H;
         // hidden units of this warp: one half each (H >= 32), or all of them
         // in the first half (H = 16: one 16-column block)
-        const int jb = H >= 32 ? half * (H / 2) : (half ? H : 0);
-        const int je = H >= 32 ? jb + H / 2 : H;
+        const bool small_h = NPAD == 64 && H < 32;  // compile-time false on the wide tiles
+        const int jb = !small_h ? half * (H / 2) : (half ? H : 0);
+        const int je = !small_h ? jb + H / 2 : H;
         for (int j0 = jb; j0 < je; j0 += 16) {
           float a0[16], a1[16], a2[16], a3[16];
           float cv[16];  // out: dc_prev (LSTM) / dh_skip (GRU)
@@ -529,7 +563,7 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
 #pragma unroll
           for (int u4 = 0; u4 < 16; u4 += 4) {
             float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f), d4 = s4, c4 = s4;
-            if (row < p.M) {
+            if (row < p.M && (!narrow || u4 < 8)) {
               s4 = __ldg(reinterpret_cast<const float4*>(sp + u4));
               d4 = __ldg(reinterpret_cast<const float4*>(dp + u4));
               if (EPI == kEpiLstmBwd && cp) c4 = __ldg(reinterpret_cast<const float4*>(cp + u4));
@@ -576,8 +610,9 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_row_gemm(RowGemmArgs p) {
         const int H = p.H;
         // hidden units of this warp: one half each (H >= 32), or all of them
         // in the first half (H = 16: one 16-column block)
-        const int jb = H >= 32 ? half * (H / 2) : (half ? H : 0);
-        const int je = H >= 32 ? jb + H / 2 : H;
+        const bool small_h = NPAD == 64 && H < 32;  // compile-time false on the wide tiles
+        const int jb = !small_h ? half * (H / 2) : (half ? H : 0);
+        const int je = !small_h ? jb + H / 2 : H;
         for (int j0 = jb; j0 < je; j0 += 16) {
           float a0[16], a1[16], a2[16], a3[16];
           // state row prefetch overlaps the TMEM reads
@@ -993,8 +1028,8 @@ bool umma_cell_supported(int in, int H) {
   // in + H <= 192: the weight-gradient kernel's raw [X | Hm] staging slot;
   // any in >= 1 (rows that are not 16 B multiples are copied by element);
   // H = 16 runs its 4H = 64 gate columns in the first epilogue half and pads
-  // the weight gradient's row tile to 128
-  return umma_enabled() && (H == 16 || H == 32 || H == 64) && in >= 1 && in + H <= 192;
+  // the weight gradient's row tile to 128; H = 8 works in 8-column blocks
+  return umma_enabled() && (H == 8 || H == 16 || H == 32 || H == 64) && in >= 1 && in + H <= 192;
 }
 
 int umma_npad(int N) { return N <= 64 ? 64 : (N <= 128 ? 128 : (N <= 192 ? 192 : 256)); }
