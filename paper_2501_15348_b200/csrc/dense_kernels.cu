@@ -5,6 +5,8 @@
 // update and the tape write are fused into the GEMM epilogue (no pre-activation
 // round trip through HBM). Weight gradients use a fixed-order split over rows
 // (partials + ordered reduction) so every run is bit-reproducible.
+#include <algorithm>
+
 #include "common.cuh"
 #include "dense_kernels.h"
 
@@ -621,6 +623,63 @@ void pack_cell(bool lstm, int in, int H, const float* flat, float* W, float* bia
   const int64_t total = static_cast<int64_t>(in + H) * 4 * H + 4 * H;
   DGNN_LAUNCH(k_pack_cell, wave_grid(total, 256, 4), 256, 0, stream, lstm ? 1 : 0, in, H, flat, W,
               bias);
+}
+
+namespace {
+// all cells of a model in one launch (blockIdx.y = cell)
+__global__ void k_zero_cells(const CellGradDesc* __restrict__ cells, int n) {
+  const CellGradDesc c = cells[blockIdx.y];
+  const int64_t nw = static_cast<int64_t>(c.in + c.H) * 4 * c.H, nb = 4 * c.H;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nw + nb;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (i < nw) c.dW[i] = 0.f;
+    else c.db[i - nw] = 0.f;
+  }
+  (void)n;
+}
+
+__global__ void k_unpack_cells(const CellGradDesc* __restrict__ cells, float* __restrict__ flat) {
+  const CellGradDesc c = cells[blockIdx.y];
+  const int lstm = c.lstm, in = c.in, H = c.H;
+  const int gates = lstm ? 4 : 3;
+  const int NC = 4 * H;
+  const int64_t per_gate = static_cast<int64_t>(in) * H + static_cast<int64_t>(H) * H + H;
+  const int64_t total = per_gate * gates;
+  float* out = flat + c.offset;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int g = static_cast<int>(i / per_gate);
+    int64_t o = i - g * per_gate;
+    float v;
+    if (o < static_cast<int64_t>(in) * H) {
+      const int k = static_cast<int>(o / H), j = static_cast<int>(o % H);
+      v = c.dW[static_cast<int64_t>(k) * NC + g * H + j];
+    } else if ((o -= static_cast<int64_t>(in) * H) < static_cast<int64_t>(H) * H) {
+      const int k = static_cast<int>(o / H), j = static_cast<int>(o % H);
+      const int q = lstm ? g : (g == 2 ? 3 : g);
+      v = c.dW[static_cast<int64_t>(in + k) * NC + q * H + j];
+    } else {
+      const int j = static_cast<int>(o - static_cast<int64_t>(H) * H);
+      v = c.db[g * H + j];
+    }
+    out[i] += v;
+  }
+}
+}  // namespace
+
+void zero_cell_grads(const CellGradDesc* cells_dev, int n, int64_t max_elems, cudaStream_t stream) {
+  if (n <= 0) return;
+  const dim3 grid(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((max_elems + 255) / 256, 256))),
+                  static_cast<unsigned>(n));
+  DGNN_LAUNCH(k_zero_cells, grid, 256, 0, stream, cells_dev, n);
+}
+
+void unpack_cell_grads(const CellGradDesc* cells_dev, int n, int64_t max_elems, float* flat_grad,
+                       cudaStream_t stream) {
+  if (n <= 0) return;
+  const dim3 grid(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((max_elems + 255) / 256, 256))),
+                  static_cast<unsigned>(n));
+  DGNN_LAUNCH(k_unpack_cells, grid, 256, 0, stream, cells_dev, flat_grad);
 }
 
 void unpack_cell_grad(bool lstm, int in, int H, const float* dW, const float* db,

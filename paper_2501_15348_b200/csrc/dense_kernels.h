@@ -71,6 +71,18 @@ void adam_step(int64_t n, float* p, float* m, float* v, const float* g, float gs
 void pack_cell(bool lstm, int in, int H, const float* flat, float* W, float* bias,
                cudaStream_t stream);
 // flat_grad += unpack(dW, db).
+// Per-cell weight / bias gradient accumulators of a model, for the batched
+// zeroing and unpacking below (one launch per sample for all cells).
+struct CellGradDesc {
+  float* dW;
+  float* db;
+  int lstm, in, H;
+  int64_t offset;  // the cell's first parameter in the flat buffer
+};
+void zero_cell_grads(const CellGradDesc* cells_dev, int n, int64_t max_elems, cudaStream_t stream);
+void unpack_cell_grads(const CellGradDesc* cells_dev, int n, int64_t max_elems, float* flat_grad,
+                       cudaStream_t stream);
+
 void unpack_cell_grad(bool lstm, int in, int H, const float* dW, const float* db,
                       float* flat_grad, cudaStream_t stream);
 

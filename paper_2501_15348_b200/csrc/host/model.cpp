@@ -272,6 +272,19 @@ std::unique_ptr<DgnnModel> DgnnModel::create(const ModelConfig& cfg, cudaStream_
   set_linear_umma(m->head_, stream);
   m->num_params_ = off;
   m->params_ = cuda::DevArray<float>(off, stream);
+  {
+    std::vector<cuda::CellGradDesc> descs;
+    for (auto* cells : {&m->enc_, &m->dec_, &m->rnn_})
+      for (auto& c : *cells) {
+        descs.push_back({c.dW.get(), c.db.get(), c.lstm ? 1 : 0, c.in, c.H, c.offset});
+        m->cell_grad_max_ = std::max<int64_t>(m->cell_grad_max_, static_cast<int64_t>(c.in + c.H + 1) * 4 * c.H);
+      }
+    m->n_cell_grads_ = static_cast<int>(descs.size());
+    m->cell_grads_ = cuda::DevArray<cuda::CellGradDesc>(std::max<size_t>(descs.size(), 1), stream);
+    if (!descs.empty())
+      DGNN_CUDA(cudaMemcpyAsync(m->cell_grads_.get(), descs.data(), sizeof(cuda::CellGradDesc) * descs.size(),
+                                cudaMemcpyHostToDevice, stream));
+  }
   m->unflatten_params(m->init_);
   return m;
 }
@@ -766,17 +779,6 @@ StepGrads cell_step_backward(CellSlot& c, const CellTape& tape, const float* X, 
   return out;
 }
 
-void zero_cell_accumulators(std::vector<CellSlot>& cells, cudaStream_t st) {
-  for (auto& c : cells) {
-    c.dW.zero(st);
-    c.db.zero(st);
-  }
-}
-
-void flush_cell_grads(std::vector<CellSlot>& cells, float* flat, cudaStream_t st) {
-  for (auto& c : cells) cuda::unpack_cell_grad(c.lstm, c.in, c.H, c.dW.get(), c.db.get(), flat + c.offset, st);
-}
-
 void head_backward(DgnnModel& model, NodeId n, const float* h_top, const Buf& dpred, Buf& dh,
                    Grads& g, cudaStream_t st) {
   linear_param_grads(model, model.head_, n, h_top, dpred->get(), g, st);
@@ -972,9 +974,7 @@ void model_backward(DgnnModel& model, const SeqSample& sample, const ForwardArti
   for (const LinearSlot& gl : model.gcn_)
     if (gl.umma_wgrad) ws_n = std::max(ws_n, cuda::umma_wgrad_workspace(n, gl.in, linear_wgrad_h(gl)));
   cuda::DevArray<float> ws(ws_n, stream);
-  zero_cell_accumulators(model.enc_, stream);
-  zero_cell_accumulators(model.dec_, stream);
-  zero_cell_accumulators(model.rnn_, stream);
+  cuda::zero_cell_grads(model.cell_grad_table(), model.cell_grad_count(), model.cell_grad_max_elems(), stream);
   if (is_stacked(model.cfg_.arch)) {
     Grads g{grad, ws.get()};
     stacked_backward(model, sample, fwd, dpred, g, stream);
@@ -985,9 +985,8 @@ void model_backward(DgnnModel& model, const SeqSample& sample, const ForwardArti
     Grads g[2] = {{grad, ws.get()}, {grad, lanes.two ? ws1.get() : ws.get()}};
     integrated_backward(model, sample, fwd, dpred, g, lanes);  // ends joined
   }
-  flush_cell_grads(model.enc_, grad, stream);
-  flush_cell_grads(model.dec_, grad, stream);
-  flush_cell_grads(model.rnn_, grad, stream);
+  cuda::unpack_cell_grads(model.cell_grad_table(), model.cell_grad_count(), model.cell_grad_max_elems(), grad,
+                          stream);
 }
 
 std::vector<Buf> seed_loss(const SeqSample& sample, const ForwardArtifacts& fwd, int feature_dim,

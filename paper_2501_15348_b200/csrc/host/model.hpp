@@ -123,6 +123,11 @@ class DgnnModel {
 
   float* params() { return params_.get(); }
   void refresh_packed();  // after any parameter change
+  // every cell's gradient accumulators (enc, dec, rnn) for one-launch
+  // zeroing / unpacking per sample
+  const cuda::CellGradDesc* cell_grad_table() const { return cell_grads_.get(); }
+  int cell_grad_count() const { return n_cell_grads_; }
+  int64_t cell_grad_max_elems() const { return cell_grad_max_; }
   void set_gate_recompute(bool on);
 
   ModelConfig cfg_;
@@ -136,6 +141,9 @@ class DgnnModel {
   std::vector<double> init_;
   int64_t num_params_ = 0;
   cuda::DevArray<float> params_;
+  cuda::DevArray<cuda::CellGradDesc> cell_grads_;
+  int n_cell_grads_ = 0;
+  int64_t cell_grad_max_ = 0;
 };
 
 // One (batch, window) training sample (ref inc/model.hpp:65-73) over
