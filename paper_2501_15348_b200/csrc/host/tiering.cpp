@@ -2,6 +2,7 @@
 #include "tiering.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <utility>
 
 namespace dgnn {
@@ -71,8 +72,17 @@ Shape shape_of(const AggResult& r) {
 
 }  // namespace
 
+namespace {
+// device bytes of spills in flight before the host waits: max(budget, 4 GB),
+// or DGNN_TIER_INFLIGHT_MB (tests force the backpressure path with it)
+int64_t inflight_cap(int64_t budget) {
+  if (const char* e = std::getenv("DGNN_TIER_INFLIGHT_MB")) return std::max<int64_t>(1, std::atoll(e)) << 20;
+  return std::max<int64_t>(budget, int64_t{4} << 30);
+}
+}  // namespace
+
 HbmTier::HbmTier(int64_t budget_bytes, cudaStream_t compute)
-    : budget_(budget_bytes), retiring_cap_(std::max<int64_t>(budget_bytes, int64_t{4} << 30)), compute_(compute) {
+    : budget_(budget_bytes), retiring_cap_(inflight_cap(budget_bytes)), compute_(compute) {
   DGNN_CUDA(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
   DGNN_CUDA(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
 }

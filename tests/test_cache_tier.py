@@ -62,3 +62,39 @@ def test_spilling_cache_matches_reference(ref, arch, aggr):
             "scratch_calls", "incremental_calls", "fallbacks"]
     st = s1.stats()
     assert [st[k] for k in keys] == r.stats[0, :9].tolist()
+
+
+def test_spill_backpressure_keeps_results(ref):
+    """The in-flight spill cap (HbmTier backpressure): with it forced to 1 MB
+    every spill waits for the previous ones' device -> host copies, and the
+    run stays bitwise equal to the unbudgeted one (each variant in its own
+    process: the cap is read when the tier is created)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    prog = r"""
+import json, sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np
+from paper_2501_15348_b200 import api
+g = api.Synth(300, 4, 8, 14, 0.05, 0.05, seed=7).to_graph()
+budget = int(sys.argv[2])
+s = api.TrainSession(g, api.TrainConfig(arch="tgcn", hidden=16, cache_frac=1.0, hbm_cache_budget_bytes=budget))
+l = np.concatenate([s.run_epoch()["sample_losses"] for _ in range(2)])
+print(json.dumps({"losses": l.tolist(), "params": s.params().tolist(), "tier": s.tier_stats()}))
+"""
+    def run(budget, cap_mb):
+        env = dict(os.environ)
+        if cap_mb:
+            env["DGNN_TIER_INFLIGHT_MB"] = str(cap_mb)
+        r = subprocess.run([sys.executable, "-c", prog, root, str(budget)], capture_output=True, text=True,
+                           env=env, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    base = run(0, None)
+    tight = run(2 * 300 * 8 * 4, 1)
+    assert tight["tier"]["spills"] > 0 and tight["tier"]["refills"] > 0
+    assert tight["losses"] == base["losses"]
+    assert tight["params"] == base["params"]
